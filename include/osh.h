@@ -1,0 +1,168 @@
+/*
+ * osh.h — C ABI of the B200-native Canzona optimizer step ("optishard" drop-in).
+ *
+ * This is the boundary between host code that speaks the reference's C++
+ * interface (include/optishard/*.hpp, namespace optishard) and the sm_100a
+ * CUDA library libosh.so. Plain C types only: no C++ or torch types cross it.
+ * Every entry point returns an osh_status; on failure osh_last_error() holds
+ * a thread-local message. No exception crosses the ABI.
+ *
+ * Reference interfaces replaced (paths relative to the reference checkout):
+ *   status codes          proj/include/optishard/common.hpp:19-60 (exception taxonomy)
+ *   osh_layout_build      workload.hpp:164-194   build_buffer_layout
+ *   osh_param_cost        cost.hpp:81-90         param_cost
+ *   osh_plan_dp           dp_partition.hpp:149-293 equal_chunk / atomic_ownership / alpha_balanced
+ *   osh_plan_validate     dp_partition.hpp:297-371 validate_plan
+ *   osh_param_owner       dp_partition.hpp:374-395 param_owner
+ *   osh_plan_tp           tp_schedule.hpp:90-143 build_micro_groups
+ *   osh_plan_*_serialize  serialize.hpp:252-366  serialize_dp_plan / serialize_tp_plan
+ *   osh_muon_apply        verify.hpp:138-147     muon_apply (one tensor, host buffers)
+ *   osh_newton_schulz     verify.hpp:118-134     newton_schulz_orthogonalize
+ *   osh_ctx_* / osh_step  verify.hpp:225-322     run_partitioned, executed for real:
+ *                          variable-size reduce-scatter -> owner Muon -> all-gather
+ */
+#ifndef OSH_H_
+#define OSH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSH_ABI_VERSION 1
+
+typedef enum osh_status {
+  OSH_OK = 0,
+  OSH_ERR_CONFIG = 1,        /* optishard::ConfigError */
+  OSH_ERR_LAYOUT = 2,        /* optishard::LayoutError */
+  OSH_ERR_SHARD = 3,         /* optishard::ShardError */
+  OSH_ERR_UNSUPPORTED = 4,   /* optishard::UnsupportedError */
+  OSH_ERR_PLAN = 5,          /* optishard::PlanError */
+  OSH_ERR_UNSCHEDULABLE = 6, /* optishard::UnschedulableError */
+  OSH_ERR_FORMAT = 7,        /* optishard::FormatError */
+  OSH_ERR_CUDA = 16,
+  OSH_ERR_NCCL = 17,
+  OSH_ERR_OOM = 18,
+  OSH_ERR_ARG = 19
+} osh_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* osh_last_error(void);
+int osh_abi_version(void);
+
+/* ------------------------------------------------------------ workload
+ * One parameter tensor (ParamSpec, workload.hpp:31-44). ndim is 1 or 2;
+ * tp_split: 0 none, 1 column, 2 row (TpSplit, workload.hpp:21). */
+typedef struct osh_param_desc {
+  int32_t id;
+  int32_t ndim;
+  int64_t shape[2];
+  int32_t dtype_bytes;
+  int32_t tp_split;
+  int32_t vocab_space;
+  int32_t reserved_;
+} osh_param_desc;
+
+/* Cost kinds (CostKind, cost.hpp:19). */
+enum { OSH_COST_NUMEL = 0, OSH_COST_FLOPS_MUON = 1, OSH_COST_FLOPS_SHAMPOO = 2,
+       OSH_COST_FLOPS_SOAP = 3, OSH_COST_BYTES = 4 };
+/* Plan methods (PlanMethod, dp_partition.hpp:26). */
+enum { OSH_PLAN_EQUAL_CHUNK = 0, OSH_PLAN_ATOMIC_OWNERSHIP = 1, OSH_PLAN_ALPHA_BALANCED = 2 };
+
+typedef struct osh_cost_model {
+  int32_t kind;
+  int32_t ns_steps;       /* default 5 */
+  double shampoo_coeff;   /* default 1.0 */
+  double soap_coeff;      /* default 2.0 */
+} osh_cost_model;
+
+/* Synthetic transformer parameter list (generate_transformer_params,
+ * workload.hpp:113-148). With out == NULL only *n_out is written. */
+osh_status osh_generate_params(int32_t num_layers, int64_t hidden, int64_t ffn, int32_t heads,
+                               int64_t vocab, int32_t dtype_bytes, osh_param_desc* out,
+                               int32_t capacity, int32_t* n_out);
+
+/* Per-tensor planning cost (param_cost, cost.hpp:81-90). */
+osh_status osh_param_cost(const osh_param_desc* p, const osh_cost_model* model, uint64_t* out);
+
+/* Greedy declaration-order bucket packing (build_buffer_layout). Outputs, per
+ * parameter, its bucket index and element offset inside the bucket, plus
+ * per-bucket element counts (bucket_numel must hold n entries). */
+osh_status osh_layout_build(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                            int32_t* bucket_of, int64_t* offset_in_bucket, int64_t* bucket_numel,
+                            int32_t* n_buckets);
+
+/* Data-parallel partition plan. cuts: n_buckets x (ranks+1) int64 (row-major),
+ * rank_loads: ranks uint64. *atomic receives the plan's atomic flag. */
+osh_status osh_plan_dp(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                       int32_t ranks, int32_t method, const osh_cost_model* model, double alpha,
+                       int64_t* cuts, uint64_t* rank_loads, int32_t* atomic);
+
+/* Serialized dp plan text ("optishard-dp-plan v1", serialize.hpp:252-271).
+ * Writes up to cap bytes (NUL-terminated when room) and the full length. */
+osh_status osh_plan_dp_serialize(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                                 int32_t ranks, int32_t method, const osh_cost_model* model,
+                                 double alpha, char* buf, size_t cap, size_t* len);
+
+/* Owning dp rank of every parameter under an atomic plan (param_owner). */
+osh_status osh_param_owners(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                            int32_t ranks, const int64_t* cuts, int32_t* owner_out);
+
+/* Micro-group plan text ("optishard-tp-plan v1") for the given items
+ * (build_micro_groups(items, ranks, c_max, kind), tp_schedule.hpp:90-131). */
+osh_status osh_plan_tp_serialize(const int32_t* item_ids, const uint64_t* item_costs, int32_t n,
+                                 int32_t ranks, uint64_t c_max, int32_t cost_kind, char* buf,
+                                 size_t cap, size_t* len);
+
+/* ---------------------------------------------------------- optimizer */
+typedef struct osh_muon_cfg {
+  double lr;        /* 0.02 (OptimizerConfig, verify.hpp:31-35) */
+  double beta;      /* 0.9 */
+  int32_t ns_steps; /* 5 */
+  int32_t reserved_;
+  double ns_a, ns_b, ns_c; /* 3.4445, -4.7750, 2.0315 (verify.hpp:120) */
+} osh_muon_cfg;
+
+/* Fills cfg with the reference defaults. */
+void osh_muon_cfg_default(osh_muon_cfg* cfg);
+
+/* ------------------------------------------------ kernel-level entry points
+ * Device pointers; `stream` is a cudaStream_t (NULL = legacy default). */
+typedef struct osh_matrix_ref {
+  const void* ptr;    /* bf16, [batch][rows][ld] */
+  int32_t batch, rows, cols;
+  int32_t reserved_;
+  int64_t ld, bstride;
+} osh_matrix_ref;
+
+typedef struct osh_final_target {
+  float* w;           /* fp32 master weight, original [rows][cols] */
+  void* replica;      /* bf16 replica of the same tensor, nullable */
+  double* sq_norm;    /* += ||lr*update||^2, nullable */
+  int32_t transposed; /* tensor is X^T of the Newton-Schulz iterate */
+  int32_t reserved_;
+} osh_final_target;
+
+typedef struct osh_gemm_problem {
+  osh_matrix_ref a;   /* M x K, K-major */
+  osh_matrix_ref b;   /* K-major: N x K ; MN-major: K x N */
+  int32_t b_mn_major;
+  int32_t reserved_;
+  osh_matrix_ref out; /* M x N bf16 */
+  osh_matrix_ref aux; /* M x N bf16 */
+  const float* scale; /* per batch, nullable */
+  const osh_final_target* final_targets;
+} osh_gemm_problem;
+
+enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3 };
+
+/* One grouped tcgen05 GEMM launch (the Newton-Schulz building block). */
+osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* problems, int32_t n_problems,
+                       float alpha, float beta, float lr, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OSH_H_ */

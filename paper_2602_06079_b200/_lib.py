@@ -1,0 +1,122 @@
+"""ctypes binding of libosh.so (the C ABI declared in include/osh.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2602_06079_b200/csrc``). There is no fallback: if the library
+is missing every entry point raises ``OshLibraryMissing`` — the product path
+never silently runs on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libosh.so")
+
+
+class OshLibraryMissing(RuntimeError):
+    pass
+
+
+class OshError(RuntimeError):
+    """Raised for a non-zero osh_status; ``code`` holds the status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"osh status {code}: {msg}")
+        self.code = code
+
+
+# osh_status values (osh.h) -> names of the reference exception classes
+STATUS_NAMES = {
+    1: "ConfigError", 2: "LayoutError", 3: "ShardError", 4: "UnsupportedError",
+    5: "PlanError", 6: "UnschedulableError", 7: "FormatError",
+    16: "CudaError", 17: "NcclError", 18: "OutOfMemory", 19: "ArgumentError",
+}
+
+
+class ParamDesc(ctypes.Structure):
+    _fields_ = [("id", c_int32), ("ndim", c_int32), ("shape", c_int64 * 2),
+                ("dtype_bytes", c_int32), ("tp_split", c_int32), ("vocab_space", c_int32),
+                ("reserved_", c_int32)]
+
+
+class CostModelC(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("ns_steps", c_int32), ("shampoo_coeff", c_double),
+                ("soap_coeff", c_double)]
+
+
+class MuonCfgC(ctypes.Structure):
+    _fields_ = [("lr", c_double), ("beta", c_double), ("ns_steps", c_int32),
+                ("reserved_", c_int32), ("ns_a", c_double), ("ns_b", c_double),
+                ("ns_c", c_double)]
+
+
+class MatrixRef(ctypes.Structure):
+    _fields_ = [("ptr", c_void_p), ("batch", c_int32), ("rows", c_int32), ("cols", c_int32),
+                ("reserved_", c_int32), ("ld", c_int64), ("bstride", c_int64)]
+
+
+class FinalTarget(ctypes.Structure):
+    _fields_ = [("w", c_void_p), ("replica", c_void_p), ("sq_norm", c_void_p),
+                ("transposed", c_int32), ("reserved_", c_int32)]
+
+
+class GemmProblem(ctypes.Structure):
+    _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
+                ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
+                ("scale", c_void_p), ("final_targets", c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libosh.so once; raises OshLibraryMissing when it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OshLibraryMissing(
+                f"{LIB_PATH} not found: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (the CUDA extension is required; there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().osh_last_error().decode(errors="replace")
+        raise OshError(status, f"{STATUS_NAMES.get(status, 'error')}: {msg}")
+
+
+def _declare(L: ctypes.CDLL) -> None:
+    def d(name, restype, *argtypes):
+        fn = getattr(L, name)
+        fn.restype = restype
+        fn.argtypes = list(argtypes)
+
+    d("osh_last_error", c_char_p)
+    d("osh_abi_version", c_int32)
+    d("osh_ns_gemm", c_int32, c_int32, POINTER(GemmProblem), c_int32, c_float, c_float, c_float,
+      c_void_p)
+    optional = [
+        ("osh_generate_params", c_int32, c_int32, c_int64, c_int64, c_int32, c_int64, c_int32,
+         POINTER(ParamDesc), c_int32, POINTER(c_int32)),
+        ("osh_param_cost", c_int32, POINTER(ParamDesc), POINTER(CostModelC), POINTER(c_uint64)),
+        ("osh_layout_build", c_int32, POINTER(ParamDesc), c_int32, c_int64, POINTER(c_int32),
+         POINTER(c_int64), POINTER(c_int64), POINTER(c_int32)),
+        ("osh_plan_dp", c_int32, POINTER(ParamDesc), c_int32, c_int64, c_int32, c_int32,
+         POINTER(CostModelC), c_double, POINTER(c_int64), POINTER(c_uint64), POINTER(c_int32)),
+        ("osh_plan_dp_serialize", c_int32, POINTER(ParamDesc), c_int32, c_int64, c_int32, c_int32,
+         POINTER(CostModelC), c_double, ctypes.c_char_p, c_size_t, POINTER(c_size_t)),
+        ("osh_param_owners", c_int32, POINTER(ParamDesc), c_int32, c_int64, c_int32,
+         POINTER(c_int64), POINTER(c_int32)),
+        ("osh_plan_tp_serialize", c_int32, POINTER(c_int32), POINTER(c_uint64), c_int32, c_int32,
+         c_uint64, c_int32, ctypes.c_char_p, c_size_t, POINTER(c_size_t)),
+        ("osh_muon_cfg_default", None, POINTER(MuonCfgC)),
+    ]
+    for name, restype, *args in optional:
+        if hasattr(L, name):
+            d(name, restype, *args)

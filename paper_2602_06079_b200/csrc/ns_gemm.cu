@@ -1,0 +1,412 @@
+// Persistent, warp-specialised tcgen05 GEMM for the Newton-Schulz iteration
+// (see ns_gemm.cuh for the math). Layout of one CTA (256 threads, 1 CTA/SM):
+//   warp 0  lane 0 : TMA producer     (4-stage smem ring, full/empty mbarriers)
+//   warp 1  lane 0 : tcgen05.mma issuer (UMMA 128x256x16, fp32 accum in TMEM)
+//   warp 2         : TMEM allocator   (512 columns = 2 accumulator buffers)
+//   warps 4-7      : epilogue         (tcgen05.ld -> fused math -> global)
+// The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
+// tile i+1. Tiles of all problems are linearised and strided over the grid.
+#include "ns_gemm.cuh"
+#include "sm100.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+namespace osh {
+namespace {
+
+using namespace osh::sm100;
+
+constexpr uint32_t kStageBytesA = kNsBM * kNsBK * 2;  // 16 KiB
+constexpr uint32_t kStageBytesB = kNsBN * kNsBK * 2;  // 32 KiB
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kSmemBytes = 1024 + kNsStages * (kStageBytesA + kStageBytesB) + 256;
+constexpr int kRasterGroup = 8;
+
+struct TileCoord {
+  int p, b, tm, tn;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const NsGemmParams& P, int t) {
+  TileCoord c;
+  c.p = 0;
+  while (c.p + 1 < P.num_problems && t >= P.prob[c.p + 1].tile_start) ++c.p;
+  const NsGemmProblem& pr = P.prob[c.p];
+  const int local = t - pr.tile_start;
+  const int per_batch = pr.tiles_m * pr.tiles_n;
+  c.b = local / per_batch;
+  const int rem = local - c.b * per_batch;
+  // grouped rasterisation: kRasterGroup tile-rows sweep one column panel
+  const int span = kRasterGroup * pr.tiles_n;
+  const int group = rem / span;
+  const int first_m = group * kRasterGroup;
+  const int gsz = min(pr.tiles_m - first_m, kRasterGroup);
+  const int r2 = rem - group * span;
+  c.tm = first_m + r2 % gsz;
+  c.tn = r2 / gsz;
+  return c;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Loads 32 bf16 of one row (cols [col0, col0+32), masked at n) as floats.
+__device__ __forceinline__ void load_row32(const __nv_bfloat16* src, int col0, int n,
+                                           float (&v)[32]) {
+  if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = __ldg(s4 + q);
+      v[q * 8 + 0] = bf16_lo(u.x);
+      v[q * 8 + 1] = bf16_hi(u.x);
+      v[q * 8 + 2] = bf16_lo(u.y);
+      v[q * 8 + 3] = bf16_hi(u.y);
+      v[q * 8 + 4] = bf16_lo(u.z);
+      v[q * 8 + 5] = bf16_hi(u.z);
+      v[q * 8 + 6] = bf16_lo(u.w);
+      v[q * 8 + 7] = bf16_hi(u.w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (col0 + j < n) ? __bfloat162float(src[j]) : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store_row32(__nv_bfloat16* dst, int col0, int n,
+                                            const float (&v)[32]) {
+  if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+      u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+      u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+      u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+      d4[q] = u;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < n) dst[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kNsThreads, 1)
+    ns_gemm_kernel(const __grid_constant__ NsGemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = base;
+  uint8_t* smem_b = base + kNsStages * kStageBytesA;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + kNsStages * kStageBytesB);
+  uint64_t* empty_bar = full_bar + kNsStages;
+  uint64_t* tfull_bar = empty_bar + kNsStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < P.num_problems; ++p) {
+      tma_prefetch_desc(&P.prob[p].tmA);
+      tma_prefetch_desc(&P.prob[p].tmB);
+    }
+    for (int s = 0; s < kNsStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile(P, t);
+        const NsGemmProblem& pr = P.prob[c.p];
+        const int nkb = (pr.K + kNsBK - 1) / kNsBK;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], kStageBytesA + kStageBytesB);
+          tma_load_3d(smem_a + stage * kStageBytesA, &pr.tmA, &full_bar[stage], kb * kNsBK,
+                      c.tm * kNsBM, c.b);
+          uint8_t* sb = smem_b + stage * kStageBytesB;
+          if (!pr.b_mn_major) {
+            tma_load_3d(sb, &pr.tmB, &full_bar[stage], kb * kNsBK, c.tn * kNsBN, c.b);
+          } else {
+#pragma unroll
+            for (int q = 0; q < kNsBN / 64; ++q)
+              tma_load_3d(sb + q * 8192, &pr.tmB, &full_bar[stage], c.tn * kNsBN + q * 64,
+                          kb * kNsBK, c.b);
+          }
+          if (++stage == kNsStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------- tcgen05 issuer
+    if (lane == 0) {
+      const uint32_t idesc_k = idesc_bf16_f32(kNsBM, kNsBN, false, false);
+      const uint32_t idesc_mn = idesc_bf16_f32(kNsBM, kNsBN, false, true);
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile(P, t);
+        const NsGemmProblem& pr = P.prob[c.p];
+        const int nkb = (pr.K + kNsBK - 1) / kNsBK;
+        const bool mn = pr.b_mn_major != 0;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kNsBN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
+          const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
+#pragma unroll
+          for (int k = 0; k < kNsBK / 16; ++k) {
+            const uint64_t adesc = smem_desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bdesc = mn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
+                                      : smem_desc_sw128(b0 + k * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == kNsStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------- epilogue
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    uint32_t acc = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      const TileCoord c = decode_tile(P, t);
+      const NsGemmProblem& pr = P.prob[c.p];
+      const int row = c.tm * kNsBM + row_in_tile;
+      const bool row_ok = row < pr.M;
+      const float s = pr.scale != nullptr ? __ldg(pr.scale + c.b) : 1.f;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kNsBN;
+      double sq = 0.0;
+#pragma unroll 1
+      for (int chunk = 0; chunk < kNsBN / 32; ++chunk) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + chunk * 32, r);
+        tmem_ld_wait();
+        const int col0 = c.tn * kNsBN + chunk * 32;
+        if (!row_ok || col0 >= pr.N) continue;
+        float v[32];
+        if constexpr (MODE == kEpiGram) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = s * __uint_as_float(r[j]);
+          store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+        } else if constexpr (MODE == kEpiPoly) {
+          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = P.alpha * v[j] + P.beta * __uint_as_float(r[j]);
+          store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+        } else if constexpr (MODE == kEpiUpdate) {
+          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = s * (P.alpha * v[j] + __uint_as_float(r[j]));
+          store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+        } else {  // kEpiFinal
+          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+          const NsFinalTarget ft = pr.final_targets[c.b];
+          const int ncol = min(32, pr.N - col0);
+#pragma unroll 4
+          for (int j = 0; j < ncol; ++j) {
+            const float upd = P.lr * (s * (P.alpha * v[j] + __uint_as_float(r[j])));
+            const int col = col0 + j;
+            const size_t idx = ft.transposed ? static_cast<size_t>(col) * pr.M + row
+                                             : static_cast<size_t>(row) * pr.N + col;
+            const float w = ft.w[idx] - upd;
+            ft.w[idx] = w;
+            if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
+            sq += static_cast<double>(upd) * static_cast<double>(upd);
+          }
+        }
+      }
+      if constexpr (MODE == kEpiFinal) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0 && sq != 0.0) {
+          double* dst = pr.final_targets[c.b].sq_norm;
+          if (dst != nullptr) atomicAdd(dst, sq);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// rows x cols per batch, row stride ld, batch stride bstride (elements);
+// the tensor map's dim0 is `cols` (contiguous), dim1 `rows`, dim2 batch.
+bool make_map(CUtensorMap* map, const NsMatrixRef& m, uint32_t box_cols, uint32_t box_rows) {
+  EncodeFn enc = encode_fn();
+  if (enc == nullptr) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(m.cols), static_cast<cuuint64_t>(m.rows),
+                              static_cast<cuuint64_t>(m.batch)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(m.ld) * 2,
+                                 static_cast<cuuint64_t>(m.bstride) * 2};
+  const cuuint32_t box[3] = {box_cols, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(m.ptr), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  });
+  return n;
+}
+
+template <int MODE>
+cudaError_t launch_mode(const NsGemmParams& P, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ns_gemm_kernel<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int grid = std::min(P.total_tiles, sm_count());
+  ns_gemm_kernel<MODE><<<grid, kNsThreads, kSmemBytes, stream>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+double ns_gemm_flops(const NsProblemDesc* probs, int num_problems) {
+  double f = 0.0;
+  for (int i = 0; i < num_problems; ++i) {
+    const NsProblemDesc& d = probs[i];
+    const double K = d.a.cols, M = d.a.rows;
+    const double N = d.b_mn_major ? d.b.cols : d.b.rows;
+    f += 2.0 * M * N * K * d.a.batch;
+  }
+  return f;
+}
+
+cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
+                           float beta, float lr, cudaStream_t stream) {
+  if (num_problems < 1 || num_problems > kMaxProblems) return cudaErrorInvalidValue;
+  NsGemmParams P{};
+  P.num_problems = num_problems;
+  P.alpha = alpha;
+  P.beta = beta;
+  P.lr = lr;
+  int tiles = 0;
+  for (int i = 0; i < num_problems; ++i) {
+    const NsProblemDesc& d = probs[i];
+    NsGemmProblem& pr = P.prob[i];
+    pr.batch = d.a.batch;
+    pr.M = d.a.rows;
+    pr.K = d.a.cols;
+    pr.N = d.b_mn_major ? d.b.cols : d.b.rows;
+    const int kb = d.b_mn_major ? d.b.rows : d.b.cols;
+    if (kb != pr.K || d.b.batch != pr.batch || pr.M < 1 || pr.N < 1 || pr.K < 1 || pr.batch < 1)
+      return cudaErrorInvalidValue;
+    pr.b_mn_major = d.b_mn_major;
+    if (!make_map(&pr.tmA, d.a, kNsBK, kNsBM)) return cudaErrorInvalidValue;
+    if (!d.b_mn_major) {
+      if (!make_map(&pr.tmB, d.b, kNsBK, kNsBN)) return cudaErrorInvalidValue;
+    } else {
+      if (!make_map(&pr.tmB, d.b, 64, kNsBK)) return cudaErrorInvalidValue;
+    }
+    pr.tiles_m = (pr.M + kNsBM - 1) / kNsBM;
+    pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
+    pr.tile_start = tiles;
+    tiles += pr.batch * pr.tiles_m * pr.tiles_n;
+    pr.out = static_cast<__nv_bfloat16*>(const_cast<void*>(d.out.ptr));
+    pr.out_ld = d.out.ld;
+    pr.out_bstride = d.out.bstride;
+    pr.aux = static_cast<const __nv_bfloat16*>(d.aux.ptr);
+    pr.aux_ld = d.aux.ld;
+    pr.aux_bstride = d.aux.bstride;
+    pr.scale = d.scale;
+    pr.final_targets = d.final_targets;
+    if (mode == kEpiFinal && pr.final_targets == nullptr) return cudaErrorInvalidValue;
+    if ((mode == kEpiPoly || mode == kEpiUpdate || mode == kEpiFinal) && pr.aux == nullptr)
+      return cudaErrorInvalidValue;
+    if (mode != kEpiFinal && pr.out == nullptr) return cudaErrorInvalidValue;
+  }
+  P.total_tiles = tiles;
+  switch (mode) {
+    case kEpiGram: return launch_mode<kEpiGram>(P, stream);
+    case kEpiPoly: return launch_mode<kEpiPoly>(P, stream);
+    case kEpiUpdate: return launch_mode<kEpiUpdate>(P, stream);
+    case kEpiFinal: return launch_mode<kEpiFinal>(P, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace osh

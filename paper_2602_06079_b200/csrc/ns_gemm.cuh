@@ -1,0 +1,92 @@
+// Batched, grouped tcgen05 GEMM for the Muon Newton-Schulz iteration.
+//
+// One Newton-Schulz step on X (m x n, m <= n, row-major bf16) is three
+// contractions (reference verify.hpp:126-131):
+//   GRAM   A  = s^2 * (X X^T)                 m x m, K = n, both operands K-major
+//   POLY   B  = b*A + c*(A A^T)  (A = A^T)     m x m, K = m, both operands K-major
+//   UPDATE X' = s*(a*X + B X)                  m x n, K = m, X read MN-major
+//   FINAL  W -= lr * s*(a*X + B X)             last step: fused weight update
+// s is a per-matrix scale (1/||M||_F on the first step, where the iterate is
+// the raw momentum cast to bf16; 1 afterwards). The reference evaluates
+// b*(A X) + c*(A (A X)); B = b*A + c*A*A is the same polynomial with
+// 4m^2n + 2m^3 instead of 6m^2n flops per step.
+//
+// Up to kMaxProblems independent problems (shape classes) share one
+// persistent launch; every problem is batched over same-shape matrices laid
+// out as [batch][rows][ld] so a single 3-D TMA descriptor covers the class.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace osh {
+
+constexpr int kNsBM = 128;       // UMMA M (one CTA, cta_group::1)
+constexpr int kNsBN = 256;       // UMMA N
+constexpr int kNsBK = 64;        // one 128-byte swizzle row of bf16
+constexpr int kNsStages = 4;
+constexpr int kNsThreads = 256;  // warps 0-3: TMA / MMA / TMEM alloc / spare, 4-7: epilogue
+constexpr int kMaxProblems = 4;
+
+enum NsEpilogue : int { kEpiGram = 0, kEpiPoly = 1, kEpiUpdate = 2, kEpiFinal = 3 };
+
+// Where the last Newton-Schulz step of one matrix lands: the fp32 master
+// weight (and its bf16 replica) in the tensor's ORIGINAL orientation.
+struct NsFinalTarget {
+  float* w;                   // [rows][cols] row-major fp32 master weight
+  __nv_bfloat16* replica;     // bf16 copy of the same tensor (nullable)
+  double* sq_norm;            // += ||lr * update||_F^2 (nullable)
+  int transposed;             // 1: the tensor is X^T (rows > cols in the reference)
+  int pad_;
+};
+
+struct alignas(64) NsGemmProblem {
+  CUtensorMap tmA;  // [batch][M][K], K-major, box {64, 128, 1}
+  CUtensorMap tmB;  // K-major: [batch][N][K] box {64, 256, 1}; MN-major: [batch][K][N] box {64, 64, 1}
+  int batch, M, N, K;
+  int b_mn_major;
+  int tiles_m, tiles_n;
+  int tile_start;
+  __nv_bfloat16* out;
+  long long out_ld, out_bstride;
+  const __nv_bfloat16* aux;
+  long long aux_ld, aux_bstride;
+  const float* scale;                 // per-batch multiplier, nullable (= 1)
+  const NsFinalTarget* final_targets; // per batch, kEpiFinal only
+};
+
+struct NsGemmParams {
+  NsGemmProblem prob[kMaxProblems];
+  int num_problems;
+  int total_tiles;
+  float alpha, beta, lr;
+};
+
+// Host-side description of one batched operand: batch x rows x cols bf16,
+// row stride `ld` elements, batch stride `bstride` elements.
+struct NsMatrixRef {
+  const void* ptr;
+  int batch, rows, cols;
+  long long ld, bstride;
+};
+
+struct NsProblemDesc {
+  NsMatrixRef a;        // M x K
+  NsMatrixRef b;        // K-major: N x K ; MN-major: K x N
+  int b_mn_major;
+  NsMatrixRef out;      // M x N (bf16), unused for kEpiFinal
+  NsMatrixRef aux;      // M x N (bf16) or nullptr
+  const float* scale;   // device, per batch
+  const NsFinalTarget* final_targets;  // device, per batch
+};
+
+// Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).
+cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
+                           float beta, float lr, cudaStream_t stream);
+
+// Algorithmic flops of a problem list (2*M*N*K per batch element).
+double ns_gemm_flops(const NsProblemDesc* probs, int num_problems);
+
+}  // namespace osh

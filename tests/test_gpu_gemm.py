@@ -1,0 +1,162 @@
+"""Numerics of the grouped tcgen05 Newton-Schulz GEMM (osh_ns_gemm) against a
+plain PyTorch fp32 reference of the same contraction on the same bf16 inputs.
+
+Tolerance: outputs are bf16 (8-bit mantissa), accumulation fp32, so the
+max-abs error relative to the max-abs reference value must stay below 1e-2.
+"""
+import ctypes
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2602_06079_b200 import _lib  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+A, B, C = 3.4445, -4.7750, 2.0315
+
+
+def mref(t, rows=None, cols=None, batch=None):
+    """MatrixRef for a [batch][rows][ld] bf16 tensor (logical rows x cols)."""
+    assert t.dtype == torch.bfloat16 and t.is_cuda and t.dim() == 3
+    bt, r, ld = t.shape
+    m = _lib.MatrixRef()
+    m.ptr = t.data_ptr()
+    m.batch = bt if batch is None else batch
+    m.rows = r if rows is None else rows
+    m.cols = ld if cols is None else cols
+    m.ld = t.stride(1)
+    m.bstride = t.stride(0)
+    return m
+
+
+def run(mode, probs, alpha=0.0, beta=0.0, lr=0.0):
+    arr = (_lib.GemmProblem * len(probs))(*probs)
+    _lib.check(_lib.lib().osh_ns_gemm(mode, arr, len(probs), alpha, beta, lr,
+                                      torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+
+
+def padded(batch, rows, cols, ld=None, scale=1.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    ld = ld or cols
+    t = torch.zeros(batch, rows, ld, device="cuda", dtype=torch.bfloat16)
+    t[:, :, :cols] = (torch.randn(batch, rows, cols, device="cuda", generator=g) * scale).bfloat16()
+    return t
+
+
+def relerr(got, ref):
+    return ((got.float() - ref.float()).abs().max() / ref.float().abs().max().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("batch,m,n,ld", [(1, 128, 256, 256), (2, 256, 768, 768), (3, 200, 300, 304),
+                                          (1, 8, 24, 24), (2, 64, 12, 16), (1, 1024, 3072, 3072)])
+def test_gram(batch, m, n, ld):
+    x = padded(batch, m, n, ld, scale=0.05)
+    out = torch.zeros(batch, m, m + (-m) % 8, device="cuda", dtype=torch.bfloat16)
+    scale = torch.full((batch,), 0.5, device="cuda")
+    p = _lib.GemmProblem()
+    p.a = mref(x, cols=n)
+    p.b = mref(x, cols=n)
+    p.b_mn_major = 0
+    p.out = mref(out, cols=m)
+    p.scale = scale.data_ptr()
+    run(0, [p])
+    xf = x[:, :, :n].float()
+    ref = 0.5 * xf @ xf.transpose(1, 2)
+    assert relerr(out[:, :, :m], ref) < 1e-2
+
+
+@pytest.mark.parametrize("batch,m", [(1, 128), (2, 512), (4, 100)])
+def test_poly(batch, m):
+    x = padded(batch, m, 2 * m, scale=0.05)
+    a = (x.float() @ x.float().transpose(1, 2)).bfloat16()
+    ld = m + (-m) % 8
+    a_p = torch.zeros(batch, m, ld, device="cuda", dtype=torch.bfloat16)
+    a_p[:, :, :m] = a
+    out = torch.zeros_like(a_p)
+    p = _lib.GemmProblem()
+    p.a = mref(a_p, cols=m)
+    p.b = mref(a_p, cols=m)
+    p.out = mref(out, cols=m)
+    p.aux = mref(a_p, cols=m)
+    run(1, [p], alpha=B, beta=C)
+    af = a.float()
+    ref = B * af + C * af @ af
+    assert relerr(out[:, :, :m], ref) < 1e-2
+
+
+@pytest.mark.parametrize("batch,m,n", [(1, 128, 256), (2, 256, 1000), (3, 64, 4000), (1, 8, 24)])
+def test_update_mn_major(batch, m, n):
+    ld = n + (-n) % 8
+    x = padded(batch, m, n, ld, scale=0.1)
+    bm = padded(batch, m, m, m + (-m) % 8, scale=0.1, seed=1)
+    out = torch.zeros_like(x)
+    scale = torch.full((batch,), 0.25, device="cuda")
+    p = _lib.GemmProblem()
+    p.a = mref(bm, cols=m)
+    p.b = mref(x, cols=n)        # K x N = m x n, N contiguous
+    p.b_mn_major = 1
+    p.out = mref(out, cols=n)
+    p.aux = mref(x, cols=n)
+    p.scale = scale.data_ptr()
+    run(2, [p], alpha=A)
+    xf = x[:, :, :n].float()
+    ref = 0.25 * (A * xf + bm[:, :, :m].float() @ xf)
+    assert relerr(out[:, :, :n], ref) < 1e-2
+
+
+@pytest.mark.parametrize("transposed", [0, 1])
+def test_final_weight_update(transposed):
+    batch, m, n = 2, 128, 384
+    x = padded(batch, m, n, scale=0.1)
+    bm = padded(batch, m, m, scale=0.1, seed=2)
+    w0 = torch.randn(batch, m, n, device="cuda")
+    if transposed:
+        w = w0.transpose(1, 2).contiguous()   # tensor stored as [n][m]
+    else:
+        w = w0.clone()
+    rep = torch.zeros(w.shape, device="cuda", dtype=torch.bfloat16)
+    sq = torch.zeros(batch, device="cuda", dtype=torch.float64)
+    tg = (_lib.FinalTarget * batch)()
+    for i in range(batch):
+        tg[i].w = w[i].data_ptr()
+        tg[i].replica = rep[i].data_ptr()
+        tg[i].sq_norm = sq[i:].data_ptr()
+        tg[i].transposed = transposed
+    tg_dev = torch.frombuffer(bytearray(tg), dtype=torch.uint8).cuda()
+    p = _lib.GemmProblem()
+    p.a = mref(bm)
+    p.b = mref(x)
+    p.b_mn_major = 1
+    p.aux = mref(x)
+    p.final_targets = tg_dev.data_ptr()
+    lr = 0.02
+    run(3, [p], alpha=A, lr=lr)
+    upd = lr * (A * x.float() + bm.float() @ x.float())
+    ref = w0 - upd
+    got = w.transpose(1, 2) if transposed else w
+    assert (got - ref).abs().max().item() < 1e-3 * upd.abs().max().item() + 1e-6
+    assert torch.equal(rep, w.bfloat16())
+    want_sq = (upd.double() ** 2).sum(dim=(1, 2))
+    assert torch.allclose(sq, want_sq, rtol=1e-2)
+
+
+def test_grouped_problems_one_launch():
+    shapes = [(2, 128, 384), (5, 64, 192), (1, 256, 256)]
+    xs, outs, ps = [], [], []
+    for i, (bt, m, n) in enumerate(shapes):
+        x = padded(bt, m, n, scale=0.05, seed=10 + i)
+        out = torch.zeros(bt, m, m, device="cuda", dtype=torch.bfloat16)
+        p = _lib.GemmProblem()
+        p.a = mref(x)
+        p.b = mref(x)
+        p.out = mref(out)
+        xs.append(x)
+        outs.append(out)
+        ps.append(p)
+    run(0, ps)
+    for x, out in zip(xs, outs):
+        xf = x.float()
+        assert relerr(out, xf @ xf.transpose(1, 2)) < 1e-2
