@@ -2,7 +2,7 @@
  * osh.h — C ABI of the B200-native Canzona optimizer step ("optishard" drop-in).
  *
  * This is the boundary between host code that speaks the reference's C++
- * interface (include/optishard/*.hpp, namespace optishard) and the sm_100a
+ * interface (include/optishard/ headers, namespace optishard) and the sm_100a
  * CUDA library libosh.so. Plain C types only: no C++ or torch types cross it.
  * Every entry point returns an osh_status; on failure osh_last_error() holds
  * a thread-local message. No exception crosses the ABI.
