@@ -162,6 +162,85 @@ enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3
 osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* problems, int32_t n_problems,
                        float alpha, float beta, float lr, void* stream);
 
+/* ------------------------------------------------------- per-rank runtime
+ * One osh_ctx per GPU (one process or host thread per ctx; a ctx is not
+ * thread-safe). The ctx owns every device buffer it allocates; host arrays
+ * passed in are only borrowed for the duration of the call. Work is ordered on
+ * the ctx's own streams; osh_step returns once the step is ENQUEUED unless a
+ * host output is requested (osh_ctx_sync waits). */
+typedef struct osh_ctx osh_ctx;
+
+enum { OSH_COMM_NCCL = 0, /* real NCCL collectives on the dp communicator     */
+       OSH_COMM_NONE = 1  /* no collectives: the caller reduces gradients and
+                             reads owned results (single-GPU rank simulation) */ };
+enum { OSH_GRAD_F32 = 0, OSH_GRAD_BF16 = 1 };
+enum { OSH_READ_MASTER = 0, OSH_READ_MOMENTUM = 1, OSH_READ_REPLICA = 2 };
+enum { OSH_FILL_WEIGHTS = 1, OSH_FILL_GRADS = 2 };
+
+/* 128-byte ncclUniqueId for rank 0 to broadcast out of band. */
+osh_status osh_nccl_unique_id(uint8_t out[128]);
+
+osh_status osh_ctx_create(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t comm_mode,
+                          const uint8_t* nccl_uid /* 128 bytes; unused for OSH_COMM_NONE */,
+                          osh_ctx** out);
+osh_status osh_ctx_destroy(osh_ctx* ctx);
+
+/* Installs the parameter list (ids dense 0..n-1, declaration order), the
+ * bucket capacity and the dp plan's cut vectors (n_buckets x (dp_size+1),
+ * e.g. from osh_plan_dp). The plan must be atomic (whole tensors). Allocates
+ * grads, replica, owned fp32 state and the Newton-Schulz workspace
+ * (workspace_bytes <= 0: default budget). */
+osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_t n,
+                              int64_t bucket_capacity, const int64_t* cuts, int32_t n_buckets,
+                              int32_t grad_dtype, int64_t workspace_bytes);
+
+typedef struct osh_ctx_info {
+  int64_t total_numel;     /* elements of the full model */
+  int64_t owned_numel;     /* elements this rank updates */
+  int32_t n_params, n_owned, n_buckets, n_waves;
+  int64_t workspace_bytes; /* Newton-Schulz workspace */
+  int64_t device_bytes;    /* everything the ctx allocated */
+  double ns_flops_per_iter; /* algorithmic GEMM flops (4m^2n + 2m^3 per owned matrix)
+                              of ONE Newton-Schulz iteration on this rank */
+} osh_ctx_info;
+osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out);
+
+/* Device pointers of the flat gradient buffer (grad dtype) and bf16 replica,
+ * both [total_numel] in declaration order: param p starts at the sum of the
+ * numels of params 0..p-1. A training loop writes its gradients here. */
+osh_status osh_ctx_buffers(osh_ctx* ctx, void** grad, void** replica);
+
+/* Host fp32 values of one parameter -> replica (every rank) and fp32 master
+ * weight (owner only); the owner's momentum is reset to zero. */
+osh_status osh_load_param(osh_ctx* ctx, int32_t param_id, const float* values);
+/* Host fp32 gradient of one parameter -> the flat gradient buffer. */
+osh_status osh_write_grad(osh_ctx* ctx, int32_t param_id, const float* values);
+/* Device-side synthetic fill (counter-based normal draws * scale / sqrt(rows)):
+ * OSH_FILL_WEIGHTS sets replica + owned masters (+ zero momentum),
+ * OSH_FILL_GRADS the gradient buffer. For benchmarks. */
+osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float scale);
+
+/* One distributed Muon step: [H2D host_grads (flat, grad dtype) ->]
+ * RS-v -> owner Muon -> AG-v [-> D2H updated replica into host_replica_out].
+ * Either host pointer may be NULL (device-resident data). */
+osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
+                    void* host_replica_out);
+osh_status osh_ctx_sync(osh_ctx* ctx);
+
+typedef struct osh_step_timing {
+  float h2d_ms, rs_ms, compute_ms, ag_ms, d2h_ms, total_ms; /* CUDA events */
+  int32_t gemm_launches, elementwise_launches;
+  double gemm_flops;
+} osh_step_timing;
+/* Timing of the last step (synchronises the ctx's streams). */
+osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out);
+
+/* ||lr * update||_F of every parameter in the last step (owned params;
+ * -1 for params another rank owns). */
+osh_status osh_update_norms(osh_ctx* ctx, double* out);
+/* One parameter to host fp32 (OSH_READ_MASTER / _MOMENTUM: owner only). */
+osh_status osh_read_param(osh_ctx* ctx, int32_t param_id, int32_t which, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,20 @@ class FinalTarget(ctypes.Structure):
                 ("transposed", c_int32), ("reserved_", c_int32)]
 
 
+class CtxInfo(ctypes.Structure):
+    _fields_ = [("total_numel", c_int64), ("owned_numel", c_int64), ("n_params", c_int32),
+                ("n_owned", c_int32), ("n_buckets", c_int32), ("n_waves", c_int32),
+                ("workspace_bytes", c_int64), ("device_bytes", c_int64),
+                ("ns_flops_per_iter", c_double)]
+
+
+class StepTiming(ctypes.Structure):
+    _fields_ = [("h2d_ms", c_float), ("rs_ms", c_float), ("compute_ms", c_float),
+                ("ag_ms", c_float), ("d2h_ms", c_float), ("total_ms", c_float),
+                ("gemm_launches", c_int32), ("elementwise_launches", c_int32),
+                ("gemm_flops", c_double)]
+
+
 class GemmProblem(ctypes.Structure):
     _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
                 ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
@@ -116,6 +130,22 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_plan_tp_serialize", c_int32, POINTER(c_int32), POINTER(c_uint64), c_int32, c_int32,
          c_uint64, c_int32, ctypes.c_char_p, c_size_t, POINTER(c_size_t)),
         ("osh_muon_cfg_default", None, POINTER(MuonCfgC)),
+        ("osh_nccl_unique_id", c_int32, c_void_p),
+        ("osh_ctx_create", c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
+         POINTER(c_void_p)),
+        ("osh_ctx_destroy", c_int32, c_void_p),
+        ("osh_ctx_set_layout", c_int32, c_void_p, POINTER(ParamDesc), c_int32, c_int64,
+         POINTER(c_int64), c_int32, c_int32, c_int64),
+        ("osh_ctx_get_info", c_int32, c_void_p, POINTER(CtxInfo)),
+        ("osh_ctx_buffers", c_int32, c_void_p, POINTER(c_void_p), POINTER(c_void_p)),
+        ("osh_load_param", c_int32, c_void_p, c_int32, POINTER(c_float)),
+        ("osh_write_grad", c_int32, c_void_p, c_int32, POINTER(c_float)),
+        ("osh_fill_synthetic", c_int32, c_void_p, c_uint64, c_int32, c_float),
+        ("osh_step", c_int32, c_void_p, POINTER(MuonCfgC), c_void_p, c_void_p),
+        ("osh_ctx_sync", c_int32, c_void_p),
+        ("osh_last_timing", c_int32, c_void_p, POINTER(StepTiming)),
+        ("osh_update_norms", c_int32, c_void_p, POINTER(c_double)),
+        ("osh_read_param", c_int32, c_void_p, c_int32, c_int32, POINTER(c_float)),
     ]
     for name, restype, *args in optional:
         if hasattr(L, name):

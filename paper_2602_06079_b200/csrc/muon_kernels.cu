@@ -1,0 +1,163 @@
+// Elementwise Muon kernels (see muon_kernels.cuh for the math and bytes).
+#include "muon_kernels.cuh"
+
+namespace osh {
+namespace {
+
+template <typename G>
+__device__ __forceinline__ float load_grad(const void* g, size_t i);
+template <>
+__device__ __forceinline__ float load_grad<float>(const void* g, size_t i) {
+  return __ldg(static_cast<const float*>(g) + i);
+}
+template <>
+__device__ __forceinline__ float load_grad<__nv_bfloat16>(const void* g, size_t i) {
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(g)[i]);
+}
+
+// Block sum in a fixed order (xor-shuffle tree, then warps in index order).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+  return s;  // valid in thread 0
+}
+
+__device__ __forceinline__ void block_add_double(float v, double* dst, double* red) {
+  const double s = block_sum(static_cast<double>(v), red);
+  if (threadIdx.x == 0 && s != 0.0 && dst != nullptr) atomicAdd(dst, s);
+}
+
+// One 64x64 tile of one matrix per CTA; 256 threads = 8 rows x 32 columns
+// per pass, so every global access is a coalesced 128-byte (fp32) or
+// 64-byte (bf16) warp transaction.
+template <typename G>
+__global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatrixTask* tasks,
+                                                              int n_tasks, float beta) {
+  __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
+  __shared__ double red[8];
+  const long long t = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const MomentumMatrixTask T = tasks[lo];
+  const long long local = t - T.tile_start;
+  const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
+  const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < kTile / 8; ++i) {
+    const int lr = ty + 8 * i;
+    const int row = r0 + lr;
+#pragma unroll
+    for (int j = 0; j < kTile / 32; ++j) {
+      const int lc = tx + 32 * j;
+      const int col = c0 + lc;
+      __nv_bfloat16 xv = __float2bfloat16_rn(0.f);
+      if (row < T.rows && col < T.cols) {
+        const size_t idx = static_cast<size_t>(row) * T.cols + col;
+        const float mv = beta * T.m[idx] + load_grad<G>(T.g, idx);
+        T.m[idx] = mv;
+        sq += mv * mv;
+        xv = __float2bfloat16_rn(mv);
+        if (!T.transposed) T.x0[static_cast<size_t>(row) * T.ldx + col] = xv;
+      }
+      if (T.transposed) tile[lr][lc] = xv;
+    }
+  }
+  if (T.transposed) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kTile / 8; ++i) {
+      const int lc = ty + 8 * i;  // original column -> NS row
+      const int col = c0 + lc;
+#pragma unroll
+      for (int j = 0; j < kTile / 32; ++j) {
+        const int lr = tx + 32 * j;  // original row -> NS column (contiguous)
+        const int row = r0 + lr;
+        if (row < T.rows && col < T.cols)
+          T.x0[static_cast<size_t>(col) * T.ldx + row] = tile[lr][lc];
+      }
+    }
+  }
+  const double tile_sum = block_sum(static_cast<double>(sq), red);
+  if (threadIdx.x == 0) T.partial[local] = tile_sum;
+}
+
+template <typename G>
+__global__ void __launch_bounds__(256) momentum_vector_kernel(const MomentumVectorTask* tasks,
+                                                              float beta, float lr) {
+  __shared__ double red[8];
+  const MomentumVectorTask T = tasks[blockIdx.y];
+  float sq = 0.f;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < T.n; i += 256ll * gridDim.x) {
+    const float mv = beta * T.m[i] + load_grad<G>(T.g, static_cast<size_t>(i));
+    T.m[i] = mv;
+    const float upd = lr * mv;
+    const float w = T.w[i] - upd;
+    T.w[i] = w;
+    if (T.replica != nullptr) T.replica[i] = __float2bfloat16_rn(w);
+    sq += upd * upd;
+  }
+  block_add_double(sq, T.sq_norm, red);
+}
+
+__global__ void __launch_bounds__(256) ns_scales_kernel(const double* partial,
+                                                        const long long* begin, const int* count,
+                                                        float* su, float* sg) {
+  __shared__ double red[8];
+  const int i = blockIdx.x;
+  const double* p = partial + begin[i];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < count[i]; t += 256) acc += p[t];
+  const double ss = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    const double s = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    su[i] = static_cast<float>(s);
+    sg[i] = static_cast<float>(s * s);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_tasks,
+                                   long long total_tiles, int grad_dtype, float beta,
+                                   cudaStream_t s) {
+  if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
+  if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>(total_tiles));
+  if (grad_dtype == kGradBF16)
+    momentum_matrix_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
+  else
+    momentum_matrix_kernel<float><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_momentum_vector(const MomentumVectorTask* d_tasks, int n_tasks, int grad_dtype,
+                                   float beta, float lr, cudaStream_t s) {
+  if (n_tasks == 0) return cudaSuccess;
+  const dim3 grid(1, static_cast<unsigned>(n_tasks));  // one CTA per vector: deterministic norm
+  if (grad_dtype == kGradBF16)
+    momentum_vector_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(d_tasks, beta, lr);
+  else
+    momentum_vector_kernel<float><<<grid, 256, 0, s>>>(d_tasks, beta, lr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ns_scales(const double* partial, const long long* begin, const int* count,
+                             float* su, float* sg, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ns_scales_kernel<<<n, 256, 0, s>>>(partial, begin, count, su, sg);
+  return cudaGetLastError();
+}
+
+}  // namespace osh

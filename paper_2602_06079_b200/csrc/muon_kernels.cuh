@@ -1,0 +1,59 @@
+// HBM-bound elementwise kernels around the Newton-Schulz GEMMs.
+//
+//  momentum_matrix_kernel  (SURVEY.md §2.2 K1+K2) per owned matrix tile:
+//      m = beta*m + g            (fp32 state, g = reduced gradient bf16/fp32)
+//      per-tile sum of m^2 (fp64, reduced in fixed order -> ||m||_F)
+//      X0 = bf16(m) in the Newton-Schulz orientation (transposed through
+//      shared memory when rows > cols, verify.hpp:123-124); the 1/||m|| scale
+//      is folded into the first GEMM epilogues instead of a second pass.
+//  momentum_vector_kernel  (K7) m = beta*m + g; w -= lr*m; replica = bf16(w)
+//  ns_scales_kernel        s = 1/||m|| (0 for a zero matrix: the reference
+//      returns the zero iterate unchanged, verify.hpp:122), s^2 for the Gram.
+// Algorithmic HBM bytes per element: matrix pass 4+2 (g fp32/bf16 read) +
+// 4 (m read) + 4 (m write) + 2 (X0 write); vector pass 4+2 + 4+4 + 4+4 + 2.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace osh {
+
+enum GradDtype : int { kGradF32 = 0, kGradBF16 = 1 };
+
+constexpr int kTile = 64;  // momentum tile edge (elements)
+
+struct MomentumMatrixTask {
+  const void* g;         // [rows][cols] reduced gradient (dtype per launch)
+  float* m;              // [rows][cols] fp32 momentum
+  __nv_bfloat16* x0;     // NS iterate: [rows][ldx] or, transposed, [cols][ldx]
+  double* partial;       // [tiles of this task] per-tile sum of m^2 (fixed-order
+                         // reduction in ns_scales keeps the step deterministic)
+  int rows, cols;
+  int ldx;
+  int transposed;
+  long long tile_start;  // first linear tile of this task (prefix sum)
+  int tiles_c;           // column tiles
+  int pad_;
+};
+
+struct MomentumVectorTask {
+  const void* g;
+  float* m;
+  float* w;
+  __nv_bfloat16* replica;  // nullable
+  double* sq_norm;         // += ||lr*m||^2, nullable
+  long long n;
+};
+
+cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_tasks,
+                                   long long total_tiles, int grad_dtype, float beta,
+                                   cudaStream_t s);
+cudaError_t launch_momentum_vector(const MomentumVectorTask* d_tasks, int n_tasks, int grad_dtype,
+                                   float beta, float lr, cudaStream_t s);
+// Per slot i: s = 1/sqrt(sum(partial[begin_i .. begin_i+count_i))) (0 if the
+// sum is 0); scale_update = s, scale_gram = s^2. Deterministic tree order.
+cudaError_t launch_ns_scales(const double* partial, const long long* begin, const int* count,
+                             float* scale_update, float* scale_gram, int n, cudaStream_t s);
+
+}  // namespace osh

@@ -1,0 +1,504 @@
+// Per-rank runtime behind the osh_ctx_* / osh_step C ABI (see runtime.cuh).
+#include "runtime.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "status.hpp"
+
+using namespace optishard;
+
+namespace {
+
+constexpr int64_t kOwnedAlign = 64;  // elements (256 B for fp32)
+
+#define OSH_NCCL_TRY(expr)                                                                     \
+  do {                                                                                         \
+    ncclResult_t r_ = (expr);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      return osh::fail(OSH_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+
+__global__ void cast_f32_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Counter-based N(0,1) * scale for element `idx` of stream `seed`.
+__device__ __forceinline__ float synth_normal(uint64_t seed, uint64_t idx) {
+  const uint64_t r = mix64(seed ^ mix64(idx));
+  const float u1 = (static_cast<float>(r >> 40) + 1.0f) * (1.0f / 16777216.0f);
+  const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.0f / 16777216.0f);
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+// Fills [n] elements starting at flat element `base` of the model.
+__global__ void fill_synth_kernel(uint64_t seed, long long base, long long n, float scale,
+                                  float* f32, __nv_bfloat16* bf16) {
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
+    const float v = scale * synth_normal(seed, static_cast<uint64_t>(base + i));
+    if (f32 != nullptr) f32[i] = v;
+    if (bf16 != nullptr) bf16[i] = __float2bfloat16_rn(v);
+  }
+}
+
+unsigned grid_for(long long n) {
+  return static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148ll * 16));
+}
+
+size_t grad_esize(int dtype) { return dtype == osh::kGradBF16 ? 2 : 4; }
+
+osh_status check_ctx(osh_ctx* ctx, bool need_layout) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (need_layout && !ctx->layout_ready)
+    return osh::fail(OSH_ERR_PLAN, "osh_ctx_set_layout has not been called");
+  if (cudaSetDevice(ctx->device) != cudaSuccess)
+    return osh::fail(OSH_ERR_CUDA, "cudaSetDevice failed");
+  return OSH_OK;
+}
+
+bool distributed(const osh_ctx* ctx) {
+  return ctx->comm_mode == OSH_COMM_NCCL && ctx->size > 1 && ctx->comm != nullptr;
+}
+
+void free_layout(osh_ctx* ctx) {
+  ctx->engine.reset();
+  cudaFree(ctx->grad);
+  cudaFree(ctx->replica);
+  cudaFree(ctx->w);
+  cudaFree(ctx->m);
+  ctx->grad = nullptr;
+  ctx->replica = nullptr;
+  ctx->w = ctx->m = nullptr;
+  ctx->layout_ready = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+osh_status osh_nccl_unique_id(uint8_t out[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  if (out == nullptr) return osh::fail(OSH_ERR_ARG, "null output");
+  ncclUniqueId id;
+  OSH_NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return OSH_OK;
+}
+
+osh_status osh_ctx_create(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t comm_mode,
+                          const uint8_t* nccl_uid, osh_ctx** out) {
+  if (out == nullptr) return osh::fail(OSH_ERR_ARG, "null output");
+  *out = nullptr;
+  if (dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
+    return osh::fail(OSH_ERR_PLAN, "dp_rank/dp_size out of range");
+  if (comm_mode != OSH_COMM_NCCL && comm_mode != OSH_COMM_NONE)
+    return osh::fail(OSH_ERR_ARG, "unknown comm_mode");
+  OSH_CUDA_TRY(cudaSetDevice(device));
+  std::unique_ptr<osh_ctx> ctx(new osh_ctx());
+  ctx->device = device;
+  ctx->rank = dp_rank;
+  ctx->size = dp_size;
+  ctx->comm_mode = comm_mode;
+  OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking));
+  OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : ctx->ev) OSH_CUDA_TRY(cudaEventCreate(&e));
+  if (comm_mode == OSH_COMM_NCCL && dp_size > 1) {
+    if (nccl_uid == nullptr) return osh::fail(OSH_ERR_ARG, "nccl_uid required for dp_size > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_uid, sizeof(id));
+    OSH_NCCL_TRY(ncclCommInitRank(&ctx->comm, dp_size, id, dp_rank));
+  }
+  *out = ctx.release();
+  return OSH_OK;
+}
+
+osh_status osh_ctx_destroy(osh_ctx* ctx) {
+  if (ctx == nullptr) return OSH_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->compute);
+  cudaStreamSynchronize(ctx->comm_stream);
+  free_layout(ctx);
+  if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->compute);
+  cudaStreamDestroy(ctx->comm_stream);
+  delete ctx;
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_t n,
+                              int64_t bucket_capacity, const int64_t* cuts, int32_t n_buckets,
+                              int32_t grad_dtype, int64_t workspace_bytes) {
+  if (osh_status st = check_ctx(ctx, false); st != OSH_OK) return st;
+  if (grad_dtype != OSH_GRAD_F32 && grad_dtype != OSH_GRAD_BF16)
+    return osh::fail(OSH_ERR_ARG, "grad_dtype must be OSH_GRAD_F32 or OSH_GRAD_BF16");
+  if (params == nullptr || cuts == nullptr || n < 1)
+    return osh::fail(OSH_ERR_ARG, "params and cuts are required");
+  free_layout(ctx);
+  try {
+    ctx->params.clear();
+    for (int32_t i = 0; i < n; ++i) {
+      const osh_param_desc& d = params[i];
+      if (d.id != i) throw PlanError("parameter ids must be dense 0..n-1 in order");
+      ParamSpec p;
+      p.id = d.id;
+      p.name = "p" + std::to_string(d.id);
+      p.shape.assign(d.shape, d.shape + (d.ndim == 2 ? 2 : 1));
+      p.numel = 1;
+      for (const int64_t e : p.shape) p.numel *= e;
+      p.dtype_bytes = d.dtype_bytes;
+      p.tp_splittable = d.tp_split == 1 ? TpSplit::kColumn
+                        : d.tp_split == 2 ? TpSplit::kRow
+                                          : TpSplit::kNone;
+      p.vocab_space = d.vocab_space != 0;
+      ctx->params.push_back(p);
+    }
+    ctx->layout = build_buffer_layout(ctx->params, bucket_capacity);
+    if (static_cast<int32_t>(ctx->layout.buckets.size()) != n_buckets)
+      throw PlanError("cut vectors cover " + std::to_string(n_buckets) + " buckets, layout has " +
+                      std::to_string(ctx->layout.buckets.size()));
+    const int R = ctx->size;
+    DpPartitionPlan plan;
+    plan.ranks = R;
+    plan.atomic = true;
+    ctx->cuts.assign(static_cast<size_t>(n_buckets), {});
+    for (int32_t b = 0; b < n_buckets; ++b) {
+      ctx->cuts[b].assign(cuts + static_cast<size_t>(b) * (R + 1),
+                          cuts + static_cast<size_t>(b + 1) * (R + 1));
+      plan.cut_vectors.push_back(ctx->cuts[b]);
+    }
+    detail::fill_rank_sizes(plan);
+    // structural checks of validate_plan that do not need the plan's loads
+    for (int32_t b = 0; b < n_buckets; ++b) {
+      const auto& c = ctx->cuts[b];
+      const auto edges = ctx->layout.buckets[b].atomic_boundaries();
+      if (c.front() != 0 || c.back() != ctx->layout.buckets[b].numel)
+        throw PlanError("bucket " + std::to_string(b) + ": cuts must span [0, numel]");
+      for (int r = 0; r <= R; ++r) {
+        if (r < R && c[r] > c[r + 1])
+          throw PlanError("bucket " + std::to_string(b) + ": cuts are not monotone");
+        if (!std::binary_search(edges.begin(), edges.end(), c[r]))
+          throw PlanError("bucket " + std::to_string(b) + ": cut " + std::to_string(c[r]) +
+                          " splits a tensor (Muon needs an atomic plan)");
+      }
+    }
+    const size_t np = ctx->params.size();
+    ctx->flat_off.assign(np, 0);
+    ctx->owner.assign(np, 0);
+    ctx->owned_off.assign(np, -1);
+    ctx->engine_index.assign(np, -1);
+    ctx->bucket_base.assign(static_cast<size_t>(n_buckets), 0);
+    int64_t base = 0;
+    for (int32_t b = 0; b < n_buckets; ++b) {
+      const Bucket& bk = ctx->layout.buckets[b];
+      ctx->bucket_base[b] = base;
+      for (size_t j = 0; j < bk.param_ids.size(); ++j)
+        ctx->flat_off[bk.param_ids[j]] = base + bk.param_offsets[j];
+      base += bk.numel;
+    }
+    ctx->total_numel = base;
+    ctx->owned_numel = 0;
+    int64_t alloc = 0;
+    for (size_t p = 0; p < np; ++p) {
+      ctx->owner[p] = param_owner(plan, ctx->layout, static_cast<int>(p));
+      if (ctx->owner[p] == ctx->rank) {
+        ctx->owned_off[p] = alloc;
+        alloc += (ctx->params[p].numel + kOwnedAlign - 1) / kOwnedAlign * kOwnedAlign;
+        ctx->owned_numel += ctx->params[p].numel;
+      }
+    }
+    ctx->owned_alloc = alloc;
+  } catch (const PlanError& e) {
+    return osh::fail(OSH_ERR_PLAN, std::string("osh_ctx_set_layout: ") + e.what());
+  } catch (const LayoutError& e) {
+    return osh::fail(OSH_ERR_LAYOUT, std::string("osh_ctx_set_layout: ") + e.what());
+  } catch (const std::exception& e) {
+    return osh::fail(OSH_ERR_ARG, std::string("osh_ctx_set_layout: ") + e.what());
+  }
+
+  ctx->grad_dtype = grad_dtype;
+  const size_t es = grad_esize(grad_dtype);
+  OSH_CUDA_TRY(cudaMalloc(&ctx->grad, es * static_cast<size_t>(ctx->total_numel)));
+  OSH_CUDA_TRY(cudaMalloc(&ctx->replica, 2 * static_cast<size_t>(ctx->total_numel)));
+  OSH_CUDA_TRY(cudaMemset(ctx->grad, 0, es * static_cast<size_t>(ctx->total_numel)));
+  OSH_CUDA_TRY(cudaMemset(ctx->replica, 0, 2 * static_cast<size_t>(ctx->total_numel)));
+  const size_t owned_bytes = 4 * static_cast<size_t>(std::max<int64_t>(ctx->owned_alloc, 1));
+  OSH_CUDA_TRY(cudaMalloc(&ctx->w, owned_bytes));
+  OSH_CUDA_TRY(cudaMalloc(&ctx->m, owned_bytes));
+  OSH_CUDA_TRY(cudaMemset(ctx->w, 0, owned_bytes));
+  OSH_CUDA_TRY(cudaMemset(ctx->m, 0, owned_bytes));
+
+  std::vector<osh::MuonTensorDesc> tensors;
+  for (size_t p = 0; p < ctx->params.size(); ++p) {
+    if (ctx->owned_off[p] < 0) continue;
+    const ParamSpec& ps = ctx->params[p];
+    osh::MuonTensorDesc t;
+    t.is_matrix = ps.is_matrix() ? 1 : 0;
+    t.rows = static_cast<int>(ps.shape[0]);
+    t.cols = ps.is_matrix() ? static_cast<int>(ps.shape[1]) : 1;
+    t.w = ctx->w + ctx->owned_off[p];
+    t.m = ctx->m + ctx->owned_off[p];
+    t.g = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->flat_off[p]);
+    t.replica = ctx->replica + ctx->flat_off[p];
+    ctx->engine_index[p] = static_cast<int>(tensors.size());
+    tensors.push_back(t);
+  }
+  size_t budget = workspace_bytes > 0 ? static_cast<size_t>(workspace_bytes) : 0;
+  if (budget == 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    budget = std::min<size_t>(24ull << 30, free_b / 3);
+  }
+  ctx->engine = std::make_unique<osh::MuonEngine>();
+  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget); st != OSH_OK) return st;
+  ctx->layout_ready = true;
+  return OSH_OK;
+}
+
+osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  std::memset(out, 0, sizeof(*out));
+  out->total_numel = ctx->total_numel;
+  out->owned_numel = ctx->owned_numel;
+  out->n_params = static_cast<int32_t>(ctx->params.size());
+  out->n_buckets = static_cast<int32_t>(ctx->layout.buckets.size());
+  out->n_waves = ctx->engine->num_waves();
+  out->workspace_bytes = static_cast<int64_t>(ctx->engine->workspace_bytes());
+  double flops = 0.0;
+  for (size_t p = 0; p < ctx->params.size(); ++p) {
+    if (ctx->owned_off[p] < 0) continue;
+    ++out->n_owned;
+    const ParamSpec& ps = ctx->params[p];
+    if (!ps.is_matrix()) continue;
+    const double m = static_cast<double>(std::min(ps.shape[0], ps.shape[1]));
+    const double nn = static_cast<double>(std::max(ps.shape[0], ps.shape[1]));
+    flops += 4.0 * m * m * nn + 2.0 * m * m * m;
+  }
+  out->ns_flops_per_iter = flops;
+  out->device_bytes = static_cast<int64_t>(
+      grad_esize(ctx->grad_dtype) * ctx->total_numel + 2 * ctx->total_numel +
+      8 * std::max<int64_t>(ctx->owned_alloc, 1) + ctx->engine->workspace_bytes());
+  return OSH_OK;
+}
+
+osh_status osh_ctx_buffers(osh_ctx* ctx, void** grad, void** replica) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  if (grad != nullptr) *grad = ctx->grad;
+  if (replica != nullptr) *replica = ctx->replica;
+  return OSH_OK;
+}
+
+osh_status osh_load_param(osh_ctx* ctx, int32_t pid, const float* values) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  if (pid < 0 || pid >= static_cast<int32_t>(ctx->params.size()) || values == nullptr)
+    return osh::fail(OSH_ERR_PLAN, "osh_load_param: unknown parameter");
+  const int64_t n = ctx->params[pid].numel;
+  float* stage = nullptr;
+  OSH_CUDA_TRY(cudaMalloc(&stage, 4 * static_cast<size_t>(n)));
+  OSH_CUDA_TRY(cudaMemcpy(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+  cast_f32_bf16_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(stage, ctx->replica + ctx->flat_off[pid], n);
+  if (ctx->owned_off[pid] >= 0) {
+    OSH_CUDA_TRY(cudaMemcpyAsync(ctx->w + ctx->owned_off[pid], stage, 4 * static_cast<size_t>(n),
+                                 cudaMemcpyDeviceToDevice, ctx->compute));
+    OSH_CUDA_TRY(cudaMemsetAsync(ctx->m + ctx->owned_off[pid], 0, 4 * static_cast<size_t>(n),
+                                 ctx->compute));
+  }
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+  cudaFree(stage);
+  return OSH_OK;
+}
+
+osh_status osh_write_grad(osh_ctx* ctx, int32_t pid, const float* values) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  if (pid < 0 || pid >= static_cast<int32_t>(ctx->params.size()) || values == nullptr)
+    return osh::fail(OSH_ERR_PLAN, "osh_write_grad: unknown parameter");
+  const int64_t n = ctx->params[pid].numel;
+  if (ctx->grad_dtype == OSH_GRAD_F32) {
+    OSH_CUDA_TRY(cudaMemcpy(static_cast<float*>(ctx->grad) + ctx->flat_off[pid], values,
+                            4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+    return OSH_OK;
+  }
+  float* stage = nullptr;
+  OSH_CUDA_TRY(cudaMalloc(&stage, 4 * static_cast<size_t>(n)));
+  OSH_CUDA_TRY(cudaMemcpy(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+  cast_f32_bf16_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
+      stage, static_cast<__nv_bfloat16*>(ctx->grad) + ctx->flat_off[pid], n);
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+  cudaFree(stage);
+  return OSH_OK;
+}
+
+osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float scale) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  for (size_t p = 0; p < ctx->params.size(); ++p) {
+    const ParamSpec& ps = ctx->params[p];
+    const float s = scale / std::sqrt(static_cast<float>(ps.shape[0]));
+    const long long n = ps.numel, base = ctx->flat_off[p];
+    if (what == OSH_FILL_WEIGHTS) {
+      fill_synth_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
+          seed, base, n, s, ctx->owned_off[p] >= 0 ? ctx->w + ctx->owned_off[p] : nullptr,
+          ctx->replica + base);
+      if (ctx->owned_off[p] >= 0)
+        OSH_CUDA_TRY(cudaMemsetAsync(ctx->m + ctx->owned_off[p], 0, 4 * static_cast<size_t>(n),
+                                     ctx->compute));
+    } else if (what == OSH_FILL_GRADS) {
+      if (ctx->grad_dtype == OSH_GRAD_F32)
+        fill_synth_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
+            seed, base, n, s, static_cast<float*>(ctx->grad) + base, nullptr);
+      else
+        fill_synth_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
+            seed, base, n, s, nullptr, static_cast<__nv_bfloat16*>(ctx->grad) + base);
+    } else {
+      return osh::fail(OSH_ERR_ARG, "osh_fill_synthetic: unknown target");
+    }
+  }
+  OSH_CUDA_TRY(cudaGetLastError());
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+  return OSH_OK;
+}
+
+osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
+                    void* host_replica_out) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  if (cfg == nullptr) return osh::fail(OSH_ERR_ARG, "null cfg");
+  const size_t gbytes = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->total_numel);
+  const bool dist = distributed(ctx);
+  cudaStream_t cs = ctx->compute, ns = ctx->comm_stream;
+  OSH_CUDA_TRY(cudaEventRecord(ctx->ev[5], cs));
+  if (host_grads != nullptr)
+    OSH_CUDA_TRY(cudaMemcpyAsync(ctx->grad, host_grads, gbytes, cudaMemcpyHostToDevice, cs));
+  OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
+  const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
+  const size_t es = grad_esize(ctx->grad_dtype);
+  if (dist) {
+    // RS-v: the owner of slice r of every bucket receives the sum in place.
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
+    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+      OSH_NCCL_TRY(ncclGroupStart());
+      for (int r = 0; r < ctx->size; ++r) {
+        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
+        if (cnt == 0) continue;
+        uint8_t* p = static_cast<uint8_t*>(ctx->grad) +
+                     es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
+        OSH_NCCL_TRY(ncclReduce(p, p, static_cast<size_t>(cnt), gtype, ncclSum, r, ctx->comm, ns));
+      }
+      OSH_NCCL_TRY(ncclGroupEnd());
+    }
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], ns));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[1], 0));
+  } else {
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));
+  }
+  if (osh_status st = ctx->engine->run(*cfg, cs); st != OSH_OK) return st;
+  OSH_CUDA_TRY(cudaGetLastError());
+  OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
+  if (dist) {
+    // AG-v: every owner broadcasts its updated bf16 slice of every bucket.
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
+    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+      OSH_NCCL_TRY(ncclGroupStart());
+      for (int r = 0; r < ctx->size; ++r) {
+        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
+        if (cnt == 0) continue;
+        __nv_bfloat16* p = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
+        OSH_NCCL_TRY(ncclBroadcast(p, p, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, ns));
+      }
+      OSH_NCCL_TRY(ncclGroupEnd());
+    }
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
+  } else {
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
+  }
+  if (host_replica_out != nullptr)
+    OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
+                                 2 * static_cast<size_t>(ctx->total_numel),
+                                 cudaMemcpyDeviceToHost, cs));
+  OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
+  const osh::NsLaunchStats& s = ctx->engine->stats();
+  ctx->last_timing.gemm_launches = s.launches_gemm;
+  ctx->last_timing.elementwise_launches = s.launches_elementwise;
+  ctx->last_timing.gemm_flops = s.gemm_flops;
+  if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+  return OSH_OK;
+}
+
+osh_status osh_ctx_sync(osh_ctx* ctx) {
+  if (osh_status st = check_ctx(ctx, false); st != OSH_OK) return st;
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->comm_stream));
+  if (ctx->comm != nullptr) {
+    ncclResult_t async_err = ncclSuccess;
+    OSH_NCCL_TRY(ncclCommGetAsyncError(ctx->comm, &async_err));
+    if (async_err != ncclSuccess)
+      return osh::fail(OSH_ERR_NCCL, std::string("NCCL async error: ") +
+                                         ncclGetErrorString(async_err));
+  }
+  return OSH_OK;
+}
+
+osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  auto ms = [&](int a, int b) {
+    float t = 0.f;
+    return cudaEventElapsedTime(&t, ctx->ev[a], ctx->ev[b]) == cudaSuccess ? t : -1.f;
+  };
+  osh_step_timing t = ctx->last_timing;
+  t.h2d_ms = ms(5, 0);
+  t.rs_ms = ms(0, 1);
+  t.compute_ms = ms(1, 2);
+  t.ag_ms = ms(2, 3);
+  t.d2h_ms = ms(3, 4);
+  t.total_ms = ms(5, 4);
+  *out = t;
+  return OSH_OK;
+}
+
+osh_status osh_update_norms(osh_ctx* ctx, double* out) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
+  const int nt = ctx->engine->num_tensors();
+  std::vector<double> sq(static_cast<size_t>(std::max(nt, 1)), 0.0);
+  if (nt > 0)
+    OSH_CUDA_TRY(cudaMemcpy(sq.data(), ctx->engine->update_sq(), sizeof(double) * nt,
+                            cudaMemcpyDeviceToHost));
+  for (size_t p = 0; p < ctx->params.size(); ++p)
+    out[p] = ctx->engine_index[p] >= 0 ? std::sqrt(sq[ctx->engine_index[p]]) : -1.0;
+  return OSH_OK;
+}
+
+osh_status osh_read_param(osh_ctx* ctx, int32_t pid, int32_t which, float* out) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  if (!ctx->layout_ready || pid < 0 || pid >= static_cast<int32_t>(ctx->params.size()) ||
+      out == nullptr)
+    return osh::fail(OSH_ERR_PLAN, "osh_read_param: unknown parameter");
+  const size_t n = static_cast<size_t>(ctx->params[pid].numel);
+  if (which == OSH_READ_REPLICA) {
+    std::vector<uint16_t> h(n);
+    OSH_CUDA_TRY(cudaMemcpy(h.data(), ctx->replica + ctx->flat_off[pid], 2 * n,
+                            cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) {
+      const uint32_t bits = static_cast<uint32_t>(h[i]) << 16;
+      std::memcpy(out + i, &bits, 4);
+    }
+    return OSH_OK;
+  }
+  if (ctx->owned_off[pid] < 0)
+    return osh::fail(OSH_ERR_PLAN, "osh_read_param: parameter " + std::to_string(pid) +
+                                       " is owned by rank " + std::to_string(ctx->owner[pid]));
+  const float* src = (which == OSH_READ_MASTER ? ctx->w : ctx->m) + ctx->owned_off[pid];
+  OSH_CUDA_TRY(cudaMemcpy(out, src, 4 * n, cudaMemcpyDeviceToHost));
+  return OSH_OK;
+}
+
+}  // extern "C"

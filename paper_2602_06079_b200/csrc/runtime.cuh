@@ -1,0 +1,61 @@
+// osh_ctx: one data-parallel rank of the Canzona optimizer step on one B200.
+//
+// HBM layout:
+//   grad    [total_numel]  grad dtype   the rank's local gradient buckets, flat
+//                                       in declaration order (bucket i starts at
+//                                       the sum of earlier bucket sizes); after
+//                                       the reduce-scatter the owned slices hold
+//                                       the reduced gradient (in-place ncclReduce)
+//   replica [total_numel]  bf16         the model replica every rank forwards
+//                                       with; owners write their slices, the
+//                                       all-gather (in-place ncclBroadcast)
+//                                       distributes them
+//   w, m    [owned, 256 B aligned per tensor]  fp32 master weight + momentum
+//   NS workspace (MuonEngine)
+// Step = RS-v (per bucket: one ncclReduce per rank slice, grouped) ->
+//        MuonEngine::run (owned tensors) -> AG-v (per bucket: one
+//        ncclBroadcast per rank slice, grouped). Collectives run on a comm
+//        stream; CUDA events time each phase on the stream it runs on.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "ns_engine.cuh"
+#include "optishard/optishard.hpp"
+#include "osh.h"
+
+struct osh_ctx {
+  int device = 0;
+  int rank = 0, size = 1;
+  int comm_mode = 0;  // OSH_COMM_NCCL or OSH_COMM_NONE (caller reduces; no all-gather)
+  ncclComm_t comm = nullptr;
+  cudaStream_t compute = nullptr, comm_stream = nullptr;
+  cudaEvent_t ev[8] = {};
+
+  // layout
+  std::vector<optishard::ParamSpec> params;
+  optishard::BufferLayout layout;
+  std::vector<std::vector<int64_t>> cuts;  // [bucket][R+1]
+  std::vector<int64_t> flat_off;           // per param: element offset in grad/replica
+  std::vector<int64_t> bucket_base;        // per bucket: element offset
+  std::vector<int> owner;                  // per param
+  std::vector<int64_t> owned_off;          // per param: offset in w/m (-1: not owned)
+  std::vector<int> engine_index;           // per param: tensor index in engine (-1)
+  int64_t total_numel = 0, owned_numel = 0, owned_alloc = 0;
+  int grad_dtype = 0;
+
+  void* grad = nullptr;
+  __nv_bfloat16* replica = nullptr;
+  float* w = nullptr;
+  float* m = nullptr;
+  std::unique_ptr<osh::MuonEngine> engine;
+  bool layout_ready = false;
+  osh_step_timing last_timing{};
+};

@@ -1,0 +1,142 @@
+"""Per-rank driver of the B200 Canzona optimizer step (Python mirror of the
+reference's ``run_partitioned``, proj/include/optishard/verify.hpp:225-322,
+executed for real: variable-size NCCL reduce-scatter -> owner Muon on sm_100a
+-> variable-size all-gather). All work happens in libosh.so behind the C ABI;
+this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .planner import DpPartitionPlan, ParamSpec, _desc_array
+
+GRAD_DTYPES = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
+READ = {"master": 0, "momentum": 1, "replica": 2}
+
+
+@dataclass
+class OptimizerConfig:
+    """OptimizerConfig (verify.hpp:31-35) + the quintic coefficients (:120)."""
+    lr: float = 0.02
+    beta: float = 0.9
+    ns_steps: int = 5
+    ns_a: float = 3.4445
+    ns_b: float = -4.7750
+    ns_c: float = 2.0315
+
+    def c(self) -> _lib.MuonCfgC:
+        return _lib.MuonCfgC(self.lr, self.beta, self.ns_steps, 0, self.ns_a, self.ns_b, self.ns_c)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _lib.check(_lib.lib().osh_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+class DistributedMuon:
+    """One data-parallel rank. ``comm='nccl'`` runs the real collectives
+    (dp_size > 1 needs ``nccl_uid``); ``comm='none'`` skips them: the caller
+    supplies already-reduced gradients and reads its owned results."""
+
+    def __init__(self, params: Sequence[ParamSpec], bucket_capacity: int, plan: DpPartitionPlan,
+                 rank: int = 0, device: int = 0, comm: str = "nccl",
+                 nccl_uid: Optional[bytes] = None, grad_dtype: str = "f32",
+                 workspace_bytes: int = 0):
+        L = _lib.lib()
+        self.params = list(params)
+        self.rank, self.world = rank, plan.ranks
+        self.grad_dtype = grad_dtype
+        ctx = ctypes.c_void_p()
+        uid = None
+        if nccl_uid is not None:
+            uid = ctypes.cast(ctypes.create_string_buffer(nccl_uid, 128), ctypes.c_void_p)
+        _lib.check(L.osh_ctx_create(device, rank, plan.ranks, 0 if comm == "nccl" else 1, uid,
+                                    ctypes.byref(ctx)))
+        self._ctx = ctx
+        cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)
+        _lib.check(L.osh_ctx_set_layout(ctx, _desc_array(self.params), len(self.params),
+                                        bucket_capacity,
+                                        cuts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        cuts.shape[0], GRAD_DTYPES[grad_dtype], workspace_bytes))
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if self._ctx is not None and self._ctx.value:
+            _lib.check(_lib.lib().osh_ctx_destroy(self._ctx))
+        self._ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ data
+    def info(self) -> dict:
+        i = _lib.CtxInfo()
+        _lib.check(_lib.lib().osh_ctx_get_info(self._ctx, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _lib.CtxInfo._fields_}
+
+    def buffers(self):
+        g, r = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.lib().osh_ctx_buffers(self._ctx, ctypes.byref(g), ctypes.byref(r)))
+        return g.value, r.value
+
+    @staticmethod
+    def _f32(a) -> np.ndarray:
+        return np.ascontiguousarray(np.asarray(a, dtype=np.float32)).reshape(-1)
+
+    def load_param(self, pid: int, values) -> None:
+        v = self._f32(values)
+        _lib.check(_lib.lib().osh_load_param(self._ctx, pid,
+                                             v.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+
+    def write_grad(self, pid: int, values) -> None:
+        v = self._f32(values)
+        _lib.check(_lib.lib().osh_write_grad(self._ctx, pid,
+                                             v.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+
+    def fill_synthetic(self, seed: int, what: str, scale: float = 1.0) -> None:
+        _lib.check(_lib.lib().osh_fill_synthetic(self._ctx, seed, 1 if what == "weights" else 2,
+                                                 scale))
+
+    def read_param(self, pid: int, which: str = "master") -> np.ndarray:
+        p = self.params[pid]
+        out = np.empty(p.numel, np.float32)
+        _lib.check(_lib.lib().osh_read_param(self._ctx, pid, READ[which],
+                                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return out.reshape(p.shape)
+
+    # ------------------------------------------------------------ step
+    def step(self, cfg: OptimizerConfig = OptimizerConfig(), host_grads=None,
+             host_replica_out=None) -> None:
+        """host_grads / host_replica_out: objects with a data pointer (int) —
+        e.g. pinned torch tensors' data_ptr() — or None for device-resident."""
+        c = cfg.c()
+        _lib.check(_lib.lib().osh_step(self._ctx, ctypes.byref(c), host_grads, host_replica_out))
+
+    def sync(self) -> None:
+        _lib.check(_lib.lib().osh_ctx_sync(self._ctx))
+
+    def timing(self) -> dict:
+        t = _lib.StepTiming()
+        _lib.check(_lib.lib().osh_last_timing(self._ctx, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in _lib.StepTiming._fields_}
+
+    def update_norms(self) -> np.ndarray:
+        out = np.zeros(len(self.params))
+        _lib.check(_lib.lib().osh_update_norms(
+            self._ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
