@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py — Canzona distributed Muon optimizer step, Qwen3-8B shapes, on B200.
+
+One "step" = the reference's distributed optimizer step executed for real
+(SURVEY.md §8 D1): from "every rank holds its local bf16 gradient buckets" to
+"every rank holds the updated bf16 replica": variable-size NCCL reduce-scatter
+to the alpha-balanced owners -> per-owner Muon (momentum + 5 quintic
+Newton-Schulz iterations on tcgen05 + fused weight update) -> variable-size
+NCCL all-gather. Workload: configs/qwen3-8b-like.cfg (183 tensors, 7.28e9
+params, 12 buckets of <= 622,329,856 elements), plan alpha-balanced alpha=1
+numel over N = --gpus data-parallel ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torch.distributed.run (one process per GPU); torch's gloo
+group only carries the NCCL unique id and the max-over-ranks reductions.
+Rank 0 prints ONE JSON line. `value` is the device-resident step time (CUDA
+events on the ctx's compute stream, max over ranks); `e2e` repeats the step
+through the C ABI with host (pinned) gradients in and the updated replica out.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Muon optimizer step ms (Qwen3-8B shapes) at 1/2/4/8 B200; max/mean rank load"
+CONFIG = os.path.join(ROOT, "configs", "qwen3-8b-like.cfg")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--cost", default="numel")
+    ap.add_argument("--grad-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workspace-gb", type=float, default=0.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ plumbing
+class Dist:
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.pg = td
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if not self.pg:
+            return b
+        obj = [b]
+        self.pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def gather(self, x):
+        if not self.pg:
+            return [x]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, x)
+        return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc, self.lines = None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self, n_gpus):
+        if self.proc is None:
+            return None
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= n_gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant GEMM from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ns_gemm_ncu.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_reference_step(params, plan, owners, ranks, threads=None):
+    """The reference's CPU Muon step (fp64 restatement, oracle/), timed on a
+    bounded sample: one Newton-Schulz iteration (reference 3-product form) per
+    shape class — classes with n > 12288 are timed at n = 12288 and scaled
+    linearly in n (every product is O(m^2 n)) — plus one momentum/update pass,
+    extrapolated to the full step and to each rank's owned tensors."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    fast = O.set_fast_blas(True)
+    if threads:
+        O.lib().orc_set_threads(threads)
+    classes = {}
+    for p in params:
+        if p.is_matrix:
+            m, n = min(p.shape), max(p.shape)
+            classes.setdefault((m, n), []).append(p.id)
+    per_iter = {}
+    sampled = []
+    rng = np.random.default_rng(0)
+    for (m, n) in sorted(classes):
+        ns = min(n, 12288)
+        x = rng.standard_normal((m, ns))
+        t0 = time.perf_counter()
+        O.newton_schulz(x, 1)
+        dt = time.perf_counter() - t0
+        per_iter[(m, n)] = dt * (n / ns)
+        sampled.append(f"{m}x{ns}")
+    # elementwise: momentum + update over 1e7 elements (fp64)
+    k = 10_000_000
+    w, mo, g = np.zeros((k, 1)), np.zeros((k, 1)), rng.standard_normal((k, 1))
+    t0 = time.perf_counter()
+    O.muon_apply(False, O.OptimizerConfig(), w, mo, g)
+    ew = (time.perf_counter() - t0) / k
+    rank_ms = [0.0] * ranks
+    for p in params:
+        t = ew * p.numel
+        if p.is_matrix:
+            t += 5 * per_iter[(min(p.shape), max(p.shape))]
+        rank_ms[owners[p.id]] += 1e3 * t
+    O.set_fast_blas(False)
+    return {
+        "full_ms": sum(rank_ms),
+        "rank_ms": rank_ms,
+        "critical_path_ms": max(rank_ms),
+        "cores": O.lib().orc_get_threads(),
+        "blas": "numpy OpenBLAS (ILP64 dgemm)" if fast else "exact blocked GEMM",
+        "sample": "1 NS iteration per shape class (" + ", ".join(sampled) +
+                  "; n>12288 scaled linearly in n) + 1e7-element momentum/update pass, "
+                  "extrapolated to 5 iterations x every tensor, per-rank critical path",
+    }
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(a, dist: Dist):
+    import numpy as np
+    import torch
+
+    from paper_2602_06079_b200 import planner as P
+    from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, nccl_unique_id
+
+    N = dist.world
+    torch.cuda.set_device(dist.local)
+    cfg = P.load_config(a.config)
+    params = P.generate_transformer_params(cfg)
+    cap = cfg.bucket_capacity
+    t_plan = time.perf_counter()
+    plan = P.plan_dp(params, cap, N, "alpha-balanced", a.cost, a.alpha)
+    plan_us = (time.perf_counter() - t_plan) * 1e6
+    owners = P.param_owners(params, cap, plan)
+    uid = dist.bcast_bytes(nccl_unique_id() if dist.rank == 0 and N > 1 else None)
+    eng = DistributedMuon(params, cap, plan, rank=dist.rank, device=dist.local,
+                          comm="nccl", nccl_uid=uid, grad_dtype=a.grad_dtype,
+                          workspace_bytes=int(a.workspace_gb * (1 << 30)))
+    info = eng.info()
+    eng.fill_synthetic(42, "weights")
+    eng.fill_synthetic(1000 + dist.rank, "grads")
+    ocfg = OptimizerConfig()
+    stream = torch.cuda.ExternalStream(eng.stream())
+    for _ in range(a.warmup):
+        eng.step(ocfg)
+    eng.sync()
+    dist.barrier()
+
+    clocks = ClockSampler() if dist.rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.4)
+    eng.profile_gemm(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    eng.sync()
+    dist.barrier()
+    e0.record(stream)
+    phases = []
+    for _ in range(a.steps):
+        eng.step(ocfg)
+    e1.record(stream)
+    e1.synchronize()
+    eng.sync()
+    ms = e0.elapsed_time(e1) / a.steps
+    eng.profile_gemm(False)
+    prof = eng.gemm_profile(reset=True)
+    last = eng.timing()
+    clock = clocks.stop(torch.cuda.device_count()) if clocks else None
+
+    # e2e through the C ABI with host buffers (pinned)
+    e2e = None
+    if not a.no_e2e and a.e2e_steps > 0:
+        total = info["total_numel"]
+        gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
+        hg = torch.empty(total, dtype=gdt, pin_memory=True)
+        hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
+        # host gradients: synthetic bf16/f32 values staged through the device in
+        # 256M-element chunks (outside the timed region)
+        chunk = 1 << 28
+        for off in range(0, total, chunk):
+            c = min(chunk, total - off)
+            hg[off:off + c].copy_(torch.randn(c, device="cuda", dtype=gdt).mul_(0.01))
+        torch.cuda.synchronize()
+        dist.barrier()
+        eng.sync()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.e2e_steps):
+            eng.step(ocfg, host_grads=hg.data_ptr(), host_replica_out=hr.data_ptr())
+        f1.record(stream)
+        f1.synchronize()
+        e2e_ms = f0.elapsed_time(f1) / a.e2e_steps
+        e2e = {"e2e_ms": e2e_ms, "h2d": total * hg.element_size(), "d2h": total * 2}
+        del hg, hr
+
+    rec = {"ms": ms, "prof": prof, "last": last, "info": info, "e2e": e2e,
+           "owned_numel": info["owned_numel"], "ns_flops": info["ns_flops_per_iter"] * 5}
+    allrec = dist.gather(rec)
+    eng.close()
+    if dist.rank != 0:
+        return None
+
+    peaks, peak_src = measured_peaks()
+    ms_max = max(r["ms"] for r in allrec)
+    flops = [r["ns_flops"] for r in allrec]
+    comp = [r["last"]["compute_ms"] for r in allrec]
+    numel_loads = [float(x) for x in plan.rank_loads]
+
+    def rlb(v):
+        v = [float(x) for x in v]
+        return max(v) / (sum(v) / len(v)) if sum(v) > 0 else 1.0
+
+    p0 = allrec[0]["prof"]
+    achieved = p0["flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    out = {
+        "metric": METRIC,
+        "value": round(ms_max, 3),
+        "unit": "ms",
+        "n_gpus": N,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": round(ms_max, 3),
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16 NS operands / fp32 accum+state / " + a.grad_dtype + " grads",
+        "data": "synthetic: counter-based normal weights/grads of the reference generator's shapes",
+        "config": {
+            "workload": "qwen3-8b-like Muon step (L36 h4096 f12288 v151936: 183 tensors, "
+                        f"{info['total_numel']} params, {info['n_buckets']} buckets cap {cap})",
+            "plan": f"alpha-balanced alpha={a.alpha} cost={a.cost}",
+            "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype,
+            "parallelism": f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)",
+            "l2": "inputs (weights, momentum, grads) >> 126 MB L2; no flush needed",
+        },
+        "max_mean_rank_load": {
+            "plan_numel": round(rlb(numel_loads), 4),
+            "ns_gemm_flops": round(rlb(flops), 4),
+            "measured_compute_ms": round(rlb(comp), 4),
+            "per_rank_compute_ms": [round(c, 2) for c in comp],
+        },
+        "phases_ms_rank0": {k: round(allrec[0]["last"][k], 3)
+                            for k in ("rs_ms", "compute_ms", "ag_ms", "total_ms")},
+        "gpu_launches": int(a.steps * (allrec[0]["last"]["gemm_launches"] +
+                                       allrec[0]["last"]["elementwise_launches"])),
+        "roofline": {
+            "bound": "tensor",
+            "kernel": "ns_gemm_kernel (tcgen05 UMMA 128x256, all NS GEMM launches)",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4),
+            "peak_source": peak_src + " bf16_tflops_sustained",
+            "traffic": ncu_traffic(),
+            "launches_timed": p0["launches"],
+            "gemm_ms_per_step": round(p0["ms"] / a.steps, 3),
+            "step_frac_in_gemm": round(p0["ms"] / a.steps / allrec[0]["ms"], 4),
+        },
+        "planner_us": round(plan_us, 1),
+    }
+    if clock:
+        out["clocks"] = clock
+    if allrec[0]["e2e"]:
+        e = max(r["e2e"]["e2e_ms"] for r in allrec)
+        out["e2e"] = {"value": round(e, 3), "unit": "ms",
+                      "h2d_bytes_per_step": allrec[0]["e2e"]["h2d"],
+                      "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"]}
+    if N == 1 and not a.no_cpu_baseline:
+        cb = cpu_reference_step(params, plan, owners, 1)
+        out["cpu_baseline"] = {"value": round(cb["critical_path_ms"], 1), "unit": "ms",
+                               "cores": cb["cores"], "kind": "port", "sample": cb["sample"],
+                               "extrapolated": True, "blas": cb["blas"]}
+    return out
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(a, dist: Dist):
+    if dist.rank != 0:
+        return None
+    from paper_2602_06079_b200 import planner as P
+
+    cfg = P.load_config(a.config)
+    params = P.generate_transformer_params(cfg)
+    N = dist.world
+    plan = P.plan_dp(params, cfg.bucket_capacity, N, "alpha-balanced", a.cost, a.alpha)
+    owners = P.param_owners(params, cfg.bucket_capacity, plan)
+    threads = os.cpu_count()
+    for _ in range(a.warmup):
+        cpu_reference_step(params, plan, owners, N, threads)
+    vals, last = [], None
+    for _ in range(a.steps):
+        last = cpu_reference_step(params, plan, owners, N, threads)
+        vals.append(last["critical_path_ms"])
+    v = statistics.median(vals)
+    return {
+        "metric": METRIC, "value": round(v, 1), "unit": "ms", "n_gpus": N, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(v, 1), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic normal matrices of the reference generator's shapes",
+        "config": {"workload": "qwen3-8b-like Muon step, CPU fp64 (reference algorithm)",
+                   "ranks": N, "plan": f"alpha-balanced alpha={a.alpha} cost={a.cost}"},
+        "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": last["cores"],
+                         "kind": "port", "sample": last["sample"], "blas": last["blas"]},
+        "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    a = parse_args()
+    dist = Dist()
+    if a.impl == "reference":
+        out = run_reference(a, dist)
+    else:
+        out = run_ours(a, dist)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -226,6 +226,20 @@ osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float s
 osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
                     void* host_replica_out);
 osh_status osh_ctx_sync(osh_ctx* ctx);
+/* The ctx's compute stream (cudaStream_t): the step's last event is recorded
+ * on it, so events recorded here bracket whole steps. */
+osh_status osh_ctx_stream(osh_ctx* ctx, void** stream);
+/* Optional per-GEMM-launch CUDA-event timing inside osh_step (for roofline
+ * reporting); costs two event records per launch. */
+osh_status osh_ctx_profile_gemm(osh_ctx* ctx, int32_t enable);
+typedef struct osh_gemm_profile {
+  int32_t launches;       /* GEMM launches timed since the last reset */
+  int32_t reserved_;
+  double flops;           /* algorithmic flops of those launches */
+  double ms;              /* sum of their CUDA-event durations */
+} osh_gemm_profile;
+/* Accumulated GEMM timing (synchronises); reset != 0 clears it afterwards. */
+osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t reset);
 
 typedef struct osh_step_timing {
   float h2d_ms, rs_ms, compute_ms, ag_ms, d2h_ms, total_ms; /* CUDA events */

@@ -76,6 +76,10 @@ class StepTiming(ctypes.Structure):
                 ("gemm_flops", c_double)]
 
 
+class GemmProfile(ctypes.Structure):
+    _fields_ = [("launches", c_int32), ("reserved_", c_int32), ("flops", c_double), ("ms", c_double)]
+
+
 class GemmProblem(ctypes.Structure):
     _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
                 ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
@@ -146,6 +150,9 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_last_timing", c_int32, c_void_p, POINTER(StepTiming)),
         ("osh_update_norms", c_int32, c_void_p, POINTER(c_double)),
         ("osh_read_param", c_int32, c_void_p, c_int32, c_int32, POINTER(c_float)),
+        ("osh_ctx_stream", c_int32, c_void_p, POINTER(c_void_p)),
+        ("osh_ctx_profile_gemm", c_int32, c_void_p, c_int32),
+        ("osh_gemm_profile_read", c_int32, c_void_p, POINTER(GemmProfile), c_int32),
     ]
     for name, restype, *args in optional:
         if hasattr(L, name):

@@ -34,7 +34,46 @@ NsMatrixRef ref(const void* p, int batch, int rows, int cols, long long ld) {
 
 }  // namespace
 
-MuonEngine::~MuonEngine() { release(); }
+MuonEngine::~MuonEngine() {
+  release();
+  for (const Timed& t : timed_) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (cudaEvent_t ev : event_pool_) cudaEventDestroy(ev);
+}
+
+cudaEvent_t MuonEngine::take_event() {
+  if (!event_pool_.empty()) {
+    cudaEvent_t ev = event_pool_.back();
+    event_pool_.pop_back();
+    return ev;
+  }
+  cudaEvent_t ev = nullptr;
+  cudaEventCreate(&ev);
+  return ev;
+}
+
+void MuonEngine::read_profile(int* launches, double* flops, double* ms, bool reset) {
+  *launches = 0;
+  *flops = 0.0;
+  *ms = 0.0;
+  for (const Timed& t : timed_) {
+    float dt = 0.f;
+    cudaEventSynchronize(t.b);
+    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
+    ++*launches;
+    *flops += t.flops;
+    *ms += dt;
+  }
+  if (reset) {
+    for (const Timed& t : timed_) {
+      event_pool_.push_back(t.a);
+      event_pool_.push_back(t.b);
+    }
+    timed_.clear();
+  }
+}
 
 void MuonEngine::release() {
   cudaFree(d_ws_);
@@ -278,13 +317,29 @@ osh_status MuonEngine::run(const osh_muon_cfg& cfg, cudaStream_t s) {
         upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
                                last ? d_final_ + c.slot0 : nullptr};
       }
-      cudaError_t e = ns_gemm_launch(kEpiGram, gram, np, 0.f, 0.f, 0.f, s);
+      const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b,
+                                    float l) {
+        const bool rec = profile_ && timed_.size() < 100000;
+        Timed t{};
+        if (rec) {
+          t.a = take_event();
+          t.b = take_event();
+          t.flops = ns_gemm_flops(pd, np);
+          cudaEventRecord(t.a, s);
+        }
+        const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, l, s);
+        if (rec) {
+          cudaEventRecord(t.b, s);
+          timed_.push_back(t);
+        }
+        return err;
+      };
+      cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f, 0.f);
       if (e == cudaSuccess)
-        e = ns_gemm_launch(kEpiPoly, poly, np, static_cast<float>(cfg.ns_b),
-                           static_cast<float>(cfg.ns_c), 0.f, s);
+        e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b),
+                         static_cast<float>(cfg.ns_c), 0.f);
       if (e == cudaSuccess)
-        e = ns_gemm_launch(last ? kEpiFinal : kEpiUpdate, upd, np, static_cast<float>(cfg.ns_a),
-                           0.f, lr, s);
+        e = timed_launch(last ? kEpiFinal : kEpiUpdate, upd, static_cast<float>(cfg.ns_a), 0.f, lr);
       if (e != cudaSuccess)
         return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") +
                                       cudaGetErrorString(e));

@@ -58,6 +58,10 @@ class MuonEngine {
   size_t workspace_bytes() const { return ws_bytes_; }
   const NsLaunchStats& stats() const { return stats_; }  // per run()
   int num_waves() const { return static_cast<int>(waves_.size()); }
+  // Per-launch CUDA-event timing of the GEMMs (roofline reporting).
+  void set_profile(bool on) { profile_ = on; }
+  // Sums the recorded launches (host-synchronises on the events).
+  void read_profile(int* launches, double* flops, double* ms, bool reset);
   int num_tensors() const { return n_tensors_; }
 
  private:
@@ -91,6 +95,14 @@ class MuonEngine {
   MomentumVectorTask* d_vtasks_ = nullptr;
   NsFinalTarget* d_final_ = nullptr;  // per slot
   NsLaunchStats stats_;
+  bool profile_ = false;
+  struct Timed {
+    cudaEvent_t a, b;
+    double flops;
+  };
+  std::vector<Timed> timed_;   // recorded since the last reset
+  std::vector<cudaEvent_t> event_pool_;
+  cudaEvent_t take_event();
 };
 
 }  // namespace osh

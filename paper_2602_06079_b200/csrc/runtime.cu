@@ -73,6 +73,8 @@ bool distributed(const osh_ctx* ctx) {
 void free_layout(osh_ctx* ctx) {
   ctx->engine.reset();
   cudaFree(ctx->grad);
+  cudaFree(ctx->grad_owned);
+  ctx->grad_owned = nullptr;
   cudaFree(ctx->replica);
   cudaFree(ctx->w);
   cudaFree(ctx->m);
@@ -194,6 +196,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     }
     const size_t np = ctx->params.size();
     ctx->flat_off.assign(np, 0);
+    ctx->bucket_of.assign(np, 0);
     ctx->owner.assign(np, 0);
     ctx->owned_off.assign(np, -1);
     ctx->engine_index.assign(np, -1);
@@ -202,8 +205,10 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     for (int32_t b = 0; b < n_buckets; ++b) {
       const Bucket& bk = ctx->layout.buckets[b];
       ctx->bucket_base[b] = base;
-      for (size_t j = 0; j < bk.param_ids.size(); ++j)
+      for (size_t j = 0; j < bk.param_ids.size(); ++j) {
         ctx->flat_off[bk.param_ids[j]] = base + bk.param_offsets[j];
+        ctx->bucket_of[bk.param_ids[j]] = b;
+      }
       base += bk.numel;
     }
     ctx->total_numel = base;
@@ -232,6 +237,16 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   OSH_CUDA_TRY(cudaMalloc(&ctx->replica, 2 * static_cast<size_t>(ctx->total_numel)));
   OSH_CUDA_TRY(cudaMemset(ctx->grad, 0, es * static_cast<size_t>(ctx->total_numel)));
   OSH_CUDA_TRY(cudaMemset(ctx->replica, 0, 2 * static_cast<size_t>(ctx->total_numel)));
+  // Reduced-gradient slices of this rank (NCCL mode): bucket after bucket.
+  const bool reduce_out = distributed(ctx);
+  ctx->owned_slice_off.assign(ctx->cuts.size(), 0);
+  int64_t slice_total = 0;
+  for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+    ctx->owned_slice_off[b] = slice_total;
+    slice_total += ctx->cuts[b][ctx->rank + 1] - ctx->cuts[b][ctx->rank];
+  }
+  if (reduce_out)
+    OSH_CUDA_TRY(cudaMalloc(&ctx->grad_owned, es * static_cast<size_t>(std::max<int64_t>(slice_total, 1))));
   const size_t owned_bytes = 4 * static_cast<size_t>(std::max<int64_t>(ctx->owned_alloc, 1));
   OSH_CUDA_TRY(cudaMalloc(&ctx->w, owned_bytes));
   OSH_CUDA_TRY(cudaMalloc(&ctx->m, owned_bytes));
@@ -248,7 +263,15 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     t.cols = ps.is_matrix() ? static_cast<int>(ps.shape[1]) : 1;
     t.w = ctx->w + ctx->owned_off[p];
     t.m = ctx->m + ctx->owned_off[p];
-    t.g = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->flat_off[p]);
+    if (reduce_out) {
+      // position of p inside this rank's reduced slice of its bucket
+      const int bucket = ctx->bucket_of[p];
+      const int64_t in_slice = ctx->flat_off[p] - ctx->bucket_base[bucket] - ctx->cuts[bucket][ctx->rank];
+      t.g = static_cast<uint8_t*>(ctx->grad_owned) +
+            es * static_cast<size_t>(ctx->owned_slice_off[bucket] + in_slice);
+    } else {
+      t.g = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->flat_off[p]);
+    }
     t.replica = ctx->replica + ctx->flat_off[p];
     ctx->engine_index[p] = static_cast<int>(tensors.size());
     tensors.push_back(t);
@@ -381,16 +404,21 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
   const size_t es = grad_esize(ctx->grad_dtype);
   if (dist) {
-    // RS-v: the owner of slice r of every bucket receives the sum in place.
+    // RS-v: the owner of slice r of every bucket receives the sum of all
+    // ranks' slices in its grad_owned region; local gradients stay intact.
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
     for (size_t b = 0; b < ctx->cuts.size(); ++b) {
       OSH_NCCL_TRY(ncclGroupStart());
       for (int r = 0; r < ctx->size; ++r) {
         const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
         if (cnt == 0) continue;
-        uint8_t* p = static_cast<uint8_t*>(ctx->grad) +
-                     es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
-        OSH_NCCL_TRY(ncclReduce(p, p, static_cast<size_t>(cnt), gtype, ncclSum, r, ctx->comm, ns));
+        const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) +
+                             es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
+        // only the root's recvbuff is used: this rank's reduced-slice region
+        uint8_t* dst = static_cast<uint8_t*>(ctx->grad_owned) +
+                       es * static_cast<size_t>(ctx->owned_slice_off[b]);
+        OSH_NCCL_TRY(ncclReduce(src, r == ctx->rank ? dst : nullptr, static_cast<size_t>(cnt),
+                                gtype, ncclSum, r, ctx->comm, ns));
       }
       OSH_NCCL_TRY(ncclGroupEnd());
     }
@@ -444,6 +472,28 @@ osh_status osh_ctx_sync(osh_ctx* ctx) {
       return osh::fail(OSH_ERR_NCCL, std::string("NCCL async error: ") +
                                          ncclGetErrorString(async_err));
   }
+  return OSH_OK;
+}
+
+osh_status osh_ctx_stream(osh_ctx* ctx, void** stream) {
+  if (osh_status st = check_ctx(ctx, false); st != OSH_OK) return st;
+  *stream = ctx->compute;
+  return OSH_OK;
+}
+
+osh_status osh_ctx_profile_gemm(osh_ctx* ctx, int32_t enable) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  ctx->engine->set_profile(enable != 0);
+  return OSH_OK;
+}
+
+osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t reset) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
+  std::memset(out, 0, sizeof(*out));
+  int n = 0;
+  ctx->engine->read_profile(&n, &out->flops, &out->ms, reset != 0);
+  out->launches = n;
   return OSH_OK;
 }
 

@@ -3,9 +3,9 @@
 // HBM layout:
 //   grad    [total_numel]  grad dtype   the rank's local gradient buckets, flat
 //                                       in declaration order (bucket i starts at
-//                                       the sum of earlier bucket sizes); after
-//                                       the reduce-scatter the owned slices hold
-//                                       the reduced gradient (in-place ncclReduce)
+//                                       the sum of earlier bucket sizes)
+//   grad_owned [owned]     grad dtype   (R > 1) this rank's reduced slices, bucket
+//                                       after bucket: the ncclReduce root output
 //   replica [total_numel]  bf16         the model replica every rank forwards
 //                                       with; owners write their slices, the
 //                                       all-gather (in-place ncclBroadcast)
@@ -45,6 +45,7 @@ struct osh_ctx {
   std::vector<std::vector<int64_t>> cuts;  // [bucket][R+1]
   std::vector<int64_t> flat_off;           // per param: element offset in grad/replica
   std::vector<int64_t> bucket_base;        // per bucket: element offset
+  std::vector<int> bucket_of;              // per param
   std::vector<int> owner;                  // per param
   std::vector<int64_t> owned_off;          // per param: offset in w/m (-1: not owned)
   std::vector<int> engine_index;           // per param: tensor index in engine (-1)
@@ -52,6 +53,8 @@ struct osh_ctx {
   int grad_dtype = 0;
 
   void* grad = nullptr;
+  void* grad_owned = nullptr;              // NCCL mode, R > 1: reduced owned slices
+  std::vector<int64_t> owned_slice_off;    // per bucket: offset of this rank's slice in grad_owned
   __nv_bfloat16* replica = nullptr;
   float* w = nullptr;
   float* m = nullptr;

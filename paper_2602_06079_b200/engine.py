@@ -135,6 +135,20 @@ class DistributedMuon:
         _lib.check(_lib.lib().osh_last_timing(self._ctx, ctypes.byref(t)))
         return {k: getattr(t, k) for k, _ in _lib.StepTiming._fields_}
 
+    def stream(self) -> int:
+        """cudaStream_t of the ctx's compute stream (wrap with torch.cuda.ExternalStream)."""
+        s = ctypes.c_void_p()
+        _lib.check(_lib.lib().osh_ctx_stream(self._ctx, ctypes.byref(s)))
+        return s.value or 0
+
+    def profile_gemm(self, enable: bool = True) -> None:
+        _lib.check(_lib.lib().osh_ctx_profile_gemm(self._ctx, 1 if enable else 0))
+
+    def gemm_profile(self, reset: bool = True) -> dict:
+        p = _lib.GemmProfile()
+        _lib.check(_lib.lib().osh_gemm_profile_read(self._ctx, ctypes.byref(p), 1 if reset else 0))
+        return {"launches": p.launches, "flops": p.flops, "ms": p.ms}
+
     def update_norms(self) -> np.ndarray:
         out = np.zeros(len(self.params))
         _lib.check(_lib.lib().osh_update_norms(
