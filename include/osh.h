@@ -128,6 +128,21 @@ typedef struct osh_muon_cfg {
 /* Fills cfg with the reference defaults. */
 void osh_muon_cfg_default(osh_muon_cfg* cfg);
 
+/* Single-tensor host-buffer drop-ins (fp64 host arrays, row-major, the
+ * reference's Eigen::MatrixXd values). Each call runs the GPU path on
+ * `device` (a temporary one-rank context): the NS iterate is bf16 with fp32
+ * accumulation, so results match the fp64 reference to the tolerance stated
+ * in tests/test_gpu_parity.py, not bit for bit.
+ *   osh_newton_schulz_host  newton_schulz_orthogonalize (verify.hpp:118-134):
+ *                           x (rows x cols) is replaced by its orthogonalisation
+ *   osh_muon_apply_host     muon_apply (verify.hpp:138-147): m = beta*m + g;
+ *                           matrix: w -= lr*NS(m); vector: w -= lr*m.
+ *                           *update_norm (nullable) = ||lr * update||_F */
+osh_status osh_newton_schulz_host(int32_t device, double* x, int64_t rows, int64_t cols,
+                                  int32_t steps);
+osh_status osh_muon_apply_host(int32_t device, const osh_param_desc* p, const osh_muon_cfg* cfg,
+                               double* w, double* m, const double* g, double* update_norm);
+
 /* ------------------------------------------------ kernel-level entry points
  * Device pointers; `stream` is a cudaStream_t (NULL = legacy default). */
 typedef struct osh_matrix_ref {
@@ -154,6 +169,8 @@ typedef struct osh_gemm_problem {
   osh_matrix_ref aux; /* M x N bf16 */
   const float* scale; /* per batch, nullable */
   const osh_final_target* final_targets;
+  int32_t symmetric;  /* GRAM / POLY with M == N: compute the upper triangle, mirror */
+  int32_t reserved2_;
 } osh_gemm_problem;
 
 enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3 };
@@ -235,7 +252,9 @@ osh_status osh_ctx_profile_gemm(osh_ctx* ctx, int32_t enable);
 typedef struct osh_gemm_profile {
   int32_t launches;       /* GEMM launches timed since the last reset */
   int32_t reserved_;
-  double flops;           /* algorithmic flops of those launches */
+  double flops;           /* algorithmic flops of those launches (2MNK)      */
+  double exec_flops;      /* flops the tensor cores executed (symmetric GRAM /
+                             POLY skip the tiles below the diagonal)           */
   double ms;              /* sum of their CUDA-event durations */
 } osh_gemm_profile;
 /* Accumulated GEMM timing (synchronises); reset != 0 clears it afterwards. */
@@ -254,6 +273,9 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out);
 osh_status osh_update_norms(osh_ctx* ctx, double* out);
 /* One parameter to host fp32 (OSH_READ_MASTER / _MOMENTUM: owner only). */
 osh_status osh_read_param(osh_ctx* ctx, int32_t param_id, int32_t which, float* out);
+/* Host fp32 values into the owner's master weight or momentum (which =
+ * OSH_READ_MASTER / OSH_READ_MOMENTUM; owner only; replica untouched). */
+osh_status osh_write_state(osh_ctx* ctx, int32_t param_id, int32_t which, const float* values);
 
 #ifdef __cplusplus
 }

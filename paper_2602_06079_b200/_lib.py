@@ -77,13 +77,15 @@ class StepTiming(ctypes.Structure):
 
 
 class GemmProfile(ctypes.Structure):
-    _fields_ = [("launches", c_int32), ("reserved_", c_int32), ("flops", c_double), ("ms", c_double)]
+    _fields_ = [("launches", c_int32), ("reserved_", c_int32), ("flops", c_double),
+                ("exec_flops", c_double), ("ms", c_double)]
 
 
 class GemmProblem(ctypes.Structure):
     _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
                 ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
-                ("scale", c_void_p), ("final_targets", c_void_p)]
+                ("scale", c_void_p), ("final_targets", c_void_p), ("symmetric", c_int32),
+                ("reserved2_", c_int32)]
 
 
 _lib = None

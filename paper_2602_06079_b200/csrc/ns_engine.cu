@@ -16,7 +16,7 @@ template <typename T>
 cudaError_t upload(T** dst, const std::vector<T>& src) {
   *dst = nullptr;
   if (src.empty()) return cudaSuccess;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), sizeof(T) * src.size());
+  cudaError_t e = osh::dev_alloc(reinterpret_cast<void**>(dst), sizeof(T) * src.size());
   if (e != cudaSuccess) return e;
   return cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice);
 }
@@ -54,9 +54,11 @@ cudaEvent_t MuonEngine::take_event() {
   return ev;
 }
 
-void MuonEngine::read_profile(int* launches, double* flops, double* ms, bool reset) {
+void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, double* ms,
+                              bool reset) {
   *launches = 0;
   *flops = 0.0;
+  *exec_flops = 0.0;
   *ms = 0.0;
   for (const Timed& t : timed_) {
     float dt = 0.f;
@@ -64,6 +66,7 @@ void MuonEngine::read_profile(int* launches, double* flops, double* ms, bool res
     if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
     ++*launches;
     *flops += t.flops;
+    *exec_flops += t.exec_flops;
     *ms += dt;
   }
   if (reset) {
@@ -249,14 +252,14 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   }
   n_slots_ = slot;
 
-  OSH_CUDA_TRY(cudaMalloc(&d_ws_, std::max<size_t>(ws_bytes_, 256)));
-  OSH_CUDA_TRY(cudaMemset(d_ws_, 0, std::max<size_t>(ws_bytes_, 256)));
-  OSH_CUDA_TRY(cudaMalloc(&d_partial_, sizeof(double) * static_cast<size_t>(max_tiles)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_ws_), std::max<size_t>(ws_bytes_, 256)));
+  if (!debug_poison()) OSH_CUDA_TRY(cudaMemset(d_ws_, 0, std::max<size_t>(ws_bytes_, 256)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_partial_), sizeof(double) * static_cast<size_t>(max_tiles)));
   OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
   OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
-  OSH_CUDA_TRY(cudaMalloc(&d_scale_update_, sizeof(float) * std::max(n_slots_, 1)));
-  OSH_CUDA_TRY(cudaMalloc(&d_scale_gram_, sizeof(float) * std::max(n_slots_, 1)));
-  OSH_CUDA_TRY(cudaMalloc(&d_update_sq_, sizeof(double) * std::max(n_tensors_, 1)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_scale_update_), sizeof(float) * std::max(n_slots_, 1)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_scale_gram_), sizeof(float) * std::max(n_slots_, 1)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_update_sq_), sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(cudaMemset(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1)));
   for (MomentumMatrixTask& mt : mtasks) {
     mt.x0 = reinterpret_cast<__nv_bfloat16*>(d_ws_ + reinterpret_cast<uintptr_t>(mt.x0));
@@ -312,10 +315,10 @@ osh_status MuonEngine::run(const osh_muon_cfg& cfg, cudaStream_t s) {
         NsMatrixRef Bm = ref(B, c.batch, c.m, c.m, c.ldm);
         Bm.bstride = ab;
         gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{}, first ? d_scale_gram_ + c.slot0 : nullptr,
-                                nullptr};
-        poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr};
+                                nullptr, symmetric_ ? 1 : 0};
+        poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, symmetric_ ? 1 : 0};
         upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
-                               last ? d_final_ + c.slot0 : nullptr};
+                               last ? d_final_ + c.slot0 : nullptr, 0};
       }
       const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b,
                                     float l) {
@@ -325,6 +328,7 @@ osh_status MuonEngine::run(const osh_muon_cfg& cfg, cudaStream_t s) {
           t.a = take_event();
           t.b = take_event();
           t.flops = ns_gemm_flops(pd, np);
+          t.exec_flops = ns_gemm_executed_flops(pd, np);
           cudaEventRecord(t.a, s);
         }
         const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, l, s);

@@ -61,7 +61,9 @@ class MuonEngine {
   // Per-launch CUDA-event timing of the GEMMs (roofline reporting).
   void set_profile(bool on) { profile_ = on; }
   // Sums the recorded launches (host-synchronises on the events).
-  void read_profile(int* launches, double* flops, double* ms, bool reset);
+  void read_profile(int* launches, double* flops, double* exec_flops, double* ms, bool reset);
+  // Symmetric GRAM / POLY tiles (default on; off reproduces the full GEMMs).
+  void set_symmetric(bool on) { symmetric_ = on; }
   int num_tensors() const { return n_tensors_; }
 
  private:
@@ -96,9 +98,11 @@ class MuonEngine {
   NsFinalTarget* d_final_ = nullptr;  // per slot
   NsLaunchStats stats_;
   bool profile_ = false;
+  bool symmetric_ = true;
   struct Timed {
     cudaEvent_t a, b;
     double flops;
+    double exec_flops;
   };
   std::vector<Timed> timed_;   // recorded since the last reset
   std::vector<cudaEvent_t> event_pool_;

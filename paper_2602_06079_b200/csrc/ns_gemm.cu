@@ -21,7 +21,9 @@ using namespace osh::sm100;
 constexpr uint32_t kStageBytesA = kNsBM * kNsBK * 2;  // 16 KiB
 constexpr uint32_t kStageBytesB = kNsBN * kNsBK * 2;  // 32 KiB
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kSmemBytes = 1024 + kNsStages * (kStageBytesA + kStageBytesB) + 256;
+constexpr uint32_t kEpiStageFloats = 32 * 33;  // per epilogue warp: 32x32 fp32 transpose tile
+constexpr uint32_t kSmemBytes =
+    1024 + kNsStages * (kStageBytesA + kStageBytesB) + 256 + 4 * kEpiStageFloats * 4;
 constexpr int kRasterGroup = 8;
 
 struct TileCoord {
@@ -34,9 +36,23 @@ __device__ __forceinline__ TileCoord decode_tile(const NsGemmParams& P, int t) {
   while (c.p + 1 < P.num_problems && t >= P.prob[c.p + 1].tile_start) ++c.p;
   const NsGemmProblem& pr = P.prob[c.p];
   const int local = t - pr.tile_start;
-  const int per_batch = pr.tiles_m * pr.tiles_n;
+  const int per_batch = pr.tiles_per_batch;
   c.b = local / per_batch;
-  const int rem = local - c.b * per_batch;
+  int rem = local - c.b * per_batch;
+  if (pr.symmetric) {
+    // column-major over the tiles that touch the upper triangle: column tn
+    // holds tiles tm = 0 .. min(tiles_m, 2*tn + 2) - 1 (BM = BN / 2)
+    int tn = 0;
+    for (;;) {
+      const int cnt = min(pr.tiles_m, 2 * tn + 2);
+      if (rem < cnt) break;
+      rem -= cnt;
+      ++tn;
+    }
+    c.tm = rem;
+    c.tn = tn;
+    return c;
+  }
   // grouped rasterisation: kRasterGroup tile-rows sweep one column panel
   const int span = kRasterGroup * pr.tiles_n;
   const int group = rem / span;
@@ -99,6 +115,26 @@ __device__ __forceinline__ void store_row32(__nv_bfloat16* dst, int col0, int n,
   }
 }
 
+// Symmetric output: element (row, c) is written directly when c >= row and
+// mirrored to (c, row) when c > row, so every element has exactly one writer.
+__device__ __forceinline__ void store_row32_sym(__nv_bfloat16* out, long long ld, int row,
+                                                int col0, int n, const float (&v)[32]) {
+  if (col0 >= row) {
+    store_row32(out + row * ld + col0, col0, n, v);
+  } else if (col0 + 31 >= row) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j >= row && col0 + j < n) out[row * ld + col0 + j] = __float2bfloat16_rn(v[j]);
+  }
+  if (col0 + 31 > row) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int c = col0 + j;
+      if (c > row && c < n) out[static_cast<long long>(c) * ld + row] = __float2bfloat16_rn(v[j]);
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kNsThreads, 1)
     ns_gemm_kernel(const __grid_constant__ NsGemmParams P) {
@@ -112,6 +148,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   uint64_t* tfull_bar = empty_bar + kNsStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* epi_stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -224,36 +261,80 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         tmem_ld_32x32b_x32(taddr + chunk * 32, r);
         tmem_ld_wait();
         const int col0 = c.tn * kNsBN + chunk * 32;
-        if (!row_ok || col0 >= pr.N) continue;
+        if (col0 >= pr.N) continue;  // warp-uniform
+        if (MODE != kEpiFinal && !row_ok) continue;
         float v[32];
         if constexpr (MODE == kEpiGram) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = s * __uint_as_float(r[j]);
-          store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+          if (pr.symmetric)
+            store_row32_sym(pr.out + c.b * pr.out_bstride, pr.out_ld, row, col0, pr.N, v);
+          else
+            store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiPoly) {
           load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = P.alpha * v[j] + P.beta * __uint_as_float(r[j]);
-          store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+          if (pr.symmetric)
+            store_row32_sym(pr.out + c.b * pr.out_bstride, pr.out_ld, row, col0, pr.N, v);
+          else
+            store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiUpdate) {
           load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = s * (P.alpha * v[j] + __uint_as_float(r[j]));
           store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
-        } else {  // kEpiFinal
-          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+        } else {  // kEpiFinal: every lane takes part (warp-level transpose below)
+          float upd[32];
+          if (row_ok) {
+            load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              upd[j] = (col0 + j < pr.N)
+                           ? P.lr * (s * (P.alpha * v[j] + __uint_as_float(r[j])))
+                           : 0.f;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) upd[j] = 0.f;
+          }
           const NsFinalTarget ft = pr.final_targets[c.b];
-          const int ncol = min(32, pr.N - col0);
+          if (ft.transposed) {
+            // W is X^T ([N][M]): for a fixed column the 32 lanes hold 32
+            // consecutive rows of X = 32 consecutive floats of W.
+            if (row_ok) {
+#pragma unroll 8
+              for (int j = 0; j < 32; ++j) {
+                const int col = col0 + j;
+                if (col >= pr.N) break;
+                const size_t idx = static_cast<size_t>(col) * pr.M + row;
+                const float w = ft.w[idx] - upd[j];
+                ft.w[idx] = w;
+                if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
+                sq += static_cast<double>(upd[j]) * static_cast<double>(upd[j]);
+              }
+            }
+          } else {
+            // W is X ([M][N]): transpose the warp's 32x32 block through shared
+            // memory so each access covers 32 consecutive columns of one row.
+            float* buf = epi_stage + quarter * kEpiStageFloats;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = upd[j];
+            __syncwarp();
+            const int rbase = c.tm * kNsBM + quarter * 32;
+            const int col = col0 + lane;
 #pragma unroll 4
-          for (int j = 0; j < ncol; ++j) {
-            const float upd = P.lr * (s * (P.alpha * v[j] + __uint_as_float(r[j])));
-            const int col = col0 + j;
-            const size_t idx = ft.transposed ? static_cast<size_t>(col) * pr.M + row
-                                             : static_cast<size_t>(row) * pr.N + col;
-            const float w = ft.w[idx] - upd;
-            ft.w[idx] = w;
-            if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
-            sq += static_cast<double>(upd) * static_cast<double>(upd);
+            for (int rr = 0; rr < 32; ++rr) {
+              const int rw = rbase + rr;
+              if (rw < pr.M && col < pr.N) {
+                const float u = buf[rr * 33 + lane];
+                const size_t idx = static_cast<size_t>(rw) * pr.N + col;
+                const float w = ft.w[idx] - u;
+                ft.w[idx] = w;
+                if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
+                sq += static_cast<double>(u) * static_cast<double>(u);
+              }
+            }
+            __syncwarp();
           }
         }
       }
@@ -345,6 +426,31 @@ cudaError_t launch_mode(const NsGemmParams& P, cudaStream_t stream) {
 
 }  // namespace
 
+namespace {
+int sym_tiles(int tiles_m, int tiles_n) {
+  int t = 0;
+  for (int tn = 0; tn < tiles_n; ++tn) t += std::min(tiles_m, 2 * tn + 2);
+  return t;
+}
+}  // namespace
+
+double ns_gemm_executed_flops(const NsProblemDesc* probs, int num_problems) {
+  double f = 0.0;
+  for (int i = 0; i < num_problems; ++i) {
+    const NsProblemDesc& d = probs[i];
+    const double K = d.a.cols, M = d.a.rows;
+    const double N = d.b_mn_major ? d.b.cols : d.b.rows;
+    double frac = 1.0;
+    if (d.symmetric) {
+      const int tm = (d.a.rows + kNsBM - 1) / kNsBM;
+      const int tn = (static_cast<int>(N) + kNsBN - 1) / kNsBN;
+      frac = static_cast<double>(sym_tiles(tm, tn)) / (static_cast<double>(tm) * tn);
+    }
+    f += 2.0 * M * N * K * d.a.batch * frac;
+  }
+  return f;
+}
+
 double ns_gemm_flops(const NsProblemDesc* probs, int num_problems) {
   double f = 0.0;
   for (int i = 0; i < num_problems; ++i) {
@@ -384,8 +490,11 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     }
     pr.tiles_m = (pr.M + kNsBM - 1) / kNsBM;
     pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
+    pr.symmetric = d.symmetric && pr.M == pr.N && (mode == kEpiGram || mode == kEpiPoly) ? 1 : 0;
+    if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
+    pr.tiles_per_batch = pr.symmetric ? sym_tiles(pr.tiles_m, pr.tiles_n) : pr.tiles_m * pr.tiles_n;
     pr.tile_start = tiles;
-    tiles += pr.batch * pr.tiles_m * pr.tiles_n;
+    tiles += pr.batch * pr.tiles_per_batch;
     pr.out = static_cast<__nv_bfloat16*>(const_cast<void*>(d.out.ptr));
     pr.out_ld = d.out.ld;
     pr.out_bstride = d.out.bstride;

@@ -47,7 +47,10 @@ struct alignas(64) NsGemmProblem {
   CUtensorMap tmB;  // K-major: [batch][N][K] box {64, 256, 1}; MN-major: [batch][K][N] box {64, 64, 1}
   int batch, M, N, K;
   int b_mn_major;
+  int symmetric;      // output is symmetric (M == N): only tiles touching the
+                      // upper triangle run; the epilogue mirrors them
   int tiles_m, tiles_n;
+  int tiles_per_batch;
   int tile_start;
   __nv_bfloat16* out;
   long long out_ld, out_bstride;
@@ -80,6 +83,7 @@ struct NsProblemDesc {
   NsMatrixRef aux;      // M x N (bf16) or nullptr
   const float* scale;   // device, per batch
   const NsFinalTarget* final_targets;  // device, per batch
+  int symmetric = 0;    // GRAM / POLY: out = out^T, compute the upper triangle only
 };
 
 // Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).
@@ -88,5 +92,8 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
 
 // Algorithmic flops of a problem list (2*M*N*K per batch element).
 double ns_gemm_flops(const NsProblemDesc* probs, int num_problems);
+// Flops the tensor cores actually execute (symmetric problems skip the tiles
+// strictly below the diagonal).
+double ns_gemm_executed_flops(const NsProblemDesc* probs, int num_problems);
 
 }  // namespace osh

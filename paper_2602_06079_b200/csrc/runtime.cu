@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "status.hpp"
 
@@ -233,8 +234,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
 
   ctx->grad_dtype = grad_dtype;
   const size_t es = grad_esize(grad_dtype);
-  OSH_CUDA_TRY(cudaMalloc(&ctx->grad, es * static_cast<size_t>(ctx->total_numel)));
-  OSH_CUDA_TRY(cudaMalloc(&ctx->replica, 2 * static_cast<size_t>(ctx->total_numel)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->grad), es * static_cast<size_t>(ctx->total_numel)));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->replica), 2 * static_cast<size_t>(ctx->total_numel)));
   OSH_CUDA_TRY(cudaMemset(ctx->grad, 0, es * static_cast<size_t>(ctx->total_numel)));
   OSH_CUDA_TRY(cudaMemset(ctx->replica, 0, 2 * static_cast<size_t>(ctx->total_numel)));
   // Reduced-gradient slices of this rank (NCCL mode): bucket after bucket.
@@ -246,10 +247,10 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     slice_total += ctx->cuts[b][ctx->rank + 1] - ctx->cuts[b][ctx->rank];
   }
   if (reduce_out)
-    OSH_CUDA_TRY(cudaMalloc(&ctx->grad_owned, es * static_cast<size_t>(std::max<int64_t>(slice_total, 1))));
+    OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->grad_owned), es * static_cast<size_t>(std::max<int64_t>(slice_total, 1))));
   const size_t owned_bytes = 4 * static_cast<size_t>(std::max<int64_t>(ctx->owned_alloc, 1));
-  OSH_CUDA_TRY(cudaMalloc(&ctx->w, owned_bytes));
-  OSH_CUDA_TRY(cudaMalloc(&ctx->m, owned_bytes));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->w), owned_bytes));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->m), owned_bytes));
   OSH_CUDA_TRY(cudaMemset(ctx->w, 0, owned_bytes));
   OSH_CUDA_TRY(cudaMemset(ctx->m, 0, owned_bytes));
 
@@ -284,6 +285,9 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   }
   ctx->engine = std::make_unique<osh::MuonEngine>();
   if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget); st != OSH_OK) return st;
+  // The zero-fills and table uploads above ran on the legacy stream, which the
+  // ctx's non-blocking streams do not order against: finish them now.
+  OSH_CUDA_TRY(cudaDeviceSynchronize());
   ctx->layout_ready = true;
   return OSH_OK;
 }
@@ -327,8 +331,11 @@ osh_status osh_load_param(osh_ctx* ctx, int32_t pid, const float* values) {
     return osh::fail(OSH_ERR_PLAN, "osh_load_param: unknown parameter");
   const int64_t n = ctx->params[pid].numel;
   float* stage = nullptr;
-  OSH_CUDA_TRY(cudaMalloc(&stage, 4 * static_cast<size_t>(n)));
-  OSH_CUDA_TRY(cudaMemcpy(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&stage), 4 * static_cast<size_t>(n)));
+  // Pageable H2D copies are ordered only on the stream they are issued on:
+  // stage, convert and consume on the ctx's compute stream.
+  OSH_CUDA_TRY(cudaMemcpyAsync(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice,
+                               ctx->compute));
   cast_f32_bf16_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(stage, ctx->replica + ctx->flat_off[pid], n);
   if (ctx->owned_off[pid] >= 0) {
     OSH_CUDA_TRY(cudaMemcpyAsync(ctx->w + ctx->owned_off[pid], stage, 4 * static_cast<size_t>(n),
@@ -347,13 +354,15 @@ osh_status osh_write_grad(osh_ctx* ctx, int32_t pid, const float* values) {
     return osh::fail(OSH_ERR_PLAN, "osh_write_grad: unknown parameter");
   const int64_t n = ctx->params[pid].numel;
   if (ctx->grad_dtype == OSH_GRAD_F32) {
-    OSH_CUDA_TRY(cudaMemcpy(static_cast<float*>(ctx->grad) + ctx->flat_off[pid], values,
-                            4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+    OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<float*>(ctx->grad) + ctx->flat_off[pid], values,
+                                 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice, ctx->compute));
+    OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
     return OSH_OK;
   }
   float* stage = nullptr;
-  OSH_CUDA_TRY(cudaMalloc(&stage, 4 * static_cast<size_t>(n)));
-  OSH_CUDA_TRY(cudaMemcpy(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice));
+  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&stage), 4 * static_cast<size_t>(n)));
+  OSH_CUDA_TRY(cudaMemcpyAsync(stage, values, 4 * static_cast<size_t>(n), cudaMemcpyHostToDevice,
+                               ctx->compute));
   cast_f32_bf16_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
       stage, static_cast<__nv_bfloat16*>(ctx->grad) + ctx->flat_off[pid], n);
   OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
@@ -492,7 +501,7 @@ osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t re
   if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
   std::memset(out, 0, sizeof(*out));
   int n = 0;
-  ctx->engine->read_profile(&n, &out->flops, &out->ms, reset != 0);
+  ctx->engine->read_profile(&n, &out->flops, &out->exec_flops, &out->ms, reset != 0);
   out->launches = n;
   return OSH_OK;
 }
@@ -548,6 +557,102 @@ osh_status osh_read_param(osh_ctx* ctx, int32_t pid, int32_t which, float* out) 
                                        " is owned by rank " + std::to_string(ctx->owner[pid]));
   const float* src = (which == OSH_READ_MASTER ? ctx->w : ctx->m) + ctx->owned_off[pid];
   OSH_CUDA_TRY(cudaMemcpy(out, src, 4 * n, cudaMemcpyDeviceToHost));
+  return OSH_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+osh_status osh_write_state(osh_ctx* ctx, int32_t pid, int32_t which, const float* values) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  if (!ctx->layout_ready || pid < 0 || pid >= static_cast<int32_t>(ctx->params.size()) ||
+      values == nullptr || (which != OSH_READ_MASTER && which != OSH_READ_MOMENTUM))
+    return osh::fail(OSH_ERR_PLAN, "osh_write_state: bad parameter or target");
+  if (ctx->owned_off[pid] < 0)
+    return osh::fail(OSH_ERR_PLAN, "osh_write_state: parameter " + std::to_string(pid) +
+                                       " is owned by rank " + std::to_string(ctx->owner[pid]));
+  float* dst = (which == OSH_READ_MASTER ? ctx->w : ctx->m) + ctx->owned_off[pid];
+  OSH_CUDA_TRY(cudaMemcpyAsync(dst, values, 4 * static_cast<size_t>(ctx->params[pid].numel),
+                               cudaMemcpyHostToDevice, ctx->compute));
+  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+  return OSH_OK;
+}
+
+namespace {
+
+// One-rank, one-tensor context: the single-tensor drop-ins reuse the whole
+// distributed step machinery (same kernels) on a layout of one parameter.
+osh_status one_tensor_step(int32_t device, const osh_param_desc& d, const osh_muon_cfg& cfg,
+                           double* w, double* m, const double* g, double* update_norm) {
+  osh_ctx* ctx = nullptr;
+  if (osh_status st = osh_ctx_create(device, 0, 1, OSH_COMM_NONE, nullptr, &ctx); st != OSH_OK)
+    return st;
+  struct Guard {
+    osh_ctx* c;
+    ~Guard() { osh_ctx_destroy(c); }
+  } guard{ctx};
+  osh_param_desc p = d;
+  p.id = 0;
+  const int64_t n = p.shape[0] * (p.ndim == 2 ? p.shape[1] : 1);
+  const int64_t cuts[2] = {0, n};
+  if (osh_status st = osh_ctx_set_layout(ctx, &p, 1, n, cuts, 1, OSH_GRAD_F32, 0); st != OSH_OK)
+    return st;
+  std::vector<float> buf(static_cast<size_t>(n));
+  auto put = [&](const double* src) {
+    for (int64_t i = 0; i < n; ++i) buf[i] = static_cast<float>(src[i]);
+  };
+  put(w);
+  if (osh_status st = osh_load_param(ctx, 0, buf.data()); st != OSH_OK) return st;
+  put(m);
+  if (osh_status st = osh_write_state(ctx, 0, OSH_READ_MOMENTUM, buf.data()); st != OSH_OK)
+    return st;
+  put(g);
+  if (osh_status st = osh_write_grad(ctx, 0, buf.data()); st != OSH_OK) return st;
+  if (osh_status st = osh_step(ctx, &cfg, nullptr, nullptr); st != OSH_OK) return st;
+  if (osh_status st = osh_read_param(ctx, 0, OSH_READ_MASTER, buf.data()); st != OSH_OK) return st;
+  for (int64_t i = 0; i < n; ++i) w[i] = buf[i];
+  if (osh_status st = osh_read_param(ctx, 0, OSH_READ_MOMENTUM, buf.data()); st != OSH_OK)
+    return st;
+  for (int64_t i = 0; i < n; ++i) m[i] = buf[i];
+  if (update_norm != nullptr) {
+    double norm = 0.0;
+    if (osh_status st = osh_update_norms(ctx, &norm); st != OSH_OK) return st;
+    *update_norm = norm;
+  }
+  return OSH_OK;
+}
+
+}  // namespace
+
+osh_status osh_muon_apply_host(int32_t device, const osh_param_desc* p, const osh_muon_cfg* cfg,
+                               double* w, double* m, const double* g, double* update_norm) {
+  if (p == nullptr || cfg == nullptr || w == nullptr || m == nullptr || g == nullptr)
+    return osh::fail(OSH_ERR_ARG, "osh_muon_apply_host: null argument");
+  return one_tensor_step(device, *p, *cfg, w, m, g, update_norm);
+}
+
+osh_status osh_newton_schulz_host(int32_t device, double* x, int64_t rows, int64_t cols,
+                                  int32_t steps) {
+  if (x == nullptr || rows < 1 || cols < 1) return osh::fail(OSH_ERR_ARG, "bad matrix");
+  // NS(x) through the step machinery: momentum 0, beta 0, grad x, w 0 and
+  // lr = -1 turn "w -= lr * NS(beta*m + g)" into w = NS(x).
+  osh_param_desc d{};
+  d.ndim = 2;
+  d.shape[0] = rows;
+  d.shape[1] = cols;
+  d.dtype_bytes = 4;
+  osh_muon_cfg cfg;
+  osh_muon_cfg_default(&cfg);
+  cfg.lr = -1.0;
+  cfg.beta = 0.0;
+  cfg.ns_steps = steps;
+  const size_t n = static_cast<size_t>(rows * cols);
+  std::vector<double> w(n, 0.0), m(n, 0.0);
+  if (osh_status st = one_tensor_step(device, d, cfg, w.data(), m.data(), x, nullptr);
+      st != OSH_OK)
+    return st;
+  std::memcpy(x, w.data(), sizeof(double) * n);
   return OSH_OK;
 }
 

@@ -1,5 +1,7 @@
 #include "status.hpp"
 
+#include <cstdlib>
+
 namespace osh {
 namespace {
 thread_local std::string g_last_error;
@@ -10,6 +12,23 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 osh_status fail(osh_status code, const std::string& msg) {
   g_last_error = msg;
   return code;
+}
+
+bool debug_poison() {
+  static const bool on = [] {
+    const char* v = std::getenv("OSH_DEBUG_POISON");
+    return v != nullptr && v[0] != '\0' && v[0] != '0';
+  }();
+  return on;
+}
+
+cudaError_t dev_alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess && debug_poison()) {
+    e = cudaMemset(*p, 0xFF, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  return e;
 }
 
 }  // namespace osh

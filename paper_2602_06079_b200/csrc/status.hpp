@@ -4,12 +4,20 @@
 
 #include <string>
 
+#include <cuda_runtime.h>
+
 #include "osh.h"
 
 namespace osh {
 
 void set_error(const std::string& msg);
 osh_status fail(osh_status code, const std::string& msg);
+
+// cudaMalloc that, when OSH_DEBUG_POISON is set in the environment, fills the
+// new buffer with 0xFF bytes (NaN in bf16/fp32/fp64) so reads-before-writes
+// show up; the explicit zeroing of buffers that must start at 0 is kept.
+cudaError_t dev_alloc(void** p, size_t bytes);
+bool debug_poison();
 
 }  // namespace osh
 

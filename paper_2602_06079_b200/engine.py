@@ -147,7 +147,7 @@ class DistributedMuon:
     def gemm_profile(self, reset: bool = True) -> dict:
         p = _lib.GemmProfile()
         _lib.check(_lib.lib().osh_gemm_profile_read(self._ctx, ctypes.byref(p), 1 if reset else 0))
-        return {"launches": p.launches, "flops": p.flops, "ms": p.ms}
+        return {"launches": p.launches, "flops": p.flops, "exec_flops": p.exec_flops, "ms": p.ms}
 
     def update_norms(self) -> np.ndarray:
         out = np.zeros(len(self.params))

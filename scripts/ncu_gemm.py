@@ -27,8 +27,8 @@ x = torch.randn(bt, m, n, device="cuda").mul_(0.01).bfloat16()
 a = torch.randn(bt, m, m, device="cuda").mul_(0.01).bfloat16()
 oa = torch.empty_like(a)
 ox = torch.empty_like(x)
-g = _lib.GemmProblem(); g.a = mref(x); g.b = mref(x); g.out = mref(oa)
-pl = _lib.GemmProblem(); pl.a = mref(a); pl.b = mref(a); pl.out = mref(oa); pl.aux = mref(a)
+g = _lib.GemmProblem(); g.a = mref(x); g.b = mref(x); g.out = mref(oa); g.symmetric = int('--sym' in sys.argv)
+pl = _lib.GemmProblem(); pl.a = mref(a); pl.b = mref(a); pl.out = mref(oa); pl.aux = mref(a); pl.symmetric = int('--sym' in sys.argv)
 u = _lib.GemmProblem(); u.a = mref(a); u.b = mref(x); u.b_mn_major = 1; u.out = mref(ox); u.aux = mref(x)
 for _ in range(2):  # warm-up
     run(0, g); run(1, pl, -4.775, 2.0315); run(2, u, 3.4445)

@@ -160,3 +160,47 @@ def test_grouped_problems_one_launch():
     for x, out in zip(xs, outs):
         xf = x.float()
         assert relerr(out, xf @ xf.transpose(1, 2)) < 1e-2
+
+
+@pytest.mark.parametrize("batch,m,n", [(2, 256, 768), (1, 1024, 3072), (3, 200, 300), (1, 8, 24),
+                                       (2, 640, 128)])
+def test_gram_symmetric_tiles(batch, m, n):
+    """Upper-triangle tiles + mirrored epilogue == the full product, and the
+    output is exactly symmetric (each element has a single writer)."""
+    ld = n + (-n) % 8
+    x = padded(batch, m, n, ld, scale=0.05, seed=3)
+    ldm = m + (-m) % 8
+    out = torch.full((batch, m, ldm), float("nan"), device="cuda", dtype=torch.bfloat16)
+    p = _lib.GemmProblem()
+    p.a = mref(x, cols=n)
+    p.b = mref(x, cols=n)
+    p.out = mref(out, cols=m)
+    p.symmetric = 1
+    run(0, [p])
+    o = out[:, :, :m]
+    assert not torch.isnan(o).any()
+    assert torch.equal(o, o.transpose(1, 2))
+    xf = x[:, :, :n].float()
+    assert relerr(o, xf @ xf.transpose(1, 2)) < 1e-2
+
+
+@pytest.mark.parametrize("batch,m", [(2, 512), (1, 4096), (3, 100)])
+def test_poly_symmetric_tiles(batch, m):
+    x = padded(batch, m, 2 * m, scale=0.05, seed=4)
+    a = (x.float() @ x.float().transpose(1, 2)).bfloat16()
+    a = ((a.float() + a.float().transpose(1, 2)) * 0.5).bfloat16()   # exactly symmetric input
+    ld = m + (-m) % 8
+    a_p = torch.zeros(batch, m, ld, device="cuda", dtype=torch.bfloat16)
+    a_p[:, :, :m] = a
+    out = torch.full_like(a_p, float("nan"))
+    p = _lib.GemmProblem()
+    p.a = mref(a_p, cols=m)
+    p.b = mref(a_p, cols=m)
+    p.out = mref(out, cols=m)
+    p.aux = mref(a_p, cols=m)
+    p.symmetric = 1
+    run(1, [p], alpha=B, beta=C)
+    o = out[:, :, :m]
+    assert not torch.isnan(o).any() and torch.equal(o, o.transpose(1, 2))
+    af = a.float()
+    assert relerr(o, B * af + C * af @ af) < 1e-2

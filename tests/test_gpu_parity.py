@@ -196,4 +196,5 @@ def test_bf16_gradients_close_to_fp32():
     b = run_gpu(params, 8_000_000, 1, 2, 1, grad_dtype="bf16")
     for p in params:
         rel = np.abs(a[0][p.id] - b[0][p.id]).max() / np.abs(a[0][p.id]).max()
+        print("bf16-vs-f32", p.name, rel)
         assert rel < TOL_W, (p.name, rel)
