@@ -259,6 +259,10 @@ typedef struct osh_gemm_profile {
 } osh_gemm_profile;
 /* Accumulated GEMM timing (synchronises); reset != 0 clears it afterwards. */
 osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t reset);
+/* The recorded launches as text, one per line:
+ * "<gram|poly|update|final> <ms> <flops> <executed flops> <batch x M x N x K[+...]>".
+ * Call before osh_gemm_profile_read(..., reset=1). */
+osh_status osh_gemm_profile_dump(osh_ctx* ctx, char* buf, size_t cap, size_t* len);
 
 typedef struct osh_step_timing {
   float h2d_ms, rs_ms, compute_ms, ag_ms, d2h_ms, total_ms; /* CUDA events */

@@ -2,6 +2,7 @@
 #include "ns_engine.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <map>
 #include <string>
 
@@ -41,6 +42,21 @@ MuonEngine::~MuonEngine() {
     cudaEventDestroy(t.b);
   }
   for (cudaEvent_t ev : event_pool_) cudaEventDestroy(ev);
+}
+
+std::string MuonEngine::profile_text() const {
+  static const char* kNames[] = {"gram", "poly", "update", "final"};
+  std::string out;
+  char line[256];
+  for (const Timed& t : timed_) {
+    float dt = 0.f;
+    cudaEventSynchronize(t.b);
+    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
+    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode & 3], dt, t.flops,
+                  t.exec_flops, t.what.c_str());
+    out += line;
+  }
+  return out;
 }
 
 cudaEvent_t MuonEngine::take_event() {
@@ -329,6 +345,13 @@ osh_status MuonEngine::run(const osh_muon_cfg& cfg, cudaStream_t s) {
           t.b = take_event();
           t.flops = ns_gemm_flops(pd, np);
           t.exec_flops = ns_gemm_executed_flops(pd, np);
+          t.mode = mode;
+          for (int q = 0; q < np; ++q) {
+            if (q) t.what += "+";
+            t.what += std::to_string(pd[q].a.batch) + "x" + std::to_string(pd[q].a.rows) + "x" +
+                      std::to_string(pd[q].b_mn_major ? pd[q].b.cols : pd[q].b.rows) + "x" +
+                      std::to_string(pd[q].a.cols);
+          }
           cudaEventRecord(t.a, s);
         }
         const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, l, s);

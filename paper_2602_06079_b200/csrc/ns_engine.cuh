@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include <cuda_bf16.h>
@@ -62,6 +63,8 @@ class MuonEngine {
   void set_profile(bool on) { profile_ = on; }
   // Sums the recorded launches (host-synchronises on the events).
   void read_profile(int* launches, double* flops, double* exec_flops, double* ms, bool reset);
+  // One line per recorded launch: "mode ms flops exec_flops shapes".
+  std::string profile_text() const;
   // Symmetric GRAM / POLY tiles (default on; off reproduces the full GEMMs).
   void set_symmetric(bool on) { symmetric_ = on; }
   int num_tensors() const { return n_tensors_; }
@@ -103,6 +106,8 @@ class MuonEngine {
     cudaEvent_t a, b;
     double flops;
     double exec_flops;
+    int mode;
+    std::string what;  // e.g. "2x4096x12288+36x4096x4096"
   };
   std::vector<Timed> timed_;   // recorded since the last reset
   std::vector<cudaEvent_t> event_pool_;

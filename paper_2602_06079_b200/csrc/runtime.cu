@@ -506,6 +506,19 @@ osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t re
   return OSH_OK;
 }
 
+osh_status osh_gemm_profile_dump(osh_ctx* ctx, char* buf, size_t cap, size_t* len) {
+  if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
+  if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
+  const std::string s = ctx->engine->profile_text();
+  if (len != nullptr) *len = s.size();
+  if (buf != nullptr && cap > 0) {
+    const size_t n = std::min(s.size(), cap - 1);
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return OSH_OK;
+}
+
 osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
   if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
   auto ms = [&](int a, int b) {

@@ -144,6 +144,19 @@ class DistributedMuon:
     def profile_gemm(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().osh_ctx_profile_gemm(self._ctx, 1 if enable else 0))
 
+    def gemm_profile_launches(self) -> list:
+        """Per-launch records [(mode, ms, flops, exec_flops, shapes)] since the last reset."""
+        n = ctypes.c_size_t(0)
+        L = _lib.lib()
+        _lib.check(L.osh_gemm_profile_dump(self._ctx, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _lib.check(L.osh_gemm_profile_dump(self._ctx, buf, n.value + 1, ctypes.byref(n)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            mode, ms, fl, ex, what = line.split()
+            out.append((mode, float(ms), float(fl), float(ex), what))
+        return out
+
     def gemm_profile(self, reset: bool = True) -> dict:
         p = _lib.GemmProfile()
         _lib.check(_lib.lib().osh_gemm_profile_read(self._ctx, ctypes.byref(p), 1 if reset else 0))
