@@ -264,8 +264,12 @@ osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t re
  * Call before osh_gemm_profile_read(..., reset=1). */
 osh_status osh_gemm_profile_dump(osh_ctx* ctx, char* buf, size_t cap, size_t* len);
 
+/* CUDA-event timing of the last step: h2d / d2h = host copies, rs_ms = span
+ * of the reduce-scatter (it overlaps the first waves), compute_ms = busy time
+ * of the Muon waves (excludes waiting for the RS), ag_ms = all-gather tail
+ * left exposed after the last wave, total_ms = the whole step. */
 typedef struct osh_step_timing {
-  float h2d_ms, rs_ms, compute_ms, ag_ms, d2h_ms, total_ms; /* CUDA events */
+  float h2d_ms, rs_ms, compute_ms, ag_ms, d2h_ms, total_ms;
   int32_t gemm_launches, elementwise_launches;
   double gemm_flops;
 } osh_step_timing;

@@ -93,6 +93,78 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
   if (threadIdx.x == 0) T.partial[local] = tile_sum;
 }
 
+__global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* tasks, int n_tasks,
+                                                          float lr, int use_alt) {
+  __shared__ float tile[kTile][kTile + 1];
+  __shared__ double red[8];
+  const long long t = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  ApplyTask T = tasks[lo];
+  if (use_alt) T.x = T.x_alt;
+  const long long local = t - T.tile_start;
+  const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
+  const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (T.transposed) {
+    // X is [cols][ldx]: read the 64x64 block along X's rows (= W's columns)
+#pragma unroll
+    for (int i = 0; i < kTile / 8; ++i) {
+      const int lc = ty + 8 * i;
+      const int col = c0 + lc;
+#pragma unroll
+      for (int j = 0; j < kTile / 32; ++j) {
+        const int lr = tx + 32 * j;
+        const int row = r0 + lr;
+        tile[lr][lc] = (row < T.rows && col < T.cols)
+                           ? __bfloat162float(T.x[static_cast<size_t>(col) * T.ldx + row])
+                           : 0.f;
+      }
+    }
+    __syncthreads();
+  }
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < kTile / 8; ++i) {
+    const int lr = ty + 8 * i;
+    const int row = r0 + lr;
+#pragma unroll
+    for (int j = 0; j < kTile / 32; ++j) {
+      const int lc = tx + 32 * j;
+      const int col = c0 + lc;
+      if (row < T.rows && col < T.cols) {
+        const float x = T.transposed ? tile[lr][lc]
+                                     : __bfloat162float(T.x[static_cast<size_t>(row) * T.ldx + col]);
+        const float upd = lr * x;
+        const size_t idx = static_cast<size_t>(row) * T.cols + col;
+        const float w = T.w[idx] - upd;
+        T.w[idx] = w;
+        if (T.replica != nullptr) T.replica[idx] = __float2bfloat16_rn(w);
+        sq += upd * upd;
+      }
+    }
+  }
+  const double tile_sum = block_sum(static_cast<double>(sq), red);
+  if (threadIdx.x == 0) T.partial[local] = tile_sum;
+}
+
+__global__ void __launch_bounds__(256) partial_sums_kernel(const double* partial,
+                                                           const long long* begin,
+                                                           const int* count, const int* target,
+                                                           double* out) {
+  __shared__ double red[8];
+  const int i = blockIdx.x;
+  const double* p = partial + begin[i];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < count[i]; t += 256) acc += p[t];
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) out[target[i]] = s;
+}
+
 template <typename G>
 __global__ void __launch_bounds__(256) momentum_vector_kernel(const MomentumVectorTask* tasks,
                                                               float beta, float lr) {
@@ -139,6 +211,22 @@ cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_task
     momentum_matrix_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
   else
     momentum_matrix_kernel<float><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long total_tiles,
+                                float lr, int use_alt, cudaStream_t s) {
+  if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
+  if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  apply_update_kernel<<<static_cast<unsigned>(total_tiles), 256, 0, s>>>(d_tasks, n_tasks, lr,
+                                                                          use_alt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partial_sums(const double* partial, const long long* begin, const int* count,
+                                const int* target, double* out, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  partial_sums_kernel<<<n, 256, 0, s>>>(partial, begin, count, target, out);
   return cudaGetLastError();
 }
 

@@ -46,6 +46,30 @@ struct MomentumVectorTask {
   long long n;
 };
 
+// Final Newton-Schulz output -> weight update, per 64x64 tile of W (original
+// orientation): W -= lr * X (X read transposed through smem when the tensor
+// is X^T), replica = bf16(W), per-tile sum of (lr*X)^2 for ||dW||.
+// HBM bytes per element: 2 (X) + 4 + 4 (W) + 2 (replica) = 12.
+struct ApplyTask {
+  const __nv_bfloat16* x;      // NS iterate [rows][ldx] or, transposed, [cols][ldx]
+  const __nv_bfloat16* x_alt;  // the other ping-pong buffer (odd iteration counts)
+  float* w;                // [rows][cols] fp32 master weight
+  __nv_bfloat16* replica;  // [rows][cols] bf16 replica (nullable)
+  double* partial;         // per-tile sums of (lr*x)^2 (rebased like MomentumMatrixTask)
+  int rows, cols;
+  int ldx;
+  int transposed;
+  long long tile_start;
+  int tiles_c;
+  int pad_;
+};
+
+cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long total_tiles,
+                                float lr, int use_alt, cudaStream_t s);
+// Per slot i: out[target[i]] = sum(partial[begin_i .. begin_i + count_i)) (fixed order).
+cudaError_t launch_partial_sums(const double* partial, const long long* begin, const int* count,
+                                const int* target, double* out, int n, cudaStream_t s);
+
 cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_tasks,
                                    long long total_tiles, int grad_dtype, float beta,
                                    cudaStream_t s);

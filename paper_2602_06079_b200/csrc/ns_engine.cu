@@ -22,15 +22,31 @@ cudaError_t upload(T** dst, const std::vector<T>& src) {
   return cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice);
 }
 
-NsMatrixRef ref(const void* p, int batch, int rows, int cols, long long ld) {
+NsMatrixRef ref(const void* p, int batch, int rows, int cols, long long ld, long long bstride) {
   NsMatrixRef r;
   r.ptr = p;
   r.batch = batch;
   r.rows = rows;
   r.cols = cols;
   r.ld = ld;
-  r.bstride = ld * rows;
+  r.bstride = bstride;
   return r;
+}
+
+struct Shape {
+  int m, n, ldm, ldn;
+  size_t xb, ab;  // bytes of one X / one A (256 B rounded)
+};
+
+Shape shape_of(int rows, int cols) {
+  Shape s;
+  s.m = std::min(rows, cols);
+  s.n = std::max(rows, cols);
+  s.ldm = static_cast<int>(round_up(static_cast<size_t>(s.m), 64));
+  s.ldn = static_cast<int>(round_up(static_cast<size_t>(s.n), 64));
+  s.xb = round_up(2ull * s.m * s.ldn, 256);
+  s.ab = round_up(2ull * s.m * s.ldm, 256);
+  return s;
 }
 
 }  // namespace
@@ -42,21 +58,6 @@ MuonEngine::~MuonEngine() {
     cudaEventDestroy(t.b);
   }
   for (cudaEvent_t ev : event_pool_) cudaEventDestroy(ev);
-}
-
-std::string MuonEngine::profile_text() const {
-  static const char* kNames[] = {"gram", "poly", "update", "final"};
-  std::string out;
-  char line[256];
-  for (const Timed& t : timed_) {
-    float dt = 0.f;
-    cudaEventSynchronize(t.b);
-    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
-    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode & 3], dt, t.flops,
-                  t.exec_flops, t.what.c_str());
-    out += line;
-  }
-  return out;
 }
 
 cudaEvent_t MuonEngine::take_event() {
@@ -73,9 +74,7 @@ cudaEvent_t MuonEngine::take_event() {
 void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, double* ms,
                               bool reset) {
   *launches = 0;
-  *flops = 0.0;
-  *exec_flops = 0.0;
-  *ms = 0.0;
+  *flops = *exec_flops = *ms = 0.0;
   for (const Timed& t : timed_) {
     float dt = 0.f;
     cudaEventSynchronize(t.b);
@@ -94,146 +93,150 @@ void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, 
   }
 }
 
+std::string MuonEngine::profile_text() const {
+  static const char* kNames[] = {"gram", "poly", "update", "final"};
+  std::string out;
+  char line[512];
+  for (const Timed& t : timed_) {
+    float dt = 0.f;
+    cudaEventSynchronize(t.b);
+    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
+    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode & 3], dt, t.flops,
+                  t.exec_flops, t.what.c_str());
+    out += line;
+  }
+  return out;
+}
+
 void MuonEngine::release() {
-  cudaFree(d_ws_);
-  cudaFree(d_partial_);
-  cudaFree(d_slot_begin_);
-  cudaFree(d_slot_count_);
-  cudaFree(d_scale_update_);
-  cudaFree(d_scale_gram_);
-  cudaFree(d_update_sq_);
-  cudaFree(d_mtasks_);
-  cudaFree(d_vtasks_);
-  cudaFree(d_final_);
+  for (void* p : {static_cast<void*>(d_ws_), static_cast<void*>(d_partial_),
+                  static_cast<void*>(d_slot_begin_), static_cast<void*>(d_slot_count_),
+                  static_cast<void*>(d_slot_tensor_), static_cast<void*>(d_scale_update_),
+                  static_cast<void*>(d_scale_gram_), static_cast<void*>(d_update_sq_),
+                  static_cast<void*>(d_mtasks_), static_cast<void*>(d_atasks_),
+                  static_cast<void*>(d_vtasks_)})
+    cudaFree(p);
   d_ws_ = nullptr;
   d_partial_ = d_update_sq_ = nullptr;
   d_slot_begin_ = nullptr;
-  d_slot_count_ = nullptr;
+  d_slot_count_ = d_slot_tensor_ = nullptr;
   d_scale_update_ = d_scale_gram_ = nullptr;
   d_mtasks_ = nullptr;
+  d_atasks_ = nullptr;
   d_vtasks_ = nullptr;
-  d_final_ = nullptr;
   chunks_.clear();
   waves_.clear();
 }
 
 osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int grad_dtype,
-                             size_t budget) {
+                             size_t budget, int min_waves) {
   release();
   n_tensors_ = static_cast<int>(tensors.size());
   grad_dtype_ = grad_dtype;
 
-  // ---- shape classes (m <= n), biggest total Newton-Schulz work first
-  std::map<std::pair<int, int>, std::vector<int>> classes;
-  std::vector<MomentumVectorTask> vtasks;
+  // ---- waves: consecutive tensors (declaration order) within the budget
+  size_t total_ws = 0, largest = 0;
+  for (const MuonTensorDesc& t : tensors)
+    if (t.is_matrix) {
+      const Shape s = shape_of(t.rows, t.cols);
+      total_ws += 2 * s.xb + 2 * s.ab;
+      largest = std::max(largest, 2 * s.xb + 2 * s.ab);
+    }
+  size_t cap = budget;
+  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total_ws + min_waves - 1) / min_waves));
+  if (largest > budget)
+    return fail(OSH_ERR_OOM, "MuonEngine: one matrix needs " + std::to_string(largest) +
+                                 " workspace bytes, budget is " + std::to_string(budget));
+
+  std::vector<std::vector<int>> wave_members(1);
+  std::vector<std::vector<std::pair<int, int>>> wave_classes(1);
+  size_t used = 0;
   for (int i = 0; i < n_tensors_; ++i) {
     const MuonTensorDesc& t = tensors[i];
     if (t.is_matrix) {
-      classes[{std::min(t.rows, t.cols), std::max(t.rows, t.cols)}].push_back(i);
-    } else {
-      MomentumVectorTask v{};
-      v.g = t.g;
-      v.m = t.m;
-      v.w = t.w;
-      v.replica = t.replica;
-      v.n = static_cast<long long>(t.rows) * t.cols;
-      vtasks.push_back(v);
-    }
-  }
-  std::vector<std::pair<std::pair<int, int>, std::vector<int>>> order(classes.begin(),
-                                                                        classes.end());
-  auto work = [](const std::pair<std::pair<int, int>, std::vector<int>>& c) {
-    const double m = c.first.first, n = c.first.second;
-    return (4.0 * m * m * n + 2.0 * m * m * m) * static_cast<double>(c.second.size());
-  };
-  std::stable_sort(order.begin(), order.end(),
-                   [&](const auto& x, const auto& y) { return work(x) > work(y); });
-
-  // ---- chunks within the workspace budget
-  std::vector<std::vector<int>> chunk_members;
-  for (const auto& [shape, members] : order) {
-    Chunk c;
-    c.m = shape.first;
-    c.n = shape.second;
-    c.ldm = static_cast<int>(round_up(static_cast<size_t>(c.m), 64));
-    c.ldn = static_cast<int>(round_up(static_cast<size_t>(c.n), 64));
-    const size_t per = 2 * (2ull * c.m * c.ldn) + 2 * (2ull * c.m * c.ldm);
-    const size_t cap = std::max<size_t>(1, budget / std::max<size_t>(per, 1));
-    const size_t pieces = (members.size() + cap - 1) / cap;
-    const size_t base = members.size() / pieces, extra = members.size() % pieces;
-    size_t k = 0;
-    for (size_t p = 0; p < pieces; ++p) {
-      const size_t take = base + (p < extra ? 1 : 0);
-      c.batch = static_cast<int>(take);
-      chunks_.push_back(c);
-      chunk_members.emplace_back(members.begin() + static_cast<long>(k),
-                                 members.begin() + static_cast<long>(k + take));
-      k += take;
-    }
-  }
-  auto chunk_bytes = [](const Chunk& c) {
-    return static_cast<size_t>(c.batch) *
-           (2 * round_up(2ull * c.m * c.ldn, 256) + 2 * round_up(2ull * c.m * c.ldm, 256));
-  };
-
-  // ---- waves: first-fit of chunks (largest first) into <= 4 problems / budget
-  std::vector<int> by_size(chunks_.size());
-  for (size_t i = 0; i < by_size.size(); ++i) by_size[i] = static_cast<int>(i);
-  std::stable_sort(by_size.begin(), by_size.end(), [&](int x, int y) {
-    return chunk_bytes(chunks_[x]) > chunk_bytes(chunks_[y]);
-  });
-  std::vector<size_t> wave_bytes;
-  for (const int ci : by_size) {
-    const size_t need = chunk_bytes(chunks_[ci]);
-    bool placed = false;
-    for (size_t w = 0; w < waves_.size() && !placed; ++w) {
-      if (waves_[w].chunks.size() < static_cast<size_t>(kMaxProblems) &&
-          wave_bytes[w] + need <= budget) {
-        waves_[w].chunks.push_back(ci);
-        wave_bytes[w] += need;
-        placed = true;
+      const Shape s = shape_of(t.rows, t.cols);
+      const size_t need = 2 * s.xb + 2 * s.ab;
+      const std::pair<int, int> cls{s.m, s.n};
+      auto& classes = wave_classes.back();
+      const bool new_class = std::find(classes.begin(), classes.end(), cls) == classes.end();
+      const bool has_matrix = used > 0;
+      if (has_matrix && (used + need > cap ||
+                         (new_class && classes.size() == static_cast<size_t>(kMaxProblems)))) {
+        wave_members.emplace_back();
+        wave_classes.emplace_back();
+        used = 0;
       }
+      auto& cl = wave_classes.back();
+      if (std::find(cl.begin(), cl.end(), cls) == cl.end()) cl.push_back(cls);
+      used += need;
     }
-    if (!placed) {
-      Wave w;
-      w.chunks.push_back(ci);
-      waves_.push_back(w);
-      wave_bytes.push_back(need);
-    }
+    wave_members.back().push_back(i);
   }
+  if (wave_members.back().empty()) wave_members.pop_back();
 
-  // ---- slots, workspace offsets, task tables
+  // ---- chunks (one per class per wave), slots, tables
   std::vector<MomentumMatrixTask> mtasks;
-  std::vector<NsFinalTarget> finals;
+  std::vector<ApplyTask> atasks;
+  std::vector<MomentumVectorTask> vtasks;
+  std::vector<long long> slot_begin;
+  std::vector<int> slot_count, slot_tensor;
+  long long max_tiles = 1;
   ws_bytes_ = 0;
   int slot = 0;
-  // The update norms are accumulated per tensor into d_update_sq_ (allocated
-  // below); record the tensor index now, patch pointers after allocation.
-  std::vector<int> slot_tensor;
-  std::vector<long long> slot_begin;
-  std::vector<int> slot_count;
-  long long max_tiles = 1;
-  std::vector<int> vec_tensor;
-  for (int i = 0; i < n_tensors_; ++i)
-    if (!tensors[i].is_matrix) vec_tensor.push_back(i);
-  for (Wave& w : waves_) {
-    size_t off = 0;
+  for (size_t wi = 0; wi < wave_members.size(); ++wi) {
+    const std::vector<int>& mem = wave_members[wi];
+    Wave w;
+    w.first_bucket = tensors[mem.front()].bucket;
+    w.last_bucket = tensors[mem.back()].bucket;
     w.task0 = static_cast<int>(mtasks.size());
-    for (const int ci : w.chunks) {
-      Chunk& c = chunks_[ci];
+    w.slot0 = slot;
+    w.vec0 = static_cast<int>(vtasks.size());
+    // group matrices by class, classes in order of first appearance
+    std::vector<std::pair<int, int>> order;
+    std::map<std::pair<int, int>, std::vector<int>> by_class;
+    for (const int ti : mem) {
+      const MuonTensorDesc& t = tensors[ti];
+      if (!t.is_matrix) {
+        MomentumVectorTask v{};
+        v.g = t.g;
+        v.m = t.m;
+        v.w = t.w;
+        v.replica = t.replica;
+        v.n = static_cast<long long>(t.rows) * t.cols;
+        v.sq_norm = reinterpret_cast<double*>(static_cast<uintptr_t>(ti));  // patched below
+        vtasks.push_back(v);
+        continue;
+      }
+      const Shape s = shape_of(t.rows, t.cols);
+      const std::pair<int, int> cls{s.m, s.n};
+      if (!by_class.count(cls)) order.push_back(cls);
+      by_class[cls].push_back(ti);
+    }
+    size_t off = 0;
+    for (const auto& cls : order) {
+      const std::vector<int>& members = by_class[cls];
+      const MuonTensorDesc& t0 = tensors[members.front()];
+      const Shape s = shape_of(t0.rows, t0.cols);
+      Chunk c;
+      c.m = s.m;
+      c.n = s.n;
+      c.ldm = s.ldm;
+      c.ldn = s.ldn;
+      c.batch = static_cast<int>(members.size());
       c.slot0 = slot;
-      const size_t xb = round_up(2ull * c.m * c.ldn, 256), ab = round_up(2ull * c.m * c.ldm, 256);
       c.x0 = off;
-      off += xb * c.batch;
+      off += s.xb * c.batch;
       c.x1 = off;
-      off += xb * c.batch;
+      off += s.xb * c.batch;
       c.a = off;
-      off += ab * c.batch;
+      off += s.ab * c.batch;
       c.b = off;
-      off += ab * c.batch;
+      off += s.ab * c.batch;
       for (int b = 0; b < c.batch; ++b) {
-        const int ti = chunk_members[ci][b];
+        const int ti = members[b];
         const MuonTensorDesc& t = tensors[ti];
+        const int tiles_c = (t.cols + kTile - 1) / kTile;
+        const long long ntiles = static_cast<long long>((t.rows + kTile - 1) / kTile) * tiles_c;
         MomentumMatrixTask mt{};
         mt.g = t.g;
         mt.m = t.m;
@@ -241,140 +244,153 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         mt.cols = t.cols;
         mt.ldx = c.ldn;
         mt.transposed = t.rows > t.cols ? 1 : 0;
-        mt.tiles_c = (t.cols + kTile - 1) / kTile;
+        mt.tiles_c = tiles_c;
         mt.tile_start = w.tiles;
-        // x0 patched once the workspace base is known (offset stored as ptr)
-        mt.x0 = reinterpret_cast<__nv_bfloat16*>(c.x0 + static_cast<size_t>(b) * (xb));
-        const long long ntiles = static_cast<long long>((t.rows + kTile - 1) / kTile) * mt.tiles_c;
-        // per-tile partial sums live at [tile_start, tile_start + ntiles) of
-        // the wave's partial array; the task's pointer is rebased below
-        mt.partial = nullptr;
+        // workspace / partial pointers are offsets until the buffers exist
+        mt.x0 = reinterpret_cast<__nv_bfloat16*>(c.x0 + static_cast<size_t>(b) * s.xb);
+        ApplyTask at{};
+        at.x = reinterpret_cast<const __nv_bfloat16*>(c.x0 + static_cast<size_t>(b) * s.xb);
+        at.x_alt = reinterpret_cast<const __nv_bfloat16*>(c.x1 + static_cast<size_t>(b) * s.xb);
+        at.w = t.w;
+        at.replica = t.replica;
+        at.rows = t.rows;
+        at.cols = t.cols;
+        at.ldx = c.ldn;
+        at.transposed = mt.transposed;
+        at.tile_start = w.tiles;
+        at.tiles_c = tiles_c;
+        mtasks.push_back(mt);
+        atasks.push_back(at);
         slot_begin.push_back(w.tiles);
         slot_count.push_back(static_cast<int>(ntiles));
-        w.tiles += ntiles;
-        mtasks.push_back(mt);
-        NsFinalTarget ft{};
-        ft.w = t.w;
-        ft.replica = t.replica;
-        ft.transposed = mt.transposed;
-        finals.push_back(ft);
         slot_tensor.push_back(ti);
+        w.tiles += ntiles;
         ++slot;
       }
+      w.chunks.push_back(static_cast<int>(chunks_.size()));
+      chunks_.push_back(c);
     }
     w.n_tasks = static_cast<int>(mtasks.size()) - w.task0;
+    w.n_slots = slot - w.slot0;
+    w.n_vec = static_cast<int>(vtasks.size()) - w.vec0;
     ws_bytes_ = std::max(ws_bytes_, off);
     max_tiles = std::max(max_tiles, w.tiles);
+    waves_.push_back(w);
   }
   n_slots_ = slot;
 
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_ws_), std::max<size_t>(ws_bytes_, 256)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_ws_), std::max<size_t>(ws_bytes_, 256)));
   if (!debug_poison()) OSH_CUDA_TRY(cudaMemset(d_ws_, 0, std::max<size_t>(ws_bytes_, 256)));
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_partial_), sizeof(double) * static_cast<size_t>(max_tiles)));
-  OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
-  OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_scale_update_), sizeof(float) * std::max(n_slots_, 1)));
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_scale_gram_), sizeof(float) * std::max(n_slots_, 1)));
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&d_update_sq_), sizeof(double) * std::max(n_tensors_, 1)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_partial_),
+                         sizeof(double) * static_cast<size_t>(max_tiles)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_scale_update_),
+                         sizeof(float) * std::max(n_slots_, 1)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_scale_gram_),
+                         sizeof(float) * std::max(n_slots_, 1)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_update_sq_),
+                         sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(cudaMemset(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1)));
   for (MomentumMatrixTask& mt : mtasks) {
     mt.x0 = reinterpret_cast<__nv_bfloat16*>(d_ws_ + reinterpret_cast<uintptr_t>(mt.x0));
     mt.partial = d_partial_ + mt.tile_start;  // local tile index is added in-kernel
   }
-  for (size_t s = 0; s < finals.size(); ++s) finals[s].sq_norm = d_update_sq_ + slot_tensor[s];
-  for (size_t v = 0; v < vtasks.size(); ++v) vtasks[v].sq_norm = d_update_sq_ + vec_tensor[v];
-  n_vec_tasks_ = static_cast<int>(vtasks.size());
+  for (ApplyTask& at : atasks) {
+    at.x = reinterpret_cast<const __nv_bfloat16*>(d_ws_ + reinterpret_cast<uintptr_t>(at.x));
+    at.x_alt = reinterpret_cast<const __nv_bfloat16*>(d_ws_ + reinterpret_cast<uintptr_t>(at.x_alt));
+    at.partial = d_partial_ + at.tile_start;
+  }
+  for (MomentumVectorTask& v : vtasks)
+    v.sq_norm = d_update_sq_ + reinterpret_cast<uintptr_t>(v.sq_norm);
   OSH_CUDA_TRY(upload(&d_mtasks_, mtasks));
+  OSH_CUDA_TRY(upload(&d_atasks_, atasks));
   OSH_CUDA_TRY(upload(&d_vtasks_, vtasks));
-  OSH_CUDA_TRY(upload(&d_final_, finals));
+  OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
+  OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
+  OSH_CUDA_TRY(upload(&d_slot_tensor_, slot_tensor));
+  OSH_CUDA_TRY(cudaDeviceSynchronize());
   return OSH_OK;
 }
 
-osh_status MuonEngine::run(const osh_muon_cfg& cfg, cudaStream_t s) {
-  if (cfg.ns_steps < 1 && n_slots_ > 0)
-    return fail(OSH_ERR_UNSUPPORTED, "MuonEngine: ns_steps must be >= 1 on the GPU path");
+osh_status MuonEngine::begin_step(cudaStream_t s) {
   stats_ = NsLaunchStats{};
-  const float beta = static_cast<float>(cfg.beta), lr = static_cast<float>(cfg.lr);
   OSH_CUDA_TRY(cudaMemsetAsync(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1), s));
-  if (n_vec_tasks_ > 0) {
-    OSH_CUDA_TRY(launch_momentum_vector(d_vtasks_, n_vec_tasks_, grad_dtype_, beta, lr, s));
+  return OSH_OK;
+}
+
+osh_status MuonEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
+  const Wave& w = waves_[wi];
+  if (cfg.ns_steps < 1 && w.n_slots > 0)
+    return fail(OSH_ERR_UNSUPPORTED, "MuonEngine: ns_steps must be >= 1 on the GPU path");
+  const float beta = static_cast<float>(cfg.beta), lr = static_cast<float>(cfg.lr);
+  if (w.n_vec > 0) {
+    OSH_CUDA_TRY(launch_momentum_vector(d_vtasks_ + w.vec0, w.n_vec, grad_dtype_, beta, lr, s));
     ++stats_.launches_elementwise;
   }
-  for (const Wave& w : waves_) {
-    OSH_CUDA_TRY(launch_momentum_matrix(d_mtasks_ + w.task0, w.n_tasks, w.tiles, grad_dtype_,
-                                        beta, s));
-    const int slot0 = chunks_[w.chunks.front()].slot0;
-    int nslots = 0;
-    for (const int ci : w.chunks) nslots += chunks_[ci].batch;
-    // slots of a wave are contiguous (assigned wave by wave, chunk by chunk)
-    OSH_CUDA_TRY(launch_ns_scales(d_partial_, d_slot_begin_ + slot0, d_slot_count_ + slot0,
-                                  d_scale_update_ + slot0, d_scale_gram_ + slot0, nslots, s));
-    stats_.launches_elementwise += 2;
-    const int np = static_cast<int>(w.chunks.size());
-    for (int it = 0; it < cfg.ns_steps; ++it) {
-      const bool first = it == 0, last = it == cfg.ns_steps - 1;
-      NsProblemDesc gram[kMaxProblems], poly[kMaxProblems], upd[kMaxProblems];
-      for (int q = 0; q < np; ++q) {
-        const Chunk& c = chunks_[w.chunks[q]];
-        uint8_t* xin = d_ws_ + ((it & 1) ? c.x1 : c.x0);
-        uint8_t* xout = d_ws_ + ((it & 1) ? c.x0 : c.x1);
-        uint8_t* A = d_ws_ + c.a;
-        uint8_t* B = d_ws_ + c.b;
-        const long long xb = static_cast<long long>(round_up(2ull * c.m * c.ldn, 256) / 2);
-        const long long ab = static_cast<long long>(round_up(2ull * c.m * c.ldm, 256) / 2);
-        NsMatrixRef X = ref(xin, c.batch, c.m, c.n, c.ldn);
-        X.bstride = xb;
-        NsMatrixRef Xo = ref(xout, c.batch, c.m, c.n, c.ldn);
-        Xo.bstride = xb;
-        NsMatrixRef Am = ref(A, c.batch, c.m, c.m, c.ldm);
-        Am.bstride = ab;
-        NsMatrixRef Bm = ref(B, c.batch, c.m, c.m, c.ldm);
-        Bm.bstride = ab;
-        gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{}, first ? d_scale_gram_ + c.slot0 : nullptr,
-                                nullptr, symmetric_ ? 1 : 0};
-        poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, symmetric_ ? 1 : 0};
-        upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
-                               last ? d_final_ + c.slot0 : nullptr, 0};
-      }
-      const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b,
-                                    float l) {
-        const bool rec = profile_ && timed_.size() < 100000;
-        Timed t{};
-        if (rec) {
-          t.a = take_event();
-          t.b = take_event();
-          t.flops = ns_gemm_flops(pd, np);
-          t.exec_flops = ns_gemm_executed_flops(pd, np);
-          t.mode = mode;
-          for (int q = 0; q < np; ++q) {
-            if (q) t.what += "+";
-            t.what += std::to_string(pd[q].a.batch) + "x" + std::to_string(pd[q].a.rows) + "x" +
-                      std::to_string(pd[q].b_mn_major ? pd[q].b.cols : pd[q].b.rows) + "x" +
-                      std::to_string(pd[q].a.cols);
-          }
-          cudaEventRecord(t.a, s);
-        }
-        const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, l, s);
-        if (rec) {
-          cudaEventRecord(t.b, s);
-          timed_.push_back(t);
-        }
-        return err;
-      };
-      cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f, 0.f);
-      if (e == cudaSuccess)
-        e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b),
-                         static_cast<float>(cfg.ns_c), 0.f);
-      if (e == cudaSuccess)
-        e = timed_launch(last ? kEpiFinal : kEpiUpdate, upd, static_cast<float>(cfg.ns_a), 0.f, lr);
-      if (e != cudaSuccess)
-        return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") +
-                                      cudaGetErrorString(e));
-      stats_.launches_gemm += 3;
-      stats_.gemm_flops += ns_gemm_flops(gram, np) + ns_gemm_flops(poly, np) +
-                           ns_gemm_flops(upd, np);
+  if (w.n_tasks == 0) return OSH_OK;
+  OSH_CUDA_TRY(launch_momentum_matrix(d_mtasks_ + w.task0, w.n_tasks, w.tiles, grad_dtype_, beta, s));
+  OSH_CUDA_TRY(launch_ns_scales(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
+                                d_scale_update_ + w.slot0, d_scale_gram_ + w.slot0, w.n_slots, s));
+  stats_.launches_elementwise += 2;
+  const int np = static_cast<int>(w.chunks.size());
+  for (int it = 0; it < cfg.ns_steps; ++it) {
+    const bool first = it == 0;
+    NsProblemDesc gram[kMaxProblems], poly[kMaxProblems], upd[kMaxProblems];
+    for (int q = 0; q < np; ++q) {
+      const Chunk& c = chunks_[w.chunks[q]];
+      const Shape sh = shape_of(c.m, c.n);
+      uint8_t* xin = d_ws_ + ((it & 1) ? c.x1 : c.x0);
+      uint8_t* xout = d_ws_ + ((it & 1) ? c.x0 : c.x1);
+      const long long xbs = static_cast<long long>(sh.xb / 2), abs = static_cast<long long>(sh.ab / 2);
+      const NsMatrixRef X = ref(xin, c.batch, c.m, c.n, c.ldn, xbs);
+      const NsMatrixRef Xo = ref(xout, c.batch, c.m, c.n, c.ldn, xbs);
+      const NsMatrixRef Am = ref(d_ws_ + c.a, c.batch, c.m, c.m, c.ldm, abs);
+      const NsMatrixRef Bm = ref(d_ws_ + c.b, c.batch, c.m, c.m, c.ldm, abs);
+      const int sym = symmetric_ ? 1 : 0;
+      gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{},
+                              first ? d_scale_gram_ + c.slot0 : nullptr, nullptr, sym};
+      poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, sym};
+      upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
+                             nullptr, 0};
     }
+    const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b) {
+      const bool rec = profile_ && timed_.size() < 100000;
+      Timed t{};
+      if (rec) {
+        t.a = take_event();
+        t.b = take_event();
+        t.flops = ns_gemm_flops(pd, np);
+        t.exec_flops = ns_gemm_executed_flops(pd, np);
+        t.mode = mode;
+        for (int q = 0; q < np; ++q) {
+          if (q) t.what += "+";
+          t.what += std::to_string(pd[q].a.batch) + "x" + std::to_string(pd[q].a.rows) + "x" +
+                    std::to_string(pd[q].b_mn_major ? pd[q].b.cols : pd[q].b.rows) + "x" +
+                    std::to_string(pd[q].a.cols);
+        }
+        cudaEventRecord(t.a, s);
+      }
+      const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, 0.f, s);
+      if (rec) {
+        cudaEventRecord(t.b, s);
+        timed_.push_back(std::move(t));
+      }
+      stats_.gemm_flops += ns_gemm_flops(pd, np);
+      return err;
+    };
+    cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f);
+    if (e == cudaSuccess)
+      e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b), static_cast<float>(cfg.ns_c));
+    if (e == cudaSuccess) e = timed_launch(kEpiUpdate, upd, static_cast<float>(cfg.ns_a), 0.f);
+    if (e != cudaSuccess)
+      return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") + cudaGetErrorString(e));
+    stats_.launches_gemm += 3;
   }
+  // after k iterations the iterate sits in X0 (k even) or X1 (k odd)
+  OSH_CUDA_TRY(launch_apply_update(d_atasks_ + w.task0, w.n_tasks, w.tiles, lr,
+                                   cfg.ns_steps & 1, s));
+  OSH_CUDA_TRY(launch_partial_sums(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
+                                   d_slot_tensor_ + w.slot0, d_update_sq_, w.n_slots, s));
+  stats_.launches_elementwise += 2;
   return OSH_OK;
 }
 

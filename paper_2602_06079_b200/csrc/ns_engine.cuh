@@ -1,15 +1,18 @@
 // MuonEngine: the per-rank Muon update of a fixed set of owned tensors.
 //
-// Built once per layout (the plan never changes between steps): matrices are
-// grouped into shape classes (m = min side, n = max side), classes are cut
-// into chunks that fit the Newton-Schulz workspace budget, and chunks are
-// packed up to kMaxProblems per "wave". A step is then, per wave:
-//   momentum_matrix (m = beta*m + g, ||m||^2, X0 = bf16 m)  -> ns_scales ->
-//   k x { GRAM, POLY, UPDATE }  with the last UPDATE fused into the weight
-//   update (FINAL: W -= lr*X_k, bf16 replica, ||dW||^2)
-// plus one momentum_vector launch for every 1-D tensor. All task tables live
-// in device memory and are reused every step (no host work on the hot path
-// beyond the launches themselves).
+// Built once per layout (the plan never changes between steps). Owned tensors
+// are taken in declaration order (= bucket order) and cut into WAVES that fit
+// the Newton-Schulz workspace; inside a wave, matrices of the same shape
+// class (m = min side, n = max side) form one batched problem of a grouped
+// GEMM launch (<= kMaxProblems classes per wave). Because waves follow bucket
+// order, the runtime can start a wave as soon as the reduce-scatter of its
+// last bucket has landed and all-gather a bucket as soon as the wave that
+// finishes it is done (runtime.cu). One wave of a step is:
+//   momentum_vector (1-D tensors) ; momentum_matrix (m = beta*m + g, tile
+//   sums of m^2, X0 = bf16 m) -> ns_scales -> k x {GRAM, POLY, UPDATE}
+//   -> apply_update (W -= lr*X_k, bf16 replica, tile sums of |dW|^2)
+//   -> partial_sums (||dW||^2 per tensor, fixed order)
+// All task tables live in device memory and are reused every step.
 #pragma once
 
 #include <cstdint>
@@ -28,6 +31,7 @@ namespace osh {
 struct MuonTensorDesc {
   int rows = 0, cols = 1;   // cols == 1 and !is_matrix for vectors
   int is_matrix = 0;
+  int bucket = 0;           // bucket index (declaration order)
   float* w = nullptr;       // fp32 master weight [rows][cols]
   float* m = nullptr;       // fp32 momentum
   const void* g = nullptr;  // reduced gradient (grad dtype of the engine)
@@ -37,8 +41,7 @@ struct MuonTensorDesc {
 struct NsLaunchStats {
   int launches_gemm = 0;
   int launches_elementwise = 0;
-  double gemm_flops = 0.0;      // algorithmic 2MNK of the launched GEMMs
-  double elementwise_bytes = 0.0;
+  double gemm_flops = 0.0;  // algorithmic 2MNK of the launched GEMMs
 };
 
 class MuonEngine {
@@ -48,70 +51,77 @@ class MuonEngine {
   MuonEngine(const MuonEngine&) = delete;
   MuonEngine& operator=(const MuonEngine&) = delete;
 
-  // Plans classes / chunks / waves and allocates device tables + workspace.
+  // tensors must be in declaration order. min_waves > 1 cuts the work into at
+  // least that many waves (finer RS/AG overlap) when tensors allow.
   osh_status build(const std::vector<MuonTensorDesc>& tensors, int grad_dtype,
-                   size_t workspace_budget_bytes);
-  // One Muon update of every tensor on `stream`.
-  osh_status run(const osh_muon_cfg& cfg, cudaStream_t stream);
+                   size_t workspace_budget_bytes, int min_waves);
+  osh_status begin_step(cudaStream_t stream);  // clears the update norms / stats
+  osh_status run_wave(int w, const osh_muon_cfg& cfg, cudaStream_t stream);
 
-  // ||lr * update||^2 of tensor i from the last run (device array).
+  int num_waves() const { return static_cast<int>(waves_.size()); }
+  int wave_first_bucket(int w) const { return waves_[w].first_bucket; }
+  int wave_last_bucket(int w) const { return waves_[w].last_bucket; }
+
+  // ||lr * update||^2 of tensor i from the last step (device array).
   const double* update_sq() const { return d_update_sq_; }
   size_t workspace_bytes() const { return ws_bytes_; }
-  const NsLaunchStats& stats() const { return stats_; }  // per run()
-  int num_waves() const { return static_cast<int>(waves_.size()); }
+  const NsLaunchStats& stats() const { return stats_; }  // since begin_step()
+  int num_tensors() const { return n_tensors_; }
+
   // Per-launch CUDA-event timing of the GEMMs (roofline reporting).
   void set_profile(bool on) { profile_ = on; }
-  // Sums the recorded launches (host-synchronises on the events).
   void read_profile(int* launches, double* flops, double* exec_flops, double* ms, bool reset);
   // One line per recorded launch: "mode ms flops exec_flops shapes".
   std::string profile_text() const;
   // Symmetric GRAM / POLY tiles (default on; off reproduces the full GEMMs).
   void set_symmetric(bool on) { symmetric_ = on; }
-  int num_tensors() const { return n_tensors_; }
 
  private:
   struct Chunk {
     int m = 0, n = 0, ldm = 0, ldn = 0, batch = 0;
-    int slot0 = 0;  // first matrix slot (slots are chunk-contiguous)
+    int slot0 = 0;                        // first matrix slot (chunk-contiguous)
     size_t x0 = 0, x1 = 0, a = 0, b = 0;  // byte offsets in the workspace
   };
   struct Wave {
     std::vector<int> chunks;
-    int task0 = 0, n_tasks = 0;  // momentum_matrix tasks
+    int first_bucket = 0, last_bucket = 0;
+    int task0 = 0, n_tasks = 0;  // momentum / apply tasks (same geometry)
     long long tiles = 0;
+    int slot0 = 0, n_slots = 0;
+    int vec0 = 0, n_vec = 0;
+  };
+  struct Timed {
+    cudaEvent_t a, b;
+    double flops;
+    double exec_flops;
+    int mode;
+    std::string what;  // e.g. "54x4096x4096x12288+2x4096x4096x151936"
   };
   void release();
+  cudaEvent_t take_event();
 
   int n_tensors_ = 0;
   int grad_dtype_ = kGradF32;
   std::vector<Chunk> chunks_;
   std::vector<Wave> waves_;
   int n_slots_ = 0;
-  int n_vec_tasks_ = 0;
   size_t ws_bytes_ = 0;
   uint8_t* d_ws_ = nullptr;
-  double* d_partial_ = nullptr;      // per momentum tile of the largest wave
-  long long* d_slot_begin_ = nullptr;  // per slot: first partial (wave-relative)
-  int* d_slot_count_ = nullptr;        // per slot: number of partials
-  float* d_scale_update_ = nullptr;  // per slot
-  float* d_scale_gram_ = nullptr;    // per slot
-  double* d_update_sq_ = nullptr;    // per tensor
+  double* d_partial_ = nullptr;        // per momentum / apply tile of the largest wave
+  long long* d_slot_begin_ = nullptr;  // per slot: first tile (wave-relative)
+  int* d_slot_count_ = nullptr;        // per slot: tiles
+  int* d_slot_tensor_ = nullptr;       // per slot: tensor index
+  float* d_scale_update_ = nullptr;    // per slot
+  float* d_scale_gram_ = nullptr;      // per slot
+  double* d_update_sq_ = nullptr;      // per tensor
   MomentumMatrixTask* d_mtasks_ = nullptr;
+  ApplyTask* d_atasks_ = nullptr;
   MomentumVectorTask* d_vtasks_ = nullptr;
-  NsFinalTarget* d_final_ = nullptr;  // per slot
   NsLaunchStats stats_;
   bool profile_ = false;
   bool symmetric_ = true;
-  struct Timed {
-    cudaEvent_t a, b;
-    double flops;
-    double exec_flops;
-    int mode;
-    std::string what;  // e.g. "2x4096x12288+36x4096x4096"
-  };
-  std::vector<Timed> timed_;   // recorded since the last reset
+  std::vector<Timed> timed_;
   std::vector<cudaEvent_t> event_pool_;
-  cudaEvent_t take_event();
 };
 
 }  // namespace osh

@@ -71,8 +71,25 @@ bool distributed(const osh_ctx* ctx) {
   return ctx->comm_mode == OSH_COMM_NCCL && ctx->size > 1 && ctx->comm != nullptr;
 }
 
+void destroy_events(std::vector<cudaEvent_t>& v) {
+  for (cudaEvent_t e : v) cudaEventDestroy(e);
+  v.clear();
+}
+
+cudaError_t make_events(std::vector<cudaEvent_t>& v, size_t n) {
+  v.assign(n, nullptr);
+  for (cudaEvent_t& e : v) {
+    const cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
 void free_layout(osh_ctx* ctx) {
   ctx->engine.reset();
+  destroy_events(ctx->rs_ev);
+  destroy_events(ctx->wave_begin);
+  destroy_events(ctx->wave_end);
   cudaFree(ctx->grad);
   cudaFree(ctx->grad_owned);
   ctx->grad_owned = nullptr;
@@ -260,6 +277,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     const ParamSpec& ps = ctx->params[p];
     osh::MuonTensorDesc t;
     t.is_matrix = ps.is_matrix() ? 1 : 0;
+    t.bucket = ctx->bucket_of[p];
     t.rows = static_cast<int>(ps.shape[0]);
     t.cols = ps.is_matrix() ? static_cast<int>(ps.shape[1]) : 1;
     t.w = ctx->w + ctx->owned_off[p];
@@ -284,7 +302,12 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     budget = std::min<size_t>(24ull << 30, free_b / 3);
   }
   ctx->engine = std::make_unique<osh::MuonEngine>();
-  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget); st != OSH_OK) return st;
+  const int min_waves = ctx->min_waves > 0 ? ctx->min_waves : (reduce_out ? 4 : 1);
+  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves); st != OSH_OK)
+    return st;
+  OSH_CUDA_TRY(make_events(ctx->rs_ev, ctx->cuts.size()));
+  OSH_CUDA_TRY(make_events(ctx->wave_begin, static_cast<size_t>(ctx->engine->num_waves())));
+  OSH_CUDA_TRY(make_events(ctx->wave_end, static_cast<size_t>(ctx->engine->num_waves())));
   // The zero-fills and table uploads above ran on the legacy stream, which the
   // ctx's non-blocking streams do not order against: finish them now.
   OSH_CUDA_TRY(cudaDeviceSynchronize());
@@ -412,46 +435,64 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
   const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
   const size_t es = grad_esize(ctx->grad_dtype);
+  const int nb = static_cast<int>(ctx->cuts.size());
+  osh::MuonEngine& eng = *ctx->engine;
+  const int nw = eng.num_waves();
+  if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
   if (dist) {
-    // RS-v: the owner of slice r of every bucket receives the sum of all
-    // ranks' slices in its grad_owned region; local gradients stay intact.
+    // RS-v, bucket by bucket: the owner of slice r of bucket b receives the
+    // sum of all ranks' slices in its grad_owned region (local grads intact).
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
-    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+    for (int b = 0; b < nb; ++b) {
       OSH_NCCL_TRY(ncclGroupStart());
       for (int r = 0; r < ctx->size; ++r) {
         const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
         if (cnt == 0) continue;
         const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) +
                              es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
-        // only the root's recvbuff is used: this rank's reduced-slice region
         uint8_t* dst = static_cast<uint8_t*>(ctx->grad_owned) +
                        es * static_cast<size_t>(ctx->owned_slice_off[b]);
         OSH_NCCL_TRY(ncclReduce(src, r == ctx->rank ? dst : nullptr, static_cast<size_t>(cnt),
                                 gtype, ncclSum, r, ctx->comm, ns));
       }
       OSH_NCCL_TRY(ncclGroupEnd());
+      OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ns));
     }
-    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], ns));
-    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[1], 0));
-  } else {
-    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));
   }
-  if (osh_status st = ctx->engine->run(*cfg, cs); st != OSH_OK) return st;
-  OSH_CUDA_TRY(cudaGetLastError());
+  auto all_gather = [&](int b) -> osh_status {
+    // AG-v of bucket b: every owner broadcasts its updated bf16 slice.
+    OSH_NCCL_TRY(ncclGroupStart());
+    for (int r = 0; r < ctx->size; ++r) {
+      const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
+      if (cnt == 0) continue;
+      __nv_bfloat16* p = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
+      OSH_NCCL_TRY(ncclBroadcast(p, p, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, ns));
+    }
+    OSH_NCCL_TRY(ncclGroupEnd());
+    return OSH_OK;
+  };
+  int ag_next = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[eng.wave_last_bucket(w)], 0));
+    OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
+    if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaGetLastError());
+    OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    if (dist) {
+      // buckets no later wave of this rank touches are final on this rank
+      const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
+      if (done >= ag_next) {
+        OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
+        for (; ag_next <= done; ++ag_next)
+          if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+      }
+    }
+  }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
   if (dist) {
-    // AG-v: every owner broadcasts its updated bf16 slice of every bucket.
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
-    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
-      OSH_NCCL_TRY(ncclGroupStart());
-      for (int r = 0; r < ctx->size; ++r) {
-        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
-        if (cnt == 0) continue;
-        __nv_bfloat16* p = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
-        OSH_NCCL_TRY(ncclBroadcast(p, p, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, ns));
-      }
-      OSH_NCCL_TRY(ncclGroupEnd());
-    }
+    for (; ag_next < nb; ++ag_next)
+      if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
     OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
   } else {
@@ -525,11 +566,18 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
     float t = 0.f;
     return cudaEventElapsedTime(&t, ctx->ev[a], ctx->ev[b]) == cudaSuccess ? t : -1.f;
   };
+  auto span = [](cudaEvent_t a, cudaEvent_t b) {
+    float t = 0.f;
+    return cudaEventElapsedTime(&t, a, b) == cudaSuccess ? t : 0.f;
+  };
   osh_step_timing t = ctx->last_timing;
   t.h2d_ms = ms(5, 0);
-  t.rs_ms = ms(0, 1);
-  t.compute_ms = ms(1, 2);
-  t.ag_ms = ms(2, 3);
+  const bool dist = distributed(ctx);
+  t.rs_ms = dist && !ctx->rs_ev.empty() ? span(ctx->ev[0], ctx->rs_ev.back()) : 0.f;
+  t.compute_ms = 0.f;  // busy time of the waves (excludes waiting for the RS)
+  for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
+    t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
+  t.ag_ms = ms(2, 3);  // all-gather tail exposed after the last wave
   t.d2h_ms = ms(3, 4);
   t.total_ms = ms(5, 4);
   *out = t;

@@ -13,9 +13,11 @@
 //   w, m    [owned, 256 B aligned per tensor]  fp32 master weight + momentum
 //   NS workspace (MuonEngine)
 // Step = RS-v (per bucket: one ncclReduce per rank slice, grouped) ->
-//        MuonEngine::run (owned tensors) -> AG-v (per bucket: one
-//        ncclBroadcast per rank slice, grouped). Collectives run on a comm
-//        stream; CUDA events time each phase on the stream it runs on.
+//        MuonEngine waves (owned tensors, bucket order) -> AG-v (per bucket:
+//        one ncclBroadcast per rank slice, grouped). Collectives run on a comm
+//        stream and overlap the compute stream: wave w waits only for the RS
+//        of its last bucket, bucket b is all-gathered as soon as the wave that
+//        completes it is done. CUDA events time each phase.
 #pragma once
 
 #include <cstdint>
@@ -59,6 +61,10 @@ struct osh_ctx {
   float* w = nullptr;
   float* m = nullptr;
   std::unique_ptr<osh::MuonEngine> engine;
+  std::vector<cudaEvent_t> rs_ev;       // per bucket: reduce-scatter landed
+  std::vector<cudaEvent_t> wave_begin;  // per engine wave
+  std::vector<cudaEvent_t> wave_end;
+  int min_waves = 0;                    // 0: auto (1 for R = 1, 4 with NCCL)
   bool layout_ready = false;
   osh_step_timing last_timing{};
 };
