@@ -175,6 +175,12 @@ typedef struct osh_gemm_problem {
 
 enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3 };
 
+/* UMMA CTA group of subsequent GEMM launches (process-wide): 2 = CTA pairs
+ * (tcgen05.mma.cta_group::2, 256x256 tiles; default), 1 = single-CTA
+ * 128x256 tiles. The environment variable OSH_GEMM_CTA_GROUP=1 sets 1. */
+osh_status osh_set_gemm_cta_group(int32_t cg);
+int32_t osh_gemm_cta_group(void);
+
 /* One grouped tcgen05 GEMM launch (the Newton-Schulz building block). */
 osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* problems, int32_t n_problems,
                        float alpha, float beta, float lr, void* stream);

@@ -153,6 +153,8 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_update_norms", c_int32, c_void_p, POINTER(c_double)),
         ("osh_read_param", c_int32, c_void_p, c_int32, c_int32, POINTER(c_float)),
         ("osh_ctx_stream", c_int32, c_void_p, POINTER(c_void_p)),
+        ("osh_set_gemm_cta_group", c_int32, c_int32),
+        ("osh_gemm_cta_group", c_int32),
         ("osh_ctx_profile_gemm", c_int32, c_void_p, c_int32),
         ("osh_gemm_profile_read", c_int32, c_void_p, POINTER(GemmProfile), c_int32),
         ("osh_gemm_profile_dump", c_int32, c_void_p, ctypes.c_char_p, c_size_t, POINTER(c_size_t)),

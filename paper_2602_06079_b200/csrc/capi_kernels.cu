@@ -47,3 +47,11 @@ extern "C" osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* prob
     return osh::fail(OSH_ERR_CUDA, std::string("osh_ns_gemm: ") + cudaGetErrorString(e));
   return OSH_OK;
 }
+
+extern "C" osh_status osh_set_gemm_cta_group(int32_t cg) {
+  if (cg != 1 && cg != 2) return osh::fail(OSH_ERR_ARG, "cta group must be 1 or 2");
+  osh::ns_gemm_set_cta_group(cg);
+  return OSH_OK;
+}
+
+extern "C" int32_t osh_gemm_cta_group(void) { return osh::ns_gemm_cta_group(); }

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 namespace osh {
@@ -18,12 +19,26 @@ namespace {
 
 using namespace osh::sm100;
 
-constexpr uint32_t kStageBytesA = kNsBM * kNsBK * 2;  // 16 KiB
-constexpr uint32_t kStageBytesB = kNsBN * kNsBK * 2;  // 32 KiB
+// CG = CTAs per UMMA (cta_group::1 or ::2). With CG = 2 a cluster of two CTAs
+// computes a 256 x 256 tile: each CTA stages its 128 rows of A and its half
+// (128 rows / columns) of B; the leader CTA issues tcgen05.mma.cta_group::2
+// and each CTA's TMEM receives its 128 accumulator rows.
+template <int CG>
+struct Cfg {
+  static constexpr uint32_t kRowsA = 128;                 // A rows per CTA
+  static constexpr uint32_t kTileM = 128 * CG;            // output rows per tile
+  static constexpr uint32_t kRowsB = kNsBN / CG;          // B rows (N) per CTA
+  static constexpr uint32_t kStageA = kRowsA * kNsBK * 2; // 16 KiB
+  static constexpr uint32_t kStageB = kRowsB * kNsBK * 2; // 32 or 16 KiB
+  static constexpr int kStages = CG == 1 ? 4 : 6;
+};
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kEpiStageFloats = 32 * 33;  // per epilogue warp: 32x32 fp32 transpose tile
-constexpr uint32_t kSmemBytes =
-    1024 + kNsStages * (kStageBytesA + kStageBytesB) + 256 + 4 * kEpiStageFloats * 4;
+template <int CG>
+constexpr uint32_t smem_bytes() {
+  return 1024 + Cfg<CG>::kStages * (Cfg<CG>::kStageA + Cfg<CG>::kStageB) + 256 +
+         4 * kEpiStageFloats * 4;
+}
 constexpr int kRasterGroup = 8;
 
 struct TileCoord {
@@ -41,10 +56,10 @@ __device__ __forceinline__ TileCoord decode_tile(const NsGemmParams& P, int t) {
   int rem = local - c.b * per_batch;
   if (pr.symmetric) {
     // column-major over the tiles that touch the upper triangle: column tn
-    // holds tiles tm = 0 .. min(tiles_m, 2*tn + 2) - 1 (BM = BN / 2)
+    // holds tiles tm = 0 .. min(tiles_m, (256*tn + 255) / tile_m + 1) - 1
     int tn = 0;
     for (;;) {
-      const int cnt = min(pr.tiles_m, 2 * tn + 2);
+      const int cnt = min(pr.tiles_m, (kNsBN * tn + kNsBN - 1) / P.tile_m + 1);
       if (rem < cnt) break;
       rem -= cnt;
       ++tn;
@@ -135,42 +150,51 @@ __device__ __forceinline__ void store_row32_sym(__nv_bfloat16* out, long long ld
   }
 }
 
-template <int MODE>
+template <int MODE, int CG>
 __global__ void __launch_bounds__(kNsThreads, 1)
     ns_gemm_kernel(const __grid_constant__ NsGemmParams P) {
+  using C = Cfg<CG>;
+  constexpr int kStages = C::kStages;
+  constexpr uint32_t kStageBytesA = C::kStageA, kStageBytesB = C::kStageB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = base;
-  uint8_t* smem_b = base + kNsStages * kStageBytesA;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + kNsStages * kStageBytesB);
-  uint64_t* empty_bar = full_bar + kNsStages;
-  uint64_t* tfull_bar = empty_bar + kNsStages;
+  uint8_t* smem_b = base + kStages * kStageBytesA;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + kStages * kStageBytesB);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   float* epi_stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = leader of the pair
+  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;  // tiles are per cluster
 
   if (warp == 0 && lane == 0) {
     for (int p = 0; p < P.num_problems; ++p) {
       tma_prefetch_desc(&P.prob[p].tmA);
       tma_prefetch_desc(&P.prob[p].tmB);
     }
-    for (int s = 0; s < kNsStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], 128 * CG);  // every epilogue thread of the pair
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_cg2(tmem_slot, kTmemCols);
+    else tmem_alloc(tmem_slot, kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -178,25 +202,30 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      const auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+        if constexpr (CG == 2) tma_load_3d_cg2(dst, map, &full_bar[stage], c0, c1, c2);
+        else tma_load_3d(dst, map, &full_bar[stage], c0, c1, c2);
+      };
+      for (int t = unit; t < P.total_tiles; t += n_units) {
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
         const int nkb = (pr.K + kNsBK - 1) / kNsBK;
+        const int a_row = c.tm * C::kTileM + rank * C::kRowsA;
+        const int b_row = c.tn * kNsBN + rank * C::kRowsB;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], kStageBytesA + kStageBytesB);
-          tma_load_3d(smem_a + stage * kStageBytesA, &pr.tmA, &full_bar[stage], kb * kNsBK,
-                      c.tm * kNsBM, c.b);
+          // the leader's full barrier counts the bytes of both CTAs of the pair
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
+          load(smem_a + stage * kStageBytesA, &pr.tmA, kb * kNsBK, a_row, c.b);
           uint8_t* sb = smem_b + stage * kStageBytesB;
           if (!pr.b_mn_major) {
-            tma_load_3d(sb, &pr.tmB, &full_bar[stage], kb * kNsBK, c.tn * kNsBN, c.b);
+            load(sb, &pr.tmB, kb * kNsBK, b_row, c.b);
           } else {
 #pragma unroll
-            for (int q = 0; q < kNsBN / 64; ++q)
-              tma_load_3d(sb + q * 8192, &pr.tmB, &full_bar[stage], c.tn * kNsBN + q * 64,
-                          kb * kNsBK, c.b);
+            for (int q = 0; q < static_cast<int>(C::kRowsB) / 64; ++q)
+              load(sb + q * 8192, &pr.tmB, b_row + q * 64, kb * kNsBK, c.b);
           }
-          if (++stage == kNsStages) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -205,11 +234,11 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------- tcgen05 issuer
-    if (lane == 0) {
-      const uint32_t idesc_k = idesc_bf16_f32(kNsBM, kNsBN, false, false);
-      const uint32_t idesc_mn = idesc_bf16_f32(kNsBM, kNsBN, false, true);
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc_k = idesc_bf16_f32(C::kTileM, kNsBN, false, false);
+      const uint32_t idesc_mn = idesc_bf16_f32(C::kTileM, kNsBN, false, true);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      for (int t = unit; t < P.total_tiles; t += n_units) {
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
         const int nkb = (pr.K + kNsBK - 1) / kNsBK;
@@ -227,15 +256,20 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             const uint64_t adesc = smem_desc_sw128(a0 + k * 32, 16, 1024);
             const uint64_t bdesc = mn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
                                       : smem_desc_sw128(b0 + k * 32, 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
+            if constexpr (CG == 2)
+              umma_bf16_cg2(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
+            else
+              umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
           }
-          umma_commit(&empty_bar[stage]);
-          if (++stage == kNsStages) {
+          if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
+          else umma_commit(&empty_bar[stage]);
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 2) umma_commit_cg2_mc(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -245,10 +279,11 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     uint32_t acc = 0, acc_phase = 0;
-    for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+    for (int t = unit; t < P.total_tiles; t += n_units) {
       const TileCoord c = decode_tile(P, t);
       const NsGemmProblem& pr = P.prob[c.p];
-      const int row = c.tm * kNsBM + row_in_tile;
+      const int row_base = c.tm * C::kTileM + rank * C::kRowsA;
+      const int row = row_base + row_in_tile;
       const bool row_ok = row < pr.M;
       const float s = pr.scale != nullptr ? __ldg(pr.scale + c.b) : 1.f;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -320,7 +355,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = upd[j];
             __syncwarp();
-            const int rbase = c.tm * kNsBM + quarter * 32;
+            const int rbase = row_base + quarter * 32;
             const int col = col0 + lane;
 #pragma unroll 4
             for (int rr = 0; rr < 32; ++rr) {
@@ -347,17 +382,20 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if constexpr (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
+      else mbar_arrive(&tempty_bar[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, kTmemCols);
+    else tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
@@ -410,29 +448,60 @@ int sm_count() {
   return n;
 }
 
-template <int MODE>
+template <int MODE, int CG>
 cudaError_t launch_mode(const NsGemmParams& P, cudaStream_t stream) {
   static bool configured = false;
+  constexpr uint32_t smem = smem_bytes<CG>();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ns_gemm_kernel<MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(ns_gemm_kernel<MODE, CG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int grid = std::min(P.total_tiles, sm_count());
-  ns_gemm_kernel<MODE><<<grid, kNsThreads, kSmemBytes, stream>>>(P);
-  return cudaGetLastError();
+  if constexpr (CG == 1) {
+    const int grid = std::min(P.total_tiles, sm_count());
+    ns_gemm_kernel<MODE, 1><<<grid, kNsThreads, smem, stream>>>(P);
+    return cudaGetLastError();
+  } else {
+    // one 2-CTA cluster per pair of SMs; tiles are strided over clusters
+    const int clusters = std::min(P.total_tiles, sm_count() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters));
+    cfg.blockDim = dim3(kNsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ns_gemm_kernel<MODE, 2>, P);
+  }
 }
 
-}  // namespace
+int g_cta_group = 0;  // 0: not yet read from OSH_GEMM_CTA_GROUP (default 2)
 
-namespace {
-int sym_tiles(int tiles_m, int tiles_n) {
+int cta_group() {
+  if (g_cta_group == 0) {
+    const char* v = std::getenv("OSH_GEMM_CTA_GROUP");
+    g_cta_group = (v != nullptr && v[0] == '1') ? 1 : 2;
+  }
+  return g_cta_group;
+}
+
+int sym_tiles(int tiles_m, int tiles_n, int tile_m) {
   int t = 0;
-  for (int tn = 0; tn < tiles_n; ++tn) t += std::min(tiles_m, 2 * tn + 2);
+  for (int tn = 0; tn < tiles_n; ++tn)
+    t += std::min(tiles_m, (kNsBN * tn + kNsBN - 1) / tile_m + 1);
   return t;
 }
+
 }  // namespace
+
+void ns_gemm_set_cta_group(int cg) { g_cta_group = (cg == 1) ? 1 : 2; }
+int ns_gemm_cta_group() { return cta_group(); }
 
 double ns_gemm_executed_flops(const NsProblemDesc* probs, int num_problems) {
   double f = 0.0;
@@ -442,9 +511,10 @@ double ns_gemm_executed_flops(const NsProblemDesc* probs, int num_problems) {
     const double N = d.b_mn_major ? d.b.cols : d.b.rows;
     double frac = 1.0;
     if (d.symmetric) {
-      const int tm = (d.a.rows + kNsBM - 1) / kNsBM;
+      const int tile_m = 128 * cta_group();
+      const int tm = (d.a.rows + tile_m - 1) / tile_m;
       const int tn = (static_cast<int>(N) + kNsBN - 1) / kNsBN;
-      frac = static_cast<double>(sym_tiles(tm, tn)) / (static_cast<double>(tm) * tn);
+      frac = static_cast<double>(sym_tiles(tm, tn, tile_m)) / (static_cast<double>(tm) * tn);
     }
     f += 2.0 * M * N * K * d.a.batch * frac;
   }
@@ -470,6 +540,8 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
   P.alpha = alpha;
   P.beta = beta;
   P.lr = lr;
+  const int cg = cta_group();
+  P.tile_m = 128 * cg;
   int tiles = 0;
   for (int i = 0; i < num_problems; ++i) {
     const NsProblemDesc& d = probs[i];
@@ -482,17 +554,18 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     if (kb != pr.K || d.b.batch != pr.batch || pr.M < 1 || pr.N < 1 || pr.K < 1 || pr.batch < 1)
       return cudaErrorInvalidValue;
     pr.b_mn_major = d.b_mn_major;
-    if (!make_map(&pr.tmA, d.a, kNsBK, kNsBM)) return cudaErrorInvalidValue;
+    if (!make_map(&pr.tmA, d.a, kNsBK, 128)) return cudaErrorInvalidValue;
     if (!d.b_mn_major) {
-      if (!make_map(&pr.tmB, d.b, kNsBK, kNsBN)) return cudaErrorInvalidValue;
+      if (!make_map(&pr.tmB, d.b, kNsBK, kNsBN / cg)) return cudaErrorInvalidValue;
     } else {
       if (!make_map(&pr.tmB, d.b, 64, kNsBK)) return cudaErrorInvalidValue;
     }
-    pr.tiles_m = (pr.M + kNsBM - 1) / kNsBM;
+    pr.tiles_m = (pr.M + P.tile_m - 1) / P.tile_m;
     pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
     pr.symmetric = d.symmetric && pr.M == pr.N && (mode == kEpiGram || mode == kEpiPoly) ? 1 : 0;
     if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
-    pr.tiles_per_batch = pr.symmetric ? sym_tiles(pr.tiles_m, pr.tiles_n) : pr.tiles_m * pr.tiles_n;
+    pr.tiles_per_batch =
+        pr.symmetric ? sym_tiles(pr.tiles_m, pr.tiles_n, P.tile_m) : pr.tiles_m * pr.tiles_n;
     pr.tile_start = tiles;
     tiles += pr.batch * pr.tiles_per_batch;
     pr.out = static_cast<__nv_bfloat16*>(const_cast<void*>(d.out.ptr));
@@ -509,11 +582,20 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     if (mode != kEpiFinal && pr.out == nullptr) return cudaErrorInvalidValue;
   }
   P.total_tiles = tiles;
+  if (cg == 2) {
+    switch (mode) {
+      case kEpiGram: return launch_mode<kEpiGram, 2>(P, stream);
+      case kEpiPoly: return launch_mode<kEpiPoly, 2>(P, stream);
+      case kEpiUpdate: return launch_mode<kEpiUpdate, 2>(P, stream);
+      case kEpiFinal: return launch_mode<kEpiFinal, 2>(P, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (mode) {
-    case kEpiGram: return launch_mode<kEpiGram>(P, stream);
-    case kEpiPoly: return launch_mode<kEpiPoly>(P, stream);
-    case kEpiUpdate: return launch_mode<kEpiUpdate>(P, stream);
-    case kEpiFinal: return launch_mode<kEpiFinal>(P, stream);
+    case kEpiGram: return launch_mode<kEpiGram, 1>(P, stream);
+    case kEpiPoly: return launch_mode<kEpiPoly, 1>(P, stream);
+    case kEpiUpdate: return launch_mode<kEpiUpdate, 1>(P, stream);
+    case kEpiFinal: return launch_mode<kEpiFinal, 1>(P, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -64,6 +64,7 @@ struct NsGemmParams {
   NsGemmProblem prob[kMaxProblems];
   int num_problems;
   int total_tiles;
+  int tile_m;  // output rows per tile: 128 (cta_group::1) or 256 (cta_group::2)
   float alpha, beta, lr;
 };
 
@@ -89,6 +90,11 @@ struct NsProblemDesc {
 // Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).
 cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
                            float beta, float lr, cudaStream_t stream);
+
+// UMMA CTA group used by subsequent launches: 2 (default; CTA pairs, 256x256
+// tiles) or 1 (single-CTA 128x256 tiles). OSH_GEMM_CTA_GROUP=1 overrides.
+void ns_gemm_set_cta_group(int cg);
+int ns_gemm_cta_group();
 
 // Algorithmic flops of a problem list (2*M*N*K per batch element).
 double ns_gemm_flops(const NsProblemDesc* probs, int num_problems);

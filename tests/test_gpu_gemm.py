@@ -17,6 +17,16 @@ pytestmark = pytest.mark.gpu
 A, B, C = 3.4445, -4.7750, 2.0315
 
 
+@pytest.fixture(autouse=True, params=[2, 1], ids=["cta_pair", "cta1"])
+def cta_group(request):
+    """Every numerics test runs on both UMMA variants (cta_group::2 and ::1)."""
+    L = _lib.lib()
+    before = L.osh_gemm_cta_group()
+    _lib.check(L.osh_set_gemm_cta_group(request.param))
+    yield request.param
+    _lib.check(L.osh_set_gemm_cta_group(before))
+
+
 def mref(t, rows=None, cols=None, batch=None):
     """MatrixRef for a [batch][rows][ld] bf16 tensor (logical rows x cols)."""
     assert t.dtype == torch.bfloat16 and t.is_cuda and t.dim() == 3
