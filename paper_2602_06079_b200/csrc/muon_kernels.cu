@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
 }
 
 __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* tasks, int n_tasks,
-                                                          float lr, int use_alt) {
+                                                          float lrate, int use_alt) {
   __shared__ float tile[kTile][kTile + 1];
   __shared__ double red[8];
   const long long t = blockIdx.x;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
       if (row < T.rows && col < T.cols) {
         const float x = T.transposed ? tile[lr][lc]
                                      : __bfloat162float(T.x[static_cast<size_t>(row) * T.ldx + col]);
-        const float upd = lr * x;
+        const float upd = lrate * x;
         const size_t idx = static_cast<size_t>(row) * T.cols + col;
         const float w = T.w[idx] - upd;
         T.w[idx] = w;
