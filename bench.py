@@ -44,6 +44,10 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--method", default="alpha-balanced",
+                    choices=["alpha-balanced", "atomic-ownership"],
+                    help="executable (atomic) partition; equal-chunk splits tensors, see "
+                         "scripts/plan_sweep.py")
     ap.add_argument("--cost", default="numel")
     ap.add_argument("--grad-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -230,7 +234,7 @@ def run_ours(a, dist: Dist):
     params = P.generate_transformer_params(cfg)
     cap = cfg.bucket_capacity
     t_plan = time.perf_counter()
-    plan = P.plan_dp(params, cap, N, "alpha-balanced", a.cost, a.alpha)
+    plan = P.plan_dp(params, cap, N, a.method, a.cost, a.alpha)
     plan_us = (time.perf_counter() - t_plan) * 1e6
     owners = P.param_owners(params, cap, plan)
     uid = dist.bcast_bytes(nccl_unique_id() if dist.rank == 0 and N > 1 else None)
@@ -349,7 +353,8 @@ def run_ours(a, dist: Dist):
         "config": {
             "workload": "qwen3-8b-like Muon step (L36 h4096 f12288 v151936: 183 tensors, "
                         f"{info['total_numel']} params, {info['n_buckets']} buckets cap {cap})",
-            "plan": f"alpha-balanced alpha={a.alpha} cost={a.cost}",
+            "plan": (f"alpha-balanced alpha={a.alpha}" if a.method == "alpha-balanced"
+                     else a.method) + f" cost={a.cost}",
             "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype,
             "parallelism": f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)",
             "l2": "inputs (weights, momentum, grads) >> 126 MB L2; no flush needed",
@@ -409,7 +414,7 @@ def run_reference(a, dist: Dist):
     cfg = P.load_config(a.config)
     params = P.generate_transformer_params(cfg)
     N = dist.world
-    plan = P.plan_dp(params, cfg.bucket_capacity, N, "alpha-balanced", a.cost, a.alpha)
+    plan = P.plan_dp(params, cfg.bucket_capacity, N, a.method, a.cost, a.alpha)
     owners = P.param_owners(params, cfg.bucket_capacity, plan)
     threads = os.cpu_count()
     for _ in range(a.warmup):

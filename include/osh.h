@@ -206,6 +206,19 @@ osh_status osh_nccl_unique_id(uint8_t out[128]);
 osh_status osh_ctx_create(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t comm_mode,
                           const uint8_t* nccl_uid /* 128 bytes; unused for OSH_COMM_NONE */,
                           osh_ctx** out);
+/* Data x tensor parallel rank (dp_rank, tp_rank) of a dp_size x tp_size grid:
+ * dp_uid identifies the DP communicator (the dp_size ranks with this
+ * tp_rank), tp_uid the TP communicator (the tp_size ranks with this dp_rank).
+ * With tp_size > 1, osh_ctx_set_layout takes the FULL parameter list and the
+ * DP plan over the TP-sharded view (apply_tp_sharding, workload.hpp:221);
+ * TP-plane tensors are hosted whole on one TP rank by the micro-group plan
+ * (tp_schedule.hpp:90-131, c_max from osh_ctx_set_tp_capacity). */
+osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t tp_rank,
+                             int32_t tp_size, int32_t comm_mode, const uint8_t* dp_uid,
+                             const uint8_t* tp_uid, osh_ctx** out);
+/* Micro-group capacity in numel cost units (default 268435456 = 512 MiB of
+ * bf16, as the reference CLI's plan-tp default). Call before set_layout. */
+osh_status osh_ctx_set_tp_capacity(osh_ctx* ctx, uint64_t c_max);
 osh_status osh_ctx_destroy(osh_ctx* ctx);
 
 /* Installs the parameter list (ids dense 0..n-1, declaration order), the
@@ -234,9 +247,12 @@ osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out);
 osh_status osh_ctx_buffers(osh_ctx* ctx, void** grad, void** replica);
 
 /* Host fp32 values of one parameter -> replica (every rank) and fp32 master
- * weight (owner only); the owner's momentum is reset to zero. */
+ * weight (owner only); the owner's momentum is reset to zero. With TP the
+ * values are the FULL tensor (each rank keeps its shard in the replica; the
+ * host keeps the whole master). */
 osh_status osh_load_param(osh_ctx* ctx, int32_t param_id, const float* values);
-/* Host fp32 gradient of one parameter -> the flat gradient buffer. */
+/* Host fp32 gradient of one parameter -> the flat gradient buffer (with TP:
+ * this rank's SHARD of the gradient). */
 osh_status osh_write_grad(osh_ctx* ctx, int32_t param_id, const float* values);
 /* Device-side synthetic fill (counter-based normal draws * scale / sqrt(rows)):
  * OSH_FILL_WEIGHTS sets replica + owned masters (+ zero momentum),

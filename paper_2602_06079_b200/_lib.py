@@ -140,6 +140,9 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_ctx_create", c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
          POINTER(c_void_p)),
         ("osh_ctx_destroy", c_int32, c_void_p),
+        ("osh_ctx_create_tp", c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
+         c_void_p, c_void_p, POINTER(c_void_p)),
+        ("osh_ctx_set_tp_capacity", c_int32, c_void_p, c_uint64),
         ("osh_ctx_set_layout", c_int32, c_void_p, POINTER(ParamDesc), c_int32, c_int64,
          POINTER(c_int64), c_int32, c_int32, c_int64),
         ("osh_ctx_get_info", c_int32, c_void_p, POINTER(CtxInfo)),

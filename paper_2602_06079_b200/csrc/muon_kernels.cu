@@ -165,6 +165,31 @@ __global__ void __launch_bounds__(256) partial_sums_kernel(const double* partial
   if (threadIdx.x == 0) out[target[i]] = s;
 }
 
+__global__ void __launch_bounds__(256) copy_blocks_kernel(const CopyTask* tasks, int n_tasks) {
+  const long long t = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const CopyTask T = tasks[lo];
+  const long long local = t - T.tile_start;
+  const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
+  const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < kTile / 8; ++i) {
+    const int row = r0 + ty + 8 * i;
+    if (row >= T.rows) continue;
+#pragma unroll
+    for (int j = 0; j < kTile / 32; ++j) {
+      const int col = c0 + tx + 32 * j;
+      if (col < T.cols) T.dst[row * T.ldd + col] = T.src[row * T.lds + col];
+    }
+  }
+}
+
 template <typename G>
 __global__ void __launch_bounds__(256) momentum_vector_kernel(const MomentumVectorTask* tasks,
                                                               float beta, float lr) {
@@ -227,6 +252,14 @@ cudaError_t launch_partial_sums(const double* partial, const long long* begin, c
                                 const int* target, double* out, int n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   partial_sums_kernel<<<n, 256, 0, s>>>(partial, begin, count, target, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_blocks(const CopyTask* d_tasks, int n_tasks, long long total_tiles,
+                               cudaStream_t s) {
+  if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
+  if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  copy_blocks_kernel<<<static_cast<unsigned>(total_tiles), 256, 0, s>>>(d_tasks, n_tasks);
   return cudaGetLastError();
 }
 

@@ -70,6 +70,20 @@ cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long
 cudaError_t launch_partial_sums(const double* partial, const long long* begin, const int* count,
                                 const int* target, double* out, int n, cudaStream_t s);
 
+// Strided 2-D copies of 16-bit blocks (TP gather / scatter staging):
+// dst[r*ldd + c] = src[r*lds + c], r < rows, c < cols, for every task.
+struct CopyTask {
+  const uint16_t* src;
+  uint16_t* dst;
+  long long lds, ldd;
+  int rows, cols;
+  long long tile_start;
+  int tiles_c;
+  int pad_;
+};
+cudaError_t launch_copy_blocks(const CopyTask* d_tasks, int n_tasks, long long total_tiles,
+                               cudaStream_t s);
+
 cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_tasks,
                                    long long total_tiles, int grad_dtype, float beta,
                                    cudaStream_t s);

@@ -85,7 +85,14 @@ cudaError_t make_events(std::vector<cudaEvent_t>& v, size_t n) {
   return cudaSuccess;
 }
 
+bool is_tp_item(const osh_ctx* ctx, size_t p) {
+  if (ctx->tp_size <= 1) return false;
+  const ParamSpec& f = ctx->params_full[p];
+  return f.tp_splittable != TpSplit::kNone && !f.vocab_space;
+}
+
 void free_layout(osh_ctx* ctx) {
+  osh::tp_free(ctx);
   ctx->engine.reset();
   destroy_events(ctx->rs_ev);
   destroy_events(ctx->wave_begin);
@@ -117,10 +124,21 @@ osh_status osh_nccl_unique_id(uint8_t out[128]) {
 
 osh_status osh_ctx_create(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t comm_mode,
                           const uint8_t* nccl_uid, osh_ctx** out) {
+  return osh_ctx_create_tp(device, dp_rank, dp_size, 0, 1, comm_mode, nccl_uid, nullptr, out);
+}
+
+osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, int32_t tp_rank,
+                             int32_t tp_size, int32_t comm_mode, const uint8_t* dp_uid,
+                             const uint8_t* tp_uid, osh_ctx** out) {
+  const uint8_t* nccl_uid = dp_uid;
   if (out == nullptr) return osh::fail(OSH_ERR_ARG, "null output");
   *out = nullptr;
   if (dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return osh::fail(OSH_ERR_PLAN, "dp_rank/dp_size out of range");
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+    return osh::fail(OSH_ERR_SHARD, "tp_rank/tp_size out of range");
+  if (tp_size > 1 && comm_mode != OSH_COMM_NCCL)
+    return osh::fail(OSH_ERR_UNSUPPORTED, "tensor parallelism needs OSH_COMM_NCCL");
   if (comm_mode != OSH_COMM_NCCL && comm_mode != OSH_COMM_NONE)
     return osh::fail(OSH_ERR_ARG, "unknown comm_mode");
   OSH_CUDA_TRY(cudaSetDevice(device));
@@ -138,7 +156,21 @@ osh_status osh_ctx_create(int32_t device, int32_t dp_rank, int32_t dp_size, int3
     std::memcpy(&id, nccl_uid, sizeof(id));
     OSH_NCCL_TRY(ncclCommInitRank(&ctx->comm, dp_size, id, dp_rank));
   }
+  ctx->tp_rank = tp_rank;
+  ctx->tp_size = tp_size;
+  if (tp_size > 1) {
+    if (tp_uid == nullptr) return osh::fail(OSH_ERR_ARG, "tp_uid required for tp_size > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, tp_uid, sizeof(id));
+    OSH_NCCL_TRY(ncclCommInitRank(&ctx->tp_comm, tp_size, id, tp_rank));
+  }
   *out = ctx.release();
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_tp_capacity(osh_ctx* ctx, uint64_t c_max) {
+  if (ctx == nullptr || c_max == 0) return osh::fail(OSH_ERR_UNSCHEDULABLE, "c_max must be positive");
+  ctx->tp_c_max = c_max;
   return OSH_OK;
 }
 
@@ -149,6 +181,7 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   cudaStreamSynchronize(ctx->comm_stream);
   free_layout(ctx);
   if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
+  if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->compute);
   cudaStreamDestroy(ctx->comm_stream);
@@ -182,6 +215,13 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
                                           : TpSplit::kNone;
       p.vocab_space = d.vocab_space != 0;
       ctx->params.push_back(p);
+    }
+    if (ctx->tp_size > 1) {
+      // params are the FULL tensors; the DP layout / plan are over the shard view
+      ctx->params_full = ctx->params;
+      ctx->params = apply_tp_sharding(ctx->params_full, ctx->tp_size);
+    } else {
+      ctx->params_full = ctx->params;
     }
     ctx->layout = build_buffer_layout(ctx->params, bucket_capacity);
     if (static_cast<int32_t>(ctx->layout.buckets.size()) != n_buckets)
@@ -234,7 +274,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     int64_t alloc = 0;
     for (size_t p = 0; p < np; ++p) {
       ctx->owner[p] = param_owner(plan, ctx->layout, static_cast<int>(p));
-      if (ctx->owner[p] == ctx->rank) {
+      if (ctx->owner[p] == ctx->rank && !is_tp_item(ctx, p)) {
         ctx->owned_off[p] = alloc;
         alloc += (ctx->params[p].numel + kOwnedAlign - 1) / kOwnedAlign * kOwnedAlign;
         ctx->owned_numel += ctx->params[p].numel;
@@ -243,6 +283,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     ctx->owned_alloc = alloc;
   } catch (const PlanError& e) {
     return osh::fail(OSH_ERR_PLAN, std::string("osh_ctx_set_layout: ") + e.what());
+  } catch (const ShardError& e) {
+    return osh::fail(OSH_ERR_SHARD, std::string("osh_ctx_set_layout: ") + e.what());
   } catch (const LayoutError& e) {
     return osh::fail(OSH_ERR_LAYOUT, std::string("osh_ctx_set_layout: ") + e.what());
   } catch (const std::exception& e) {
@@ -302,9 +344,12 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     budget = std::min<size_t>(24ull << 30, free_b / 3);
   }
   ctx->engine = std::make_unique<osh::MuonEngine>();
-  const int min_waves = ctx->min_waves > 0 ? ctx->min_waves : (reduce_out ? 4 : 1);
+  const int min_waves =
+      ctx->min_waves > 0 ? ctx->min_waves : (reduce_out && ctx->tp_size == 1 ? 4 : 1);
   if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves); st != OSH_OK)
     return st;
+  if (ctx->tp_size > 1)
+    if (osh_status st = osh::tp_setup(ctx, static_cast<int64_t>(budget)); st != OSH_OK) return st;
   OSH_CUDA_TRY(make_events(ctx->rs_ev, ctx->cuts.size()));
   OSH_CUDA_TRY(make_events(ctx->wave_begin, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->wave_end, static_cast<size_t>(ctx->engine->num_waves())));
@@ -334,6 +379,13 @@ osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out) {
     const double nn = static_cast<double>(std::max(ps.shape[0], ps.shape[1]));
     flops += 4.0 * m * m * nn + 2.0 * m * m * m;
   }
+  for (const osh_ctx::TpItem& it : ctx->tp_items) {
+    if (it.w == nullptr) continue;  // hosted by another TP rank
+    const double m = static_cast<double>(std::min(it.full_rows, it.full_cols));
+    const double nn = static_cast<double>(std::max(it.full_rows, it.full_cols));
+    flops += 4.0 * m * m * nn + 2.0 * m * m * m;
+    ++out->n_owned;
+  }
   out->ns_flops_per_iter = flops;
   out->device_bytes = static_cast<int64_t>(
       grad_esize(ctx->grad_dtype) * ctx->total_numel + 2 * ctx->total_numel +
@@ -352,6 +404,30 @@ osh_status osh_load_param(osh_ctx* ctx, int32_t pid, const float* values) {
   if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
   if (pid < 0 || pid >= static_cast<int32_t>(ctx->params.size()) || values == nullptr)
     return osh::fail(OSH_ERR_PLAN, "osh_load_param: unknown parameter");
+  std::vector<float> shard_buf;
+  if (ctx->tp_size > 1 && ctx->params_full[pid].tp_splittable != TpSplit::kNone) {
+    // values are the FULL tensor: keep it whole at a TP host, slice my shard
+    const ParamSpec& f = ctx->params_full[pid];
+    const int T = ctx->tp_size, t = ctx->tp_rank;
+    const int64_t R = f.shape[0], C = f.shape[1];
+    const int ti = ctx->tp_item_of.empty() ? -1 : ctx->tp_item_of[pid];
+    if (ti >= 0 && ctx->tp_items[ti].host == t) {
+      const size_t nf = static_cast<size_t>(R * C);
+      OSH_CUDA_TRY(cudaMemcpyAsync(ctx->tp_items[ti].w, values, 4 * nf, cudaMemcpyHostToDevice,
+                                   ctx->compute));
+      OSH_CUDA_TRY(cudaMemsetAsync(ctx->tp_items[ti].m, 0, 4 * nf, ctx->compute));
+      OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
+    }
+    shard_buf.resize(static_cast<size_t>(R * C / T));
+    if (f.tp_splittable == TpSplit::kRow) {
+      std::memcpy(shard_buf.data(), values + t * (R / T) * C, 4 * shard_buf.size());
+    } else {
+      const int64_t cs = C / T;
+      for (int64_t i = 0; i < R; ++i)
+        std::memcpy(shard_buf.data() + i * cs, values + i * C + t * cs, 4 * static_cast<size_t>(cs));
+    }
+    values = shard_buf.data();
+  }
   const int64_t n = ctx->params[pid].numel;
   float* stage = nullptr;
   OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&stage), 4 * static_cast<size_t>(n)));
@@ -406,6 +482,14 @@ osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float s
       if (ctx->owned_off[p] >= 0)
         OSH_CUDA_TRY(cudaMemsetAsync(ctx->m + ctx->owned_off[p], 0, 4 * static_cast<size_t>(n),
                                      ctx->compute));
+      const int ti = ctx->tp_item_of.empty() ? -1 : ctx->tp_item_of[p];
+      if (ti >= 0 && ctx->tp_items[ti].w != nullptr) {
+        const osh_ctx::TpItem& it = ctx->tp_items[ti];
+        const long long nf = it.full_rows * it.full_cols;
+        fill_synth_kernel<<<grid_for(nf), 256, 0, ctx->compute>>>(seed ^ 0x5bd1e995ull, base, nf, s,
+                                                                 it.w, nullptr);
+        OSH_CUDA_TRY(cudaMemsetAsync(it.m, 0, 4 * static_cast<size_t>(nf), ctx->compute));
+      }
     } else if (what == OSH_FILL_GRADS) {
       if (ctx->grad_dtype == OSH_GRAD_F32)
         fill_synth_kernel<<<grid_for(n), 256, 0, ctx->compute>>>(
@@ -478,7 +562,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaGetLastError());
     OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-    if (dist) {
+    if (dist && ctx->tp_size == 1) {
       // buckets no later wave of this rank touches are final on this rank
       const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
       if (done >= ag_next) {
@@ -487,6 +571,12 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
           if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
       }
     }
+  }
+  if (ctx->tp_size > 1) {
+    // micro groups need every reduced shard of the TP plane: wait for the
+    // whole reduce-scatter, then gather / compute / scatter group by group
+    if (dist && nb > 0) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[nb - 1], 0));
+    if (osh_status st = osh::tp_step(ctx, *cfg, cs); st != OSH_OK) return st;
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
   if (dist) {
@@ -594,6 +684,14 @@ osh_status osh_update_norms(osh_ctx* ctx, double* out) {
                             cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < ctx->params.size(); ++p)
     out[p] = ctx->engine_index[p] >= 0 ? std::sqrt(sq[ctx->engine_index[p]]) : -1.0;
+  // TP-plane tensors: the full-matrix update norm, reported by the host rank
+  for (const osh_ctx::TpItem& it : ctx->tp_items) {
+    if (it.engine_group < 0) continue;
+    double v = 0.0;
+    OSH_CUDA_TRY(cudaMemcpy(&v, ctx->tp_engines[it.engine_group]->update_sq() + it.engine_index,
+                            sizeof(double), cudaMemcpyDeviceToHost));
+    out[it.pid] = std::sqrt(v);
+  }
   return OSH_OK;
 }
 
@@ -613,9 +711,21 @@ osh_status osh_read_param(osh_ctx* ctx, int32_t pid, int32_t which, float* out) 
     }
     return OSH_OK;
   }
+  const int ti = ctx->tp_item_of.empty() ? -1 : ctx->tp_item_of[pid];
+  if (ti >= 0 && ctx->tp_items[ti].w != nullptr) {
+    // hosted TP-plane tensor: the FULL master / momentum
+    const osh_ctx::TpItem& it = ctx->tp_items[ti];
+    const float* src = which == OSH_READ_MASTER ? it.w : it.m;
+    OSH_CUDA_TRY(cudaMemcpy(out, src, 4 * static_cast<size_t>(it.full_rows * it.full_cols),
+                            cudaMemcpyDeviceToHost));
+    return OSH_OK;
+  }
   if (ctx->owned_off[pid] < 0)
     return osh::fail(OSH_ERR_PLAN, "osh_read_param: parameter " + std::to_string(pid) +
-                                       " is owned by rank " + std::to_string(ctx->owner[pid]));
+                                       " is owned by dp rank " + std::to_string(ctx->owner[pid]) +
+                                       (ti >= 0 ? " / hosted by tp rank " +
+                                                      std::to_string(ctx->tp_items[ti].host)
+                                                : std::string()));
   const float* src = (which == OSH_READ_MASTER ? ctx->w : ctx->m) + ctx->owned_off[pid];
   OSH_CUDA_TRY(cudaMemcpy(out, src, 4 * n, cudaMemcpyDeviceToHost));
   return OSH_OK;

@@ -67,4 +67,39 @@ struct osh_ctx {
   int min_waves = 0;                    // 0: auto (1 for R = 1, 4 with NCCL)
   bool layout_ready = false;
   osh_step_timing last_timing{};
+
+  // ---- tensor parallelism: micro-group gather -> host Muon -> scatter
+  // (paper Alg. 2; state keyed by (dp owner, tp host) as in
+  // the reference run_partitioned, verify.hpp:235-286)
+  int tp_rank = 0, tp_size = 1;
+  ncclComm_t tp_comm = nullptr;
+  uint64_t tp_c_max = 268435456ull;  // 512 MiB of bf16 (optishard_cli.cpp:77-82,198)
+  std::vector<optishard::ParamSpec> params_full;  // full shapes; `params` is the shard view
+  struct TpItem {
+    int pid = 0, group = 0, host = 0;
+    int split_dim = 0;               // W dimension split across the TP ranks
+    int64_t full_rows = 0, full_cols = 0;
+    float* w = nullptr;              // host rank only: full fp32 master
+    float* m = nullptr;              //                 full fp32 momentum
+    void* g_full = nullptr;          //                 assembled reduced gradient
+    __nv_bfloat16* rep_full = nullptr;  //              updated full bf16 matrix
+    uint8_t* stage = nullptr;        // column splits: per-peer shard staging (host)
+    int engine_group = -1, engine_index = -1;
+  };
+  std::vector<TpItem> tp_items;      // TP-plane tensors my DP rank owns
+  std::vector<int> tp_item_of;       // per param: index in tp_items or -1
+  int tp_groups = 0;
+  std::vector<std::unique_ptr<osh::MuonEngine>> tp_engines;  // per group (hosted items)
+  void* tp_mem = nullptr;
+  std::vector<std::vector<osh::CopyTask>> tp_unpack, tp_pack;  // per group (host side)
+  std::vector<osh::CopyTask*> d_tp_unpack, d_tp_pack;
+  std::vector<long long> tp_unpack_tiles, tp_pack_tiles;
 };
+
+namespace osh {
+// TP helpers (tp.cu)
+osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
+osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
+void tp_free(osh_ctx* ctx);
+void* grad_ptr(osh_ctx* ctx, int pid);
+}  // namespace osh

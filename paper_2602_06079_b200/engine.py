@@ -47,18 +47,27 @@ class DistributedMuon:
     def __init__(self, params: Sequence[ParamSpec], bucket_capacity: int, plan: DpPartitionPlan,
                  rank: int = 0, device: int = 0, comm: str = "nccl",
                  nccl_uid: Optional[bytes] = None, grad_dtype: str = "f32",
-                 workspace_bytes: int = 0):
+                 workspace_bytes: int = 0, tp_rank: int = 0, tp_size: int = 1,
+                 tp_uid: Optional[bytes] = None, tp_capacity: Optional[int] = None):
+        """With tp_size > 1: ``params`` are the FULL tensors, ``plan`` /
+        ``bucket_capacity`` describe the DP partition of the TP-sharded view
+        (planner.apply_tp_sharding), ``rank`` is the DP rank."""
         L = _lib.lib()
         self.params = list(params)
         self.rank, self.world = rank, plan.ranks
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         self.grad_dtype = grad_dtype
         ctx = ctypes.c_void_p()
-        uid = None
-        if nccl_uid is not None:
-            uid = ctypes.cast(ctypes.create_string_buffer(nccl_uid, 128), ctypes.c_void_p)
-        _lib.check(L.osh_ctx_create(device, rank, plan.ranks, 0 if comm == "nccl" else 1, uid,
-                                    ctypes.byref(ctx)))
+
+        def buf(b):
+            return None if b is None else ctypes.cast(ctypes.create_string_buffer(b, 128),
+                                                      ctypes.c_void_p)
+        _lib.check(L.osh_ctx_create_tp(device, rank, plan.ranks, tp_rank, tp_size,
+                                       0 if comm == "nccl" else 1, buf(nccl_uid), buf(tp_uid),
+                                       ctypes.byref(ctx)))
         self._ctx = ctx
+        if tp_capacity is not None:
+            _lib.check(L.osh_ctx_set_tp_capacity(ctx, tp_capacity))
         cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)
         _lib.check(L.osh_ctx_set_layout(ctx, _desc_array(self.params), len(self.params),
                                         bucket_capacity,
@@ -112,12 +121,18 @@ class DistributedMuon:
         _lib.check(_lib.lib().osh_fill_synthetic(self._ctx, seed, 1 if what == "weights" else 2,
                                                  scale))
 
-    def read_param(self, pid: int, which: str = "master") -> np.ndarray:
+    def read_param(self, pid: int, which: str = "master", shape=None) -> np.ndarray:
+        """``shape``: the shape to read (with TP: the shard shape for the
+        replica or a non-hosted tensor, the full shape for a hosted master)."""
         p = self.params[pid]
-        out = np.empty(p.numel, np.float32)
+        shape = tuple(shape) if shape is not None else tuple(p.shape)
+        n = 1
+        for e in shape:
+            n *= int(e)
+        out = np.empty(n, np.float32)
         _lib.check(_lib.lib().osh_read_param(self._ctx, pid, READ[which],
                                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
-        return out.reshape(p.shape)
+        return out.reshape(shape)
 
     # ------------------------------------------------------------ step
     def step(self, cfg: OptimizerConfig = OptimizerConfig(), host_grads=None,
