@@ -54,6 +54,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workspace-gb", type=float, default=0.0)
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel degree T (config C3: --gpus 8 --tp 2 = DP4 x TP2); "
+                         "TP-plane tensors go through the micro-group gather/compute/scatter path")
+    ap.add_argument("--tp-cmax", type=int, default=268435456,
+                    help="micro-group capacity in numel (default 512 MiB of bf16)")
     return ap.parse_args()
 
 
@@ -229,18 +234,31 @@ def run_ours(a, dist: Dist):
     from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, nccl_unique_id
 
     N = dist.world
+    T = a.tp
+    if N % T:
+        raise SystemExit(f"--tp {T} must divide the number of ranks {N}")
+    D = N // T
+    d, t = dist.rank // T, dist.rank % T
     torch.cuda.set_device(dist.local)
     cfg = P.load_config(a.config)
     params = P.generate_transformer_params(cfg)
-    cap = cfg.bucket_capacity
+    view = P.apply_tp_sharding(params, T)     # the DP partition is over the TP shards
+    cap = cfg.bucket_capacity // T
     t_plan = time.perf_counter()
-    plan = P.plan_dp(params, cap, N, a.method, a.cost, a.alpha)
+    plan = P.plan_dp(view, cap, D, a.method, a.cost, a.alpha)
     plan_us = (time.perf_counter() - t_plan) * 1e6
-    owners = P.param_owners(params, cap, plan)
-    uid = dist.bcast_bytes(nccl_unique_id() if dist.rank == 0 and N > 1 else None)
-    eng = DistributedMuon(params, cap, plan, rank=dist.rank, device=dist.local,
+    owners = P.param_owners(view, cap, plan)
+    if T == 1:
+        uid = dist.bcast_bytes(nccl_unique_id() if dist.rank == 0 and N > 1 else None)
+        tp_uid = None
+    else:
+        ids = dist.gather({"dp": nccl_unique_id() if d == 0 and D > 1 else None,
+                           "tp": nccl_unique_id() if t == 0 else None})
+        uid, tp_uid = ids[t]["dp"], ids[d * T]["tp"]
+    eng = DistributedMuon(params, cap, plan, rank=d, device=dist.local,
                           comm="nccl", nccl_uid=uid, grad_dtype=a.grad_dtype,
-                          workspace_bytes=int(a.workspace_gb * (1 << 30)))
+                          workspace_bytes=int(a.workspace_gb * (1 << 30)), tp_rank=t, tp_size=T,
+                          tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None)
     info = eng.info()
     eng.fill_synthetic(42, "weights")
     eng.fill_synthetic(1000 + dist.rank, "grads")
@@ -356,7 +374,9 @@ def run_ours(a, dist: Dist):
             "plan": (f"alpha-balanced alpha={a.alpha}" if a.method == "alpha-balanced"
                      else a.method) + f" cost={a.cost}",
             "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype,
-            "parallelism": f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)",
+            "parallelism": (f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)" if T == 1 else
+                            f"dp{D} x tp{T} (ZeRO-1 RS/AG over the TP shards + micro-group "
+                            f"gather/host-Muon/scatter, c_max {a.tp_cmax})"),
             "l2": "inputs (weights, momentum, grads) >> 126 MB L2; no flush needed",
         },
         "max_mean_rank_load": {

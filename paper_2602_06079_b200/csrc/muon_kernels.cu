@@ -15,6 +15,57 @@ __device__ __forceinline__ float load_grad<__nv_bfloat16>(const void* g, size_t 
   return __bfloat162float(static_cast<const __nv_bfloat16*>(g)[i]);
 }
 
+// 8 consecutive gradient values (bf16: one 16-byte load; fp32: two).
+template <typename G>
+__device__ __forceinline__ void load_grad8(const void* g, size_t i, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load_grad8<float>(const void* g, size_t i, float (&v)[8]) {
+  const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(g) + i);
+  const float4 a = __ldg(p), b = __ldg(p + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <>
+__device__ __forceinline__ void load_grad8<__nv_bfloat16>(const void* g, size_t i, float (&v)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(g) + i));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = __uint_as_float(w[q] << 16);
+    v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ void load_f8(const float* p, float (&v)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+__device__ __forceinline__ void store_f8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+__device__ __forceinline__ uint4 pack_bf16x8(const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    w[q] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void unpack_bf16x8(uint4 u, float (&v)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = __uint_as_float(w[q] << 16);
+    v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+  }
+}
+
 // Block sum in a fixed order (xor-shuffle tree, then warps in index order).
 __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
@@ -54,6 +105,62 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
   const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   float sq = 0.f;
+  if (T.vec) {
+    // 8 columns x 2 rows per thread: 128-bit loads / stores, 8 threads per
+    // 64-element row segment (fully coalesced 256 B of fp32 per row)
+    const int c8 = (threadIdx.x & 7) * 8, rr = threadIdx.x >> 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int lr = rr + 32 * h;
+      const int row = r0 + lr, col = c0 + c8;
+      float xv[8];
+      if (row < T.rows && col < T.cols) {
+        const size_t idx = static_cast<size_t>(row) * T.cols + col;
+        float g[8], mv[8];
+        load_grad8<G>(T.g, idx, g);
+        load_f8(T.m + idx, mv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          mv[q] = beta * mv[q] + g[q];
+          sq += mv[q] * mv[q];
+          xv[q] = mv[q];
+        }
+        store_f8(T.m + idx, mv);
+        if (!T.transposed)
+          *reinterpret_cast<uint4*>(T.x0 + static_cast<size_t>(row) * T.ldx + col) = pack_bf16x8(xv);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xv[q] = 0.f;
+      }
+      if (T.transposed)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tile[lr][c8 + q] = __float2bfloat16_rn(xv[q]);
+    }
+    if (T.transposed) {
+      __syncthreads();
+      // output row = original column lc, 8 consecutive original rows per store
+      const int lc = threadIdx.x >> 2, r8 = (threadIdx.x & 3) * 8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lr = r8 + 32 * h;
+        const int col = c0 + lc, row = r0 + lr;
+        if (col < T.cols && row < T.rows) {
+          if (row + 8 <= T.rows && ((T.ldx & 7) == 0)) {
+            float xv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xv[q] = __bfloat162float(tile[lr + q][lc]);
+            *reinterpret_cast<uint4*>(T.x0 + static_cast<size_t>(col) * T.ldx + row) = pack_bf16x8(xv);
+          } else {
+            for (int q = 0; q < 8 && row + q < T.rows; ++q)
+              T.x0[static_cast<size_t>(col) * T.ldx + row + q] = tile[lr + q][lc];
+          }
+        }
+      }
+    }
+    const double tile_sum = block_sum(static_cast<double>(sq), red);
+    if (threadIdx.x == 0) T.partial[local] = tile_sum;
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kTile / 8; ++i) {
     const int lr = ty + 8 * i;
@@ -110,6 +217,58 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
   const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
   const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (T.vec) {
+    if (T.transposed) {
+      // X block [cols][rows]: 8 consecutive original rows per 16-byte load
+      const int lc = threadIdx.x >> 2, r8 = (threadIdx.x & 3) * 8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lr = r8 + 32 * h;
+        const int col = c0 + lc, row = r0 + lr;
+        float xv[8];
+        if (col < T.cols && row + 8 <= T.rows && (T.ldx & 7) == 0) {
+          unpack_bf16x8(*reinterpret_cast<const uint4*>(T.x + static_cast<size_t>(col) * T.ldx + row), xv);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            xv[q] = (col < T.cols && row + q < T.rows)
+                        ? __bfloat162float(T.x[static_cast<size_t>(col) * T.ldx + row + q])
+                        : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tile[lr + q][lc] = xv[q];
+      }
+      __syncthreads();
+    }
+    float sq8 = 0.f;
+    const int c8 = (threadIdx.x & 7) * 8, rr = threadIdx.x >> 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int lr = rr + 32 * h;
+      const int row = r0 + lr, col = c0 + c8;
+      if (row >= T.rows || col >= T.cols) continue;
+      float xv[8], wv[8];
+      if (T.transposed) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xv[q] = tile[lr][c8 + q];
+      } else {
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(T.x + static_cast<size_t>(row) * T.ldx + col), xv);
+      }
+      const size_t idx = static_cast<size_t>(row) * T.cols + col;
+      load_f8(T.w + idx, wv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float upd = lrate * xv[q];
+        wv[q] -= upd;
+        sq8 += upd * upd;
+      }
+      store_f8(T.w + idx, wv);
+      if (T.replica != nullptr) *reinterpret_cast<uint4*>(T.replica + idx) = pack_bf16x8(wv);
+    }
+    const double tile_sum = block_sum(static_cast<double>(sq8), red);
+    if (threadIdx.x == 0) T.partial[local] = tile_sum;
+    return;
+  }
   if (T.transposed) {
     // X is [cols][ldx]: read the 64x64 block along X's rows (= W's columns)
 #pragma unroll

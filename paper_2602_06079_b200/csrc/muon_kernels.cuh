@@ -34,7 +34,7 @@ struct MomentumMatrixTask {
   int transposed;
   long long tile_start;  // first linear tile of this task (prefix sum)
   int tiles_c;           // column tiles
-  int pad_;
+  int vec;               // 1: 128-bit path (cols % 8 == 0, 16-byte aligned rows)
 };
 
 struct MomentumVectorTask {
@@ -61,7 +61,7 @@ struct ApplyTask {
   int transposed;
   long long tile_start;
   int tiles_c;
-  int pad_;
+  int vec;                 // 1: 128-bit path (cols % 8 == 0, 16-byte aligned rows)
 };
 
 cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long total_tiles,

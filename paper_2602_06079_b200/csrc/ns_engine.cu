@@ -246,6 +246,10 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         mt.transposed = t.rows > t.cols ? 1 : 0;
         mt.tiles_c = tiles_c;
         mt.tile_start = w.tiles;
+        const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        const bool vec = (t.cols % 8) == 0 && (c.ldn % 8) == 0 && a16(t.g) && a16(t.m) && a16(t.w) &&
+                         (t.replica == nullptr || a16(t.replica));
+        mt.vec = vec ? 1 : 0;
         // workspace / partial pointers are offsets until the buffers exist
         mt.x0 = reinterpret_cast<__nv_bfloat16*>(c.x0 + static_cast<size_t>(b) * s.xb);
         ApplyTask at{};
@@ -259,6 +263,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         at.transposed = mt.transposed;
         at.tile_start = w.tiles;
         at.tiles_c = tiles_c;
+        at.vec = mt.vec;
         mtasks.push_back(mt);
         atasks.push_back(at);
         slot_begin.push_back(w.tiles);

@@ -1,0 +1,58 @@
+"""Real multi-GPU paths (NCCL over NVLink): run the torchrun checks when the
+box has enough GPUs (skipped on single-GPU boxes; the CPU-side multi-rank
+logic is covered by tests/test_multi_rank_cpu.py).
+
+* scripts/multi_gpu_check.py     DP ZeRO-1: RS-v -> owner Muon -> AG-v vs the
+                                 fp64 oracle with R real contributors
+* scripts/multi_gpu_check_tp.py  DP x TP micro-group gather/host-Muon/scatter
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(nproc, script, *args):
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "scripts", script), *map(str, args)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert lines, out.stdout[-2000:] + out.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], json.dumps(res)[:3000]
+    return res
+
+
+def test_dp2_nccl_matches_oracle():
+    _run(2, "multi_gpu_check.py", 3)
+
+
+def test_tp2_micro_groups_match_oracle():
+    _run(2, "multi_gpu_check_tp.py", 1, 2, 3)
+
+
+def test_dp2_tp2_micro_groups_match_oracle():
+    _run(4, "multi_gpu_check_tp.py", 2, 2, 3)
+
+
+def test_dp4_nccl_matches_oracle():
+    _run(4, "multi_gpu_check.py", 3)
