@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workspace-gb", type=float, default=0.0)
+    ap.add_argument("--collectives", default="auto", choices=["auto", "nccl", "nvls"],
+                    help="DP RS/AG path: NCCL kernels or NVLS multicast fused into the update")
     ap.add_argument("--tp", type=int, default=1,
                     help="tensor-parallel degree T (config C3: --gpus 8 --tp 2 = DP4 x TP2); "
                          "TP-plane tensors go through the micro-group gather/compute/scatter path")
@@ -231,7 +233,8 @@ def run_ours(a, dist: Dist):
     import torch
 
     from paper_2602_06079_b200 import planner as P
-    from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, nccl_unique_id
+    from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,
+                                              nccl_unique_id)
 
     N = dist.world
     T = a.tp
@@ -258,8 +261,10 @@ def run_ours(a, dist: Dist):
     eng = DistributedMuon(params, cap, plan, rank=d, device=dist.local,
                           comm="nccl", nccl_uid=uid, grad_dtype=a.grad_dtype,
                           workspace_bytes=int(a.workspace_gb * (1 << 30)), tp_rank=t, tp_size=T,
-                          tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None)
+                          tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None,
+                          collectives=a.collectives)
     info = eng.info()
+    coll_path = COLLECTIVE_NAMES[info["collectives"]]
     eng.fill_synthetic(42, "weights")
     eng.fill_synthetic(1000 + dist.rank, "grads")
     ocfg = OptimizerConfig()
@@ -373,8 +378,10 @@ def run_ours(a, dist: Dist):
                         f"{info['total_numel']} params, {info['n_buckets']} buckets cap {cap})",
             "plan": (f"alpha-balanced alpha={a.alpha}" if a.method == "alpha-balanced"
                      else a.method) + f" cost={a.cost}",
-            "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype,
-            "parallelism": (f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)" if T == 1 else
+            "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype, "collectives": coll_path,
+            "parallelism": ((f"dp{N} (ZeRO-1 variable-size RS/AG fused into the update kernels: "
+                             "multimem.ld_reduce / multimem.st over NVSwitch)" if coll_path == "nvls"
+                             else f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)") if T == 1 else
                             f"dp{D} x tp{T} (ZeRO-1 RS/AG over the TP shards + micro-group "
                             f"gather/host-Muon/scatter, c_max {a.tp_cmax})"),
             "l2": "inputs (weights, momentum, grads) >> 126 MB L2; no flush needed",

@@ -221,6 +221,20 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
 osh_status osh_ctx_set_tp_capacity(osh_ctx* ctx, uint64_t c_max);
 osh_status osh_ctx_destroy(osh_ctx* ctx);
 
+/* How the dp reduce-scatter / all-gather move data (dp_size > 1, tp_size 1).
+ * Replaces nothing in the reference (its collectives are simulated); the
+ * semantics are SURVEY.md §8 row B4. Call before set_layout.
+ *   OSH_COLL_NCCL  NCCL kernels on a comm stream (grouped ncclReduce /
+ *                  ncclBroadcast per bucket), overlapped with the waves;
+ *   OSH_COLL_NVLS  grad / replica in NCCL symmetric windows; the owner's
+ *                  momentum kernels read the cross-rank sum with
+ *                  multimem.ld_reduce and its apply kernels write the bf16
+ *                  replica to every rank with multimem.st (NVSwitch
+ *                  multicast); OSH_ERR_UNSUPPORTED if the node cannot;
+ *   OSH_COLL_AUTO  NVLS when available, else NCCL (default). */
+enum { OSH_COLL_AUTO = 0, OSH_COLL_NCCL = 1, OSH_COLL_NVLS = 2 };
+osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode);
+
 /* Installs the parameter list (ids dense 0..n-1, declaration order), the
  * bucket capacity and the dp plan's cut vectors (n_buckets x (dp_size+1),
  * e.g. from osh_plan_dp). The plan must be atomic (whole tensors). Allocates
@@ -238,6 +252,9 @@ typedef struct osh_ctx_info {
   int64_t device_bytes;    /* everything the ctx allocated */
   double ns_flops_per_iter; /* algorithmic GEMM flops (4m^2n + 2m^3 per owned matrix)
                               of ONE Newton-Schulz iteration on this rank */
+  int32_t collectives;      /* 0 none (single rank / OSH_COMM_NONE), OSH_COLL_NCCL
+                               or OSH_COLL_NVLS: the path set_layout selected */
+  int32_t reserved;
 } osh_ctx_info;
 osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out);
 

@@ -66,7 +66,8 @@ class CtxInfo(ctypes.Structure):
     _fields_ = [("total_numel", c_int64), ("owned_numel", c_int64), ("n_params", c_int32),
                 ("n_owned", c_int32), ("n_buckets", c_int32), ("n_waves", c_int32),
                 ("workspace_bytes", c_int64), ("device_bytes", c_int64),
-                ("ns_flops_per_iter", c_double)]
+                ("ns_flops_per_iter", c_double), ("collectives", c_int32),
+                ("reserved_", c_int32)]
 
 
 class StepTiming(ctypes.Structure):
@@ -143,6 +144,7 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_ctx_create_tp", c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
          c_void_p, c_void_p, POINTER(c_void_p)),
         ("osh_ctx_set_tp_capacity", c_int32, c_void_p, c_uint64),
+        ("osh_ctx_set_collectives", c_int32, c_void_p, c_int32),
         ("osh_ctx_set_layout", c_int32, c_void_p, POINTER(ParamDesc), c_int32, c_int64,
          POINTER(c_int64), c_int32, c_int32, c_int64),
         ("osh_ctx_get_info", c_int32, c_void_p, POINTER(CtxInfo)),

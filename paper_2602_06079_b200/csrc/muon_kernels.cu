@@ -36,6 +36,39 @@ __device__ __forceinline__ void load_grad8<__nv_bfloat16>(const void* g, size_t 
   }
 }
 
+// NVLS: sum over every GPU of the 8 gradient values at a multicast address
+// (the NVSwitch reduces; bf16 accumulates in fp32).
+template <typename G>
+__device__ __forceinline__ void mc_load_grad8(const void* g, size_t i, float (&v)[8]);
+template <>
+__device__ __forceinline__ void mc_load_grad8<float>(const void* g, size_t i, float (&v)[8]) {
+  const float* p = static_cast<const float*>(g) + i;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "l"(p + 4) : "memory");
+}
+template <>
+__device__ __forceinline__ void mc_load_grad8<__nv_bfloat16>(const void* g, size_t i, float (&v)[8]) {
+  const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(g) + i;
+  uint32_t w[4];
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p) : "memory");
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = __uint_as_float(w[q] << 16);
+    v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+  }
+}
+
+// 16 bytes to the same offset of every GPU's buffer behind a multicast address.
+__device__ __forceinline__ void mc_store16(void* p, uint4 u) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "f"(__uint_as_float(u.x)), "f"(__uint_as_float(u.y)), "f"(__uint_as_float(u.z)),
+               "f"(__uint_as_float(u.w))
+               : "memory");
+}
+
 __device__ __forceinline__ void load_f8(const float* p, float (&v)[8]) {
   const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -117,7 +150,8 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
       if (row < T.rows && col < T.cols) {
         const size_t idx = static_cast<size_t>(row) * T.cols + col;
         float g[8], mv[8];
-        load_grad8<G>(T.g, idx, g);
+        if (T.g_mc) mc_load_grad8<G>(T.g, idx, g);
+        else load_grad8<G>(T.g, idx, g);
         load_f8(T.m + idx, mv);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -263,8 +297,12 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
         sq8 += upd * upd;
       }
       store_f8(T.w + idx, wv);
-      if (T.replica != nullptr) *reinterpret_cast<uint4*>(T.replica + idx) = pack_bf16x8(wv);
+      if (T.replica != nullptr) {
+        if (T.rep_mc) mc_store16(T.replica + idx, pack_bf16x8(wv));
+        else *reinterpret_cast<uint4*>(T.replica + idx) = pack_bf16x8(wv);
+      }
     }
+    if (T.rep_mc) __threadfence_system();
     const double tile_sum = block_sum(static_cast<double>(sq8), red);
     if (threadIdx.x == 0) T.partial[local] = tile_sum;
     return;
@@ -355,6 +393,32 @@ __global__ void __launch_bounds__(256) momentum_vector_kernel(const MomentumVect
   __shared__ double red[8];
   const MomentumVectorTask T = tasks[blockIdx.y];
   float sq = 0.f;
+  if (T.g_mc || T.rep_mc) {
+    // NVLS-fused: n % 8 == 0 and 16-byte alignment are guaranteed by the runtime
+    for (long long i = (blockIdx.x * 256ll + threadIdx.x) * 8; i < T.n; i += 256ll * gridDim.x * 8) {
+      float g[8], mv[8], wv[8];
+      if (T.g_mc) mc_load_grad8<G>(T.g, static_cast<size_t>(i), g);
+      else load_grad8<G>(T.g, static_cast<size_t>(i), g);
+      load_f8(T.m + i, mv);
+      load_f8(T.w + i, wv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        mv[q] = beta * mv[q] + g[q];
+        const float upd = lr * mv[q];
+        wv[q] -= upd;
+        sq += upd * upd;
+      }
+      store_f8(T.m + i, mv);
+      store_f8(T.w + i, wv);
+      if (T.replica != nullptr) {
+        if (T.rep_mc) mc_store16(T.replica + i, pack_bf16x8(wv));
+        else *reinterpret_cast<uint4*>(T.replica + i) = pack_bf16x8(wv);
+      }
+    }
+    if (T.rep_mc) __threadfence_system();
+    block_add_double(sq, T.sq_norm, red);
+    return;
+  }
   for (long long i = blockIdx.x * 256ll + threadIdx.x; i < T.n; i += 256ll * gridDim.x) {
     const float mv = beta * T.m[i] + load_grad<G>(T.g, static_cast<size_t>(i));
     T.m[i] = mv;

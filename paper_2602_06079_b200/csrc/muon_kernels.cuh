@@ -24,7 +24,11 @@ enum GradDtype : int { kGradF32 = 0, kGradBF16 = 1 };
 constexpr int kTile = 64;  // momentum tile edge (elements)
 
 struct MomentumMatrixTask {
-  const void* g;         // [rows][cols] reduced gradient (dtype per launch)
+  const void* g;         // [rows][cols] reduced gradient (dtype per launch); with
+                         // g_mc it is the NVLS multicast address of the local
+                         // gradients and the kernel reads the cross-GPU sum
+  int g_mc;              // 1: multimem.ld_reduce (RS-v fused into this kernel)
+  int pad0_;
   float* m;              // [rows][cols] fp32 momentum
   __nv_bfloat16* x0;     // NS iterate: [rows][ldx] or, transposed, [cols][ldx]
   double* partial;       // [tiles of this task] per-tile sum of m^2 (fixed-order
@@ -38,6 +42,7 @@ struct MomentumMatrixTask {
 };
 
 struct MomentumVectorTask {
+  int g_mc, rep_mc;            // NVLS fusion flags (see MomentumMatrixTask / ApplyTask)
   const void* g;
   float* m;
   float* w;
@@ -51,6 +56,8 @@ struct MomentumVectorTask {
 // is X^T), replica = bf16(W), per-tile sum of (lr*X)^2 for ||dW||.
 // HBM bytes per element: 2 (X) + 4 + 4 (W) + 2 (replica) = 12.
 struct ApplyTask {
+  int rep_mc;                  // 1: replica is a multicast address: multimem.st (AG-v fused)
+  int pad0_;
   const __nv_bfloat16* x;      // NS iterate [rows][ldx] or, transposed, [cols][ldx]
   const __nv_bfloat16* x_alt;  // the other ping-pong buffer (odd iteration counts)
   float* w;                // [rows][cols] fp32 master weight

@@ -203,6 +203,8 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         v.w = t.w;
         v.replica = t.replica;
         v.n = static_cast<long long>(t.rows) * t.cols;
+        v.g_mc = t.g_mc;
+        v.rep_mc = t.rep_mc;
         v.sq_norm = reinterpret_cast<double*>(static_cast<uintptr_t>(ti));  // patched below
         vtasks.push_back(v);
         continue;
@@ -250,6 +252,8 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         const bool vec = (t.cols % 8) == 0 && (c.ldn % 8) == 0 && a16(t.g) && a16(t.m) && a16(t.w) &&
                          (t.replica == nullptr || a16(t.replica));
         mt.vec = vec ? 1 : 0;
+        mt.g_mc = t.g_mc;
+        if (t.g_mc && !vec) return fail(OSH_ERR_UNSUPPORTED, "NVLS path needs the 128-bit layout");
         // workspace / partial pointers are offsets until the buffers exist
         mt.x0 = reinterpret_cast<__nv_bfloat16*>(c.x0 + static_cast<size_t>(b) * s.xb);
         ApplyTask at{};
@@ -264,6 +268,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         at.tile_start = w.tiles;
         at.tiles_c = tiles_c;
         at.vec = mt.vec;
+        at.rep_mc = t.rep_mc;
         mtasks.push_back(mt);
         atasks.push_back(at);
         slot_begin.push_back(w.tiles);

@@ -36,6 +36,8 @@ struct MuonTensorDesc {
   float* m = nullptr;       // fp32 momentum
   const void* g = nullptr;  // reduced gradient (grad dtype of the engine)
   __nv_bfloat16* replica = nullptr;  // bf16 replica slot (nullable)
+  int g_mc = 0;    // g is an NVLS multicast address (read the cross-GPU sum)
+  int rep_mc = 0;  // replica is an NVLS multicast address (store to every GPU)
 };
 
 struct NsLaunchStats {

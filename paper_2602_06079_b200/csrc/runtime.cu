@@ -97,10 +97,16 @@ void free_layout(osh_ctx* ctx) {
   destroy_events(ctx->rs_ev);
   destroy_events(ctx->wave_begin);
   destroy_events(ctx->wave_end);
-  cudaFree(ctx->grad);
+  if (ctx->nvls) {
+    osh::nvls_free(ctx);
+  } else {
+    cudaFree(ctx->grad);
+    cudaFree(ctx->replica);
+  }
   cudaFree(ctx->grad_owned);
   ctx->grad_owned = nullptr;
-  cudaFree(ctx->replica);
+  cudaFree(ctx->bar);
+  ctx->bar = nullptr;
   cudaFree(ctx->w);
   cudaFree(ctx->m);
   ctx->grad = nullptr;
@@ -171,6 +177,14 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
 osh_status osh_ctx_set_tp_capacity(osh_ctx* ctx, uint64_t c_max) {
   if (ctx == nullptr || c_max == 0) return osh::fail(OSH_ERR_UNSCHEDULABLE, "c_max must be positive");
   ctx->tp_c_max = c_max;
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (mode != OSH_COLL_AUTO && mode != OSH_COLL_NCCL && mode != OSH_COLL_NVLS)
+    return osh::fail(OSH_ERR_ARG, "unknown collectives mode");
+  ctx->coll_mode = mode;
   return OSH_OK;
 }
 
@@ -293,12 +307,33 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
 
   ctx->grad_dtype = grad_dtype;
   const size_t es = grad_esize(grad_dtype);
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->grad), es * static_cast<size_t>(ctx->total_numel)));
-  OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->replica), 2 * static_cast<size_t>(ctx->total_numel)));
+  // NVLS needs every tensor on the 16-byte vector layout (decided from the
+  // model alone, so every rank takes the same branch of the collective setup)
+  bool nvls_layout = distributed(ctx) && ctx->tp_size == 1;
+  for (size_t p = 0; p < ctx->params.size() && nvls_layout; ++p) {
+    const ParamSpec& ps = ctx->params[p];
+    const int64_t inner = ps.is_matrix() ? ps.shape[1] : ps.numel;
+    nvls_layout = ctx->flat_off[p] % 8 == 0 && inner % 8 == 0;
+  }
+  if (ctx->coll_mode == OSH_COLL_NVLS && !nvls_layout)
+    return osh::fail(OSH_ERR_UNSUPPORTED,
+                     "NVLS collectives need dp_size > 1, tp_size == 1 and 8-element aligned tensors");
+  if (nvls_layout && ctx->coll_mode != OSH_COLL_NCCL) {
+    constexpr size_t kGran = 2u << 20;
+    const size_t gb = (es * static_cast<size_t>(ctx->total_numel) + kGran - 1) / kGran * kGran;
+    const size_t rb = (2 * static_cast<size_t>(ctx->total_numel) + kGran - 1) / kGran * kGran;
+    if (osh_status st = osh::nvls_setup(ctx, gb, rb, ctx->coll_mode == OSH_COLL_NVLS); st != OSH_OK)
+      return st;
+  }
+  if (!ctx->nvls) {
+    OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->grad), es * static_cast<size_t>(ctx->total_numel)));
+    OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->replica), 2 * static_cast<size_t>(ctx->total_numel)));
+  }
   OSH_CUDA_TRY(cudaMemset(ctx->grad, 0, es * static_cast<size_t>(ctx->total_numel)));
   OSH_CUDA_TRY(cudaMemset(ctx->replica, 0, 2 * static_cast<size_t>(ctx->total_numel)));
+  if (distributed(ctx)) OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->bar), 16));
   // Reduced-gradient slices of this rank (NCCL mode): bucket after bucket.
-  const bool reduce_out = distributed(ctx);
+  const bool reduce_out = distributed(ctx) && !ctx->nvls;
   ctx->owned_slice_off.assign(ctx->cuts.size(), 0);
   int64_t slice_total = 0;
   for (size_t b = 0; b < ctx->cuts.size(); ++b) {
@@ -324,7 +359,11 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     t.cols = ps.is_matrix() ? static_cast<int>(ps.shape[1]) : 1;
     t.w = ctx->w + ctx->owned_off[p];
     t.m = ctx->m + ctx->owned_off[p];
-    if (reduce_out) {
+    if (ctx->nvls) {
+      // the cross-rank sum is read through the multicast address (RS-v fused)
+      t.g = static_cast<uint8_t*>(ctx->mc_grad) + es * static_cast<size_t>(ctx->flat_off[p]);
+      t.g_mc = 1;
+    } else if (reduce_out) {
       // position of p inside this rank's reduced slice of its bucket
       const int bucket = ctx->bucket_of[p];
       const int64_t in_slice = ctx->flat_off[p] - ctx->bucket_base[bucket] - ctx->cuts[bucket][ctx->rank];
@@ -334,6 +373,10 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
       t.g = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->flat_off[p]);
     }
     t.replica = ctx->replica + ctx->flat_off[p];
+    if (ctx->nvls) {
+      t.replica = ctx->mc_replica + ctx->flat_off[p];  // multimem.st to every rank (AG-v fused)
+      t.rep_mc = 1;
+    }
     ctx->engine_index[p] = static_cast<int>(tensors.size());
     tensors.push_back(t);
   }
@@ -346,6 +389,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   ctx->engine = std::make_unique<osh::MuonEngine>();
   const int min_waves =
       ctx->min_waves > 0 ? ctx->min_waves : (reduce_out && ctx->tp_size == 1 ? 4 : 1);
+  // (NVLS: reduce_out is false -> one wave when the workspace allows)
   if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves); st != OSH_OK)
     return st;
   if (ctx->tp_size > 1)
@@ -387,6 +431,7 @@ osh_status osh_ctx_get_info(osh_ctx* ctx, osh_ctx_info* out) {
     ++out->n_owned;
   }
   out->ns_flops_per_iter = flops;
+  out->collectives = !distributed(ctx) ? 0 : ctx->nvls ? OSH_COLL_NVLS : OSH_COLL_NCCL;
   out->device_bytes = static_cast<int64_t>(
       grad_esize(ctx->grad_dtype) * ctx->total_numel + 2 * ctx->total_numel +
       8 * std::max<int64_t>(ctx->owned_alloc, 1) + ctx->engine->workspace_bytes());
@@ -523,6 +568,35 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   osh::MuonEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
   if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
+  if (ctx->nvls) {
+    // barrier -> waves (reduce / broadcast inside the kernels) -> barrier
+    auto barrier = [&]() -> osh_status {
+      OSH_NCCL_TRY(ncclAllReduce(ctx->bar, ctx->bar, 1, ncclFloat32, ncclSum, ctx->comm, cs));
+      return OSH_OK;
+    };
+    if (osh_status st = barrier(); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
+    for (int w = 0; w < nw; ++w) {
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
+      if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaGetLastError());
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    }
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
+    if (osh_status st = barrier(); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
+    if (host_replica_out != nullptr)
+      OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
+                                   2 * static_cast<size_t>(ctx->total_numel),
+                                   cudaMemcpyDeviceToHost, cs));
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
+    const osh::NsLaunchStats& s = eng.stats();
+    ctx->last_timing.gemm_launches = s.launches_gemm;
+    ctx->last_timing.elementwise_launches = s.launches_elementwise;
+    ctx->last_timing.gemm_flops = s.gemm_flops;
+    if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+    return OSH_OK;
+  }
   if (dist) {
     // RS-v, bucket by bucket: the owner of slice r of bucket b receives the
     // sum of all ranks' slices in its grad_owned region (local grads intact).

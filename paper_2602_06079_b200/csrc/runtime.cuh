@@ -64,7 +64,16 @@ struct osh_ctx {
   std::vector<cudaEvent_t> rs_ev;       // per bucket: reduce-scatter landed
   std::vector<cudaEvent_t> wave_begin;  // per engine wave
   std::vector<cudaEvent_t> wave_end;
-  int min_waves = 0;                    // 0: auto (1 for R = 1, 4 with NCCL)
+  int min_waves = 0;                    // 0: auto (1 for R = 1 or NVLS, 4 with NCCL)
+  // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
+  // the update kernels reduce / broadcast through their multicast addresses
+  int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
+  bool nvls = false;
+  void* nvls_state = nullptr;
+  void* mc_grad = nullptr;              // multicast address of grad
+  __nv_bfloat16* mc_replica = nullptr;  // multicast address of replica
+  std::string nvls_why;                 // why NVLS is off (diagnostics)
+  float* bar = nullptr;                 // 1-element buffer of the step barriers
   bool layout_ready = false;
   osh_step_timing last_timing{};
 
@@ -102,4 +111,7 @@ osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
 osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);
+// NVLS helpers (nvls.cu)
+osh_status nvls_setup(osh_ctx* ctx, size_t grad_bytes, size_t replica_bytes, bool required);
+void nvls_free(osh_ctx* ctx);
 }  // namespace osh

@@ -39,6 +39,10 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+COLLECTIVES = {"auto": 0, "nccl": 1, "nvls": 2}
+COLLECTIVE_NAMES = {0: "none", 1: "nccl", 2: "nvls"}
+
+
 class DistributedMuon:
     """One data-parallel rank. ``comm='nccl'`` runs the real collectives
     (dp_size > 1 needs ``nccl_uid``); ``comm='none'`` skips them: the caller
@@ -48,10 +52,16 @@ class DistributedMuon:
                  rank: int = 0, device: int = 0, comm: str = "nccl",
                  nccl_uid: Optional[bytes] = None, grad_dtype: str = "f32",
                  workspace_bytes: int = 0, tp_rank: int = 0, tp_size: int = 1,
-                 tp_uid: Optional[bytes] = None, tp_capacity: Optional[int] = None):
+                 tp_uid: Optional[bytes] = None, tp_capacity: Optional[int] = None,
+                 collectives: str = "auto"):
         """With tp_size > 1: ``params`` are the FULL tensors, ``plan`` /
         ``bucket_capacity`` describe the DP partition of the TP-sharded view
-        (planner.apply_tp_sharding), ``rank`` is the DP rank."""
+        (planner.apply_tp_sharding), ``rank`` is the DP rank.
+
+        ``collectives`` (dp_size > 1): "nccl" = NCCL reduce-scatter /
+        all-gather kernels overlapped with the update, "nvls" = reduction and
+        broadcast fused into the update kernels through NVSwitch multicast
+        (OshError when the node cannot), "auto" = nvls when available."""
         L = _lib.lib()
         self.params = list(params)
         self.rank, self.world = rank, plan.ranks
@@ -68,6 +78,7 @@ class DistributedMuon:
         self._ctx = ctx
         if tp_capacity is not None:
             _lib.check(L.osh_ctx_set_tp_capacity(ctx, tp_capacity))
+        _lib.check(L.osh_ctx_set_collectives(ctx, COLLECTIVES[collectives]))
         cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)
         _lib.check(L.osh_ctx_set_layout(ctx, _desc_array(self.params), len(self.params),
                                         bucket_capacity,

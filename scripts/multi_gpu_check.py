@@ -1,6 +1,9 @@
 """N-GPU correctness of the real NCCL path (RS-v -> owner Muon -> AG-v).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps] [auto|nccl|nvls]
+
+The optional second argument selects the DP collective path (engine.py
+``collectives``); the JSON line reports the path the runtime actually took.
 
 Every rank writes ITS OWN contributor gradient (synth_gradient(..., rank=r),
 verify.hpp:102-107) into its local buckets; the NCCL reduce-scatter must
@@ -23,13 +26,15 @@ sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
 from paper_2602_06079_b200 import planner as P  # noqa: E402
-from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, nccl_unique_id  # noqa: E402
+from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,  # noqa: E402
+                                          nccl_unique_id)
 
 SEED = 42
 
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    coll = sys.argv[2] if len(sys.argv) > 2 else "auto"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     td.init_process_group("gloo")
@@ -43,7 +48,8 @@ def main():
     uid = [nccl_unique_id() if rank == 0 else None]
     td.broadcast_object_list(uid, src=0)
     eng = DistributedMuon(params, cap, plan, rank=rank, device=local, comm="nccl", nccl_uid=uid[0],
-                          grad_dtype="f32")
+                          grad_dtype="f32", collectives=coll)
+    path = COLLECTIVE_NAMES[eng.info()["collectives"]]
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
     norms = []
@@ -89,7 +95,7 @@ def main():
         ok &= good
         report[p.name] = {"owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
-    print(json.dumps({"world": world, "steps": steps, "ok": ok, "params": report}))
+    print(json.dumps({"world": world, "steps": steps, "collectives": path, "ok": ok, "params": report}))
     return 0 if ok else 1
 
 

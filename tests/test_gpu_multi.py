@@ -43,7 +43,13 @@ def _run(nproc, script, *args):
 
 
 def test_dp2_nccl_matches_oracle():
-    _run(2, "multi_gpu_check.py", 3)
+    res = _run(2, "multi_gpu_check.py", 3, "nccl")
+    assert res["collectives"] == "nccl"
+
+
+def test_dp2_auto_matches_oracle():
+    # NVLS-fused reduce / broadcast when the box has NVSwitch multicast
+    _run(2, "multi_gpu_check.py", 3, "auto")
 
 
 def test_tp2_micro_groups_match_oracle():
@@ -55,4 +61,8 @@ def test_dp2_tp2_micro_groups_match_oracle():
 
 
 def test_dp4_nccl_matches_oracle():
-    _run(4, "multi_gpu_check.py", 3)
+    _run(4, "multi_gpu_check.py", 3, "nccl")
+
+
+def test_dp4_auto_matches_oracle():
+    _run(4, "multi_gpu_check.py", 3, "auto")
