@@ -301,9 +301,12 @@ def run_ours(a, dist: Dist):
         d["flops"] += fl
         d["exec_flops"] += ex
         d["launches"] += 1
-    for d in by_mode.values():
-        d["tflops_alg"] = round(d["flops"] / (d["ms"] * 1e-3) / 1e12, 1) if d["ms"] else 0.0
-        d["tflops_exec"] = round(d["exec_flops"] / (d["ms"] * 1e-3) / 1e12, 1) if d["ms"] else 0.0
+    for mode, d in by_mode.items():
+        if mode in GEMM_MODES:
+            d["tflops_alg"] = round(d["flops"] / (d["ms"] * 1e-3) / 1e12, 1) if d["ms"] else 0.0
+            d["tflops_exec"] = round(d["exec_flops"] / (d["ms"] * 1e-3) / 1e12, 1) if d["ms"] else 0.0
+        elif d["flops"] > 0:  # elementwise: algorithmic bytes in the flops column
+            d["gbps_alg"] = round(d["flops"] / (d["ms"] * 1e-3) / 1e9, 1) if d["ms"] else 0.0
         d["ms_per_step"] = round(d["ms"] / a.steps, 2)
         for k in ("ms", "flops", "exec_flops"):
             d.pop(k)
@@ -463,6 +466,9 @@ def run_reference(a, dist: Dist):
         "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+
+
+GEMM_MODES = ("gram", "poly", "update", "final")
 
 
 def main():

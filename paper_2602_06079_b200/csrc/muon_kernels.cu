@@ -44,16 +44,16 @@ template <>
 __device__ __forceinline__ void mc_load_grad8<float>(const void* g, size_t i, float (&v)[8]) {
   const float* p = static_cast<const float*>(g) + i;
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p) : "memory");
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p));
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "l"(p + 4) : "memory");
+               : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "l"(p + 4));
 }
 template <>
 __device__ __forceinline__ void mc_load_grad8<__nv_bfloat16>(const void* g, size_t i, float (&v)[8]) {
   const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(g) + i;
   uint32_t w[4];
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p) : "memory");
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     v[2 * q] = __uint_as_float(w[q] << 16);
@@ -142,24 +142,37 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
     // 8 columns x 2 rows per thread: 128-bit loads / stores, 8 threads per
     // 64-element row segment (fully coalesced 256 B of fp32 per row)
     const int c8 = (threadIdx.x & 7) * 8, rr = threadIdx.x >> 3;
+    // both rows' loads are issued before either is consumed: two 16-byte
+    // requests in flight per thread (NVLS: each is a switch round trip)
+    float g[2][8], mv[2][8];
+    bool ok[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = r0 + rr + 32 * h, col = c0 + c8;
+      ok[h] = row < T.rows && col < T.cols;
+      if (ok[h]) {
+        const size_t idx = static_cast<size_t>(row) * T.cols + col;
+        if (T.g_mc) mc_load_grad8<G>(T.g, idx, g[h]);
+        else load_grad8<G>(T.g, idx, g[h]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (ok[h]) load_f8(T.m + static_cast<size_t>(r0 + rr + 32 * h) * T.cols + c0 + c8, mv[h]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int lr = rr + 32 * h;
       const int row = r0 + lr, col = c0 + c8;
       float xv[8];
-      if (row < T.rows && col < T.cols) {
+      if (ok[h]) {
         const size_t idx = static_cast<size_t>(row) * T.cols + col;
-        float g[8], mv[8];
-        if (T.g_mc) mc_load_grad8<G>(T.g, idx, g);
-        else load_grad8<G>(T.g, idx, g);
-        load_f8(T.m + idx, mv);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          mv[q] = beta * mv[q] + g[q];
-          sq += mv[q] * mv[q];
-          xv[q] = mv[q];
+          mv[h][q] = beta * mv[h][q] + g[h][q];
+          sq += mv[h][q] * mv[h][q];
+          xv[q] = mv[h][q];
         }
-        store_f8(T.m + idx, mv);
+        store_f8(T.m + idx, mv[h]);
         if (!T.transposed)
           *reinterpret_cast<uint4*>(T.x0 + static_cast<size_t>(row) * T.ldx + col) = pack_bf16x8(xv);
       } else {
@@ -236,7 +249,10 @@ __global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatr
 
 __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* tasks, int n_tasks,
                                                           float lrate, int use_alt) {
-  __shared__ float tile[kTile][kTile + 1];
+  // X values are bf16, so a bf16 staging tile is exact and keeps the CTA at
+  // 8.5 KB of shared memory: small enough to co-reside with a persistent
+  // Newton-Schulz GEMM CTA when the update of one wave overlaps the next
+  __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
   __shared__ double red[8];
   const long long t = blockIdx.x;
   int lo = 0, hi = n_tasks - 1;
@@ -270,7 +286,7 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
                         : 0.f;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) tile[lr + q][lc] = xv[q];
+        for (int q = 0; q < 8; ++q) tile[lr + q][lc] = __float2bfloat16_rn(xv[q]);
       }
       __syncthreads();
     }
@@ -284,7 +300,7 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
       float xv[8], wv[8];
       if (T.transposed) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) xv[q] = tile[lr][c8 + q];
+        for (int q = 0; q < 8; ++q) xv[q] = __bfloat162float(tile[lr][c8 + q]);
       } else {
         unpack_bf16x8(*reinterpret_cast<const uint4*>(T.x + static_cast<size_t>(row) * T.ldx + col), xv);
       }
@@ -302,9 +318,13 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
         else *reinterpret_cast<uint4*>(T.replica + idx) = pack_bf16x8(wv);
       }
     }
-    if (T.rep_mc) __threadfence_system();
     const double tile_sum = block_sum(static_cast<double>(sq8), red);
-    if (threadIdx.x == 0) T.partial[local] = tile_sum;
+    if (threadIdx.x == 0) {
+      T.partial[local] = tile_sum;
+      // the CTA's multicast stores (ordered before this by the barrier in
+      // block_sum) are performed system-wide before the kernel can complete
+      if (T.rep_mc) __threadfence_system();
+    }
     return;
   }
   if (T.transposed) {
@@ -317,9 +337,8 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
       for (int j = 0; j < kTile / 32; ++j) {
         const int lr = tx + 32 * j;
         const int row = r0 + lr;
-        tile[lr][lc] = (row < T.rows && col < T.cols)
-                           ? __bfloat162float(T.x[static_cast<size_t>(col) * T.ldx + row])
-                           : 0.f;
+        tile[lr][lc] = (row < T.rows && col < T.cols) ? T.x[static_cast<size_t>(col) * T.ldx + row]
+                                                      : __float2bfloat16_rn(0.f);
       }
     }
     __syncthreads();
@@ -334,8 +353,8 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
       const int lc = tx + 32 * j;
       const int col = c0 + lc;
       if (row < T.rows && col < T.cols) {
-        const float x = T.transposed ? tile[lr][lc]
-                                     : __bfloat162float(T.x[static_cast<size_t>(row) * T.ldx + col]);
+        const float x = __bfloat162float(T.transposed ? tile[lr][lc]
+                                                      : T.x[static_cast<size_t>(row) * T.ldx + col]);
         const float upd = lrate * x;
         const size_t idx = static_cast<size_t>(row) * T.cols + col;
         const float w = T.w[idx] - upd;
@@ -415,8 +434,8 @@ __global__ void __launch_bounds__(256) momentum_vector_kernel(const MomentumVect
         else *reinterpret_cast<uint4*>(T.replica + i) = pack_bf16x8(wv);
       }
     }
-    if (T.rep_mc) __threadfence_system();
     block_add_double(sq, T.sq_norm, red);
+    if (T.rep_mc && threadIdx.x == 0) __threadfence_system();
     return;
   }
   for (long long i = blockIdx.x * 256ll + threadIdx.x; i < T.n; i += 256ll * gridDim.x) {

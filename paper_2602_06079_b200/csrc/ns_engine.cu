@@ -77,6 +77,7 @@ void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, 
   *flops = *exec_flops = *ms = 0.0;
   for (const Timed& t : timed_) {
     float dt = 0.f;
+    if (t.mode >= kModeElementwise) continue;
     cudaEventSynchronize(t.b);
     if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
     ++*launches;
@@ -94,14 +95,16 @@ void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, 
 }
 
 std::string MuonEngine::profile_text() const {
-  static const char* kNames[] = {"gram", "poly", "update", "final"};
+  static const char* kNames[] = {"gram", "poly", "update", "final", "?", "?", "?", "?",
+                                 "momentum_vector", "momentum_matrix", "ns_scales",
+                                 "apply_update", "partial_sums"};
   std::string out;
   char line[512];
   for (const Timed& t : timed_) {
     float dt = 0.f;
     cudaEventSynchronize(t.b);
     if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
-    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode & 3], dt, t.flops,
+    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode < 13 ? t.mode : 4], dt, t.flops,
                   t.exec_flops, t.what.c_str());
     out += line;
   }
@@ -129,7 +132,7 @@ void MuonEngine::release() {
 }
 
 osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int grad_dtype,
-                             size_t budget, int min_waves) {
+                             size_t budget, int min_waves, bool double_buffer) {
   release();
   n_tensors_ = static_cast<int>(tensors.size());
   grad_dtype_ = grad_dtype;
@@ -142,15 +145,18 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       total_ws += 2 * s.xb + 2 * s.ab;
       largest = std::max(largest, 2 * s.xb + 2 * s.ab);
     }
-  size_t cap = budget;
-  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total_ws + min_waves - 1) / min_waves));
   if (largest > budget)
     return fail(OSH_ERR_OOM, "MuonEngine: one matrix needs " + std::to_string(largest) +
                                  " workspace bytes, budget is " + std::to_string(budget));
+  // double buffering: odd waves use a second workspace half, so wave w+1's
+  // momentum can run while wave w's GEMMs still read theirs
+  double_buffer_ = double_buffer && largest <= budget / 2;
+  size_t cap = double_buffer_ ? budget / 2 : budget;
+  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total_ws + min_waves - 1) / min_waves));
 
   std::vector<std::vector<int>> wave_members(1);
   std::vector<std::vector<std::pair<int, int>>> wave_classes(1);
-  size_t used = 0;
+  size_t used = 0, half = 0;
   for (int i = 0; i < n_tensors_; ++i) {
     const MuonTensorDesc& t = tensors[i];
     if (t.is_matrix) {
@@ -164,6 +170,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
                          (new_class && classes.size() == static_cast<size_t>(kMaxProblems)))) {
         wave_members.emplace_back();
         wave_classes.emplace_back();
+        half = std::max(half, used);
         used = 0;
       }
       auto& cl = wave_classes.back();
@@ -173,6 +180,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     wave_members.back().push_back(i);
   }
   if (wave_members.back().empty()) wave_members.pop_back();
+  half = (std::max(half, used) + 1023) / 1024 * 1024;
 
   // ---- chunks (one per class per wave), slots, tables
   std::vector<MomentumMatrixTask> mtasks;
@@ -203,6 +211,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         v.w = t.w;
         v.replica = t.replica;
         v.n = static_cast<long long>(t.rows) * t.cols;
+        w.elems_vector += static_cast<double>(v.n);
         v.g_mc = t.g_mc;
         v.rep_mc = t.rep_mc;
         v.sq_norm = reinterpret_cast<double*>(static_cast<uintptr_t>(ti));  // patched below
@@ -214,7 +223,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       if (!by_class.count(cls)) order.push_back(cls);
       by_class[cls].push_back(ti);
     }
-    size_t off = 0;
+    size_t off = double_buffer_ && (wi & 1) ? half : 0;
     for (const auto& cls : order) {
       const std::vector<int>& members = by_class[cls];
       const MuonTensorDesc& t0 = tensors[members.front()];
@@ -275,6 +284,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         slot_count.push_back(static_cast<int>(ntiles));
         slot_tensor.push_back(ti);
         w.tiles += ntiles;
+        w.elems_matrix += static_cast<double>(t.rows) * t.cols;
         ++slot;
       }
       w.chunks.push_back(static_cast<int>(chunks_.size()));
@@ -328,19 +338,65 @@ osh_status MuonEngine::begin_step(cudaStream_t s) {
 }
 
 osh_status MuonEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
+  if (osh_status st = run_pre(wi, cfg, s); st != OSH_OK) return st;
+  if (osh_status st = run_ns(wi, cfg, s); st != OSH_OK) return st;
+  return run_post(wi, cfg, s);
+}
+
+// profile mode: CUDA events around each elementwise launch; `bytes` is the
+// algorithmic HBM (or, NVLS, NVLink) traffic of the launch
+template <typename F>
+cudaError_t MuonEngine::timed_elementwise(int mode, double bytes, double elems, cudaStream_t s,
+                                          F&& launch) {
+  const bool rec = profile_ && timed_.size() < 100000;
+  Timed t{};
+  if (rec) {
+    t.a = take_event();
+    t.b = take_event();
+    t.flops = bytes;
+    t.exec_flops = 0.0;
+    t.mode = mode;
+    t.what = std::to_string(static_cast<long long>(elems));
+    cudaEventRecord(t.a, s);
+  }
+  const cudaError_t err = launch();
+  if (rec) {
+    cudaEventRecord(t.b, s);
+    timed_.push_back(std::move(t));
+  }
+  ++stats_.launches_elementwise;
+  return err;
+}
+
+osh_status MuonEngine::run_pre(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
   const Wave& w = waves_[wi];
   if (cfg.ns_steps < 1 && w.n_slots > 0)
     return fail(OSH_ERR_UNSUPPORTED, "MuonEngine: ns_steps must be >= 1 on the GPU path");
   const float beta = static_cast<float>(cfg.beta), lr = static_cast<float>(cfg.lr);
-  if (w.n_vec > 0) {
-    OSH_CUDA_TRY(launch_momentum_vector(d_vtasks_ + w.vec0, w.n_vec, grad_dtype_, beta, lr, s));
-    ++stats_.launches_elementwise;
-  }
+  const double ges = grad_dtype_ == kGradBF16 ? 2.0 : 4.0;
+  const double elems = w.elems_matrix + w.elems_vector;
+  const auto timed = [&](int mode, double bytes, auto&& launch) {
+    return timed_elementwise(mode, bytes, elems, s, launch);
+  };
+  if (w.n_vec > 0)
+    OSH_CUDA_TRY(timed(kModeElementwise + 0, w.elems_vector * (ges + 18.0), [&] {
+      return launch_momentum_vector(d_vtasks_ + w.vec0, w.n_vec, grad_dtype_, beta, lr, s);
+    }));
   if (w.n_tasks == 0) return OSH_OK;
-  OSH_CUDA_TRY(launch_momentum_matrix(d_mtasks_ + w.task0, w.n_tasks, w.tiles, grad_dtype_, beta, s));
-  OSH_CUDA_TRY(launch_ns_scales(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
-                                d_scale_update_ + w.slot0, d_scale_gram_ + w.slot0, w.n_slots, s));
-  stats_.launches_elementwise += 2;
+  // g read, m read + write, bf16 X0 write
+  OSH_CUDA_TRY(timed(kModeElementwise + 1, w.elems_matrix * (ges + 10.0), [&] {
+    return launch_momentum_matrix(d_mtasks_ + w.task0, w.n_tasks, w.tiles, grad_dtype_, beta, s);
+  }));
+  OSH_CUDA_TRY(timed(kModeElementwise + 2, 0.0, [&] {
+    return launch_ns_scales(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
+                            d_scale_update_ + w.slot0, d_scale_gram_ + w.slot0, w.n_slots, s);
+  }));
+  return OSH_OK;
+}
+
+osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
+  const Wave& w = waves_[wi];
+  if (w.n_tasks == 0) return OSH_OK;
   const int np = static_cast<int>(w.chunks.size());
   for (int it = 0; it < cfg.ns_steps; ++it) {
     const bool first = it == 0;
@@ -395,12 +451,26 @@ osh_status MuonEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
       return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") + cudaGetErrorString(e));
     stats_.launches_gemm += 3;
   }
-  // after k iterations the iterate sits in X0 (k even) or X1 (k odd)
-  OSH_CUDA_TRY(launch_apply_update(d_atasks_ + w.task0, w.n_tasks, w.tiles, lr,
-                                   cfg.ns_steps & 1, s));
-  OSH_CUDA_TRY(launch_partial_sums(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
-                                   d_slot_tensor_ + w.slot0, d_update_sq_, w.n_slots, s));
-  stats_.launches_elementwise += 2;
+  return OSH_OK;
+}
+
+osh_status MuonEngine::run_post(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
+  const Wave& w = waves_[wi];
+  if (w.n_tasks == 0) return OSH_OK;
+  const float lr = static_cast<float>(cfg.lr);
+  const double elems = w.elems_matrix + w.elems_vector;
+  const auto timed = [&](int mode, double bytes, auto&& launch) {
+    return timed_elementwise(mode, bytes, elems, s, launch);
+  };
+  // after k iterations the iterate sits in X0 (k even) or X1 (k odd);
+  // X read, w read + write, bf16 replica write
+  OSH_CUDA_TRY(timed(kModeElementwise + 3, w.elems_matrix * 12.0, [&] {
+    return launch_apply_update(d_atasks_ + w.task0, w.n_tasks, w.tiles, lr, cfg.ns_steps & 1, s);
+  }));
+  OSH_CUDA_TRY(timed(kModeElementwise + 4, 0.0, [&] {
+    return launch_partial_sums(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
+                               d_slot_tensor_ + w.slot0, d_update_sq_, w.n_slots, s);
+  }));
   return OSH_OK;
 }
 

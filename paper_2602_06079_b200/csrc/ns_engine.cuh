@@ -40,6 +40,10 @@ struct MuonTensorDesc {
   int rep_mc = 0;  // replica is an NVLS multicast address (store to every GPU)
 };
 
+// profile modes >= kModeElementwise: momentum_vector, momentum_matrix,
+// ns_scales, apply_update, partial_sums (GEMM modes are the OSH_EPI_* codes)
+constexpr int kModeElementwise = 8;
+
 struct NsLaunchStats {
   int launches_gemm = 0;
   int launches_elementwise = 0;
@@ -55,10 +59,21 @@ class MuonEngine {
 
   // tensors must be in declaration order. min_waves > 1 cuts the work into at
   // least that many waves (finer RS/AG overlap) when tensors allow.
+  // double_buffer: alternate waves between two workspace halves so run_pre of
+  // wave w+1 may overlap run_ns of wave w on another stream.
   osh_status build(const std::vector<MuonTensorDesc>& tensors, int grad_dtype,
-                   size_t workspace_budget_bytes, int min_waves);
+                   size_t workspace_budget_bytes, int min_waves, bool double_buffer = false);
   osh_status begin_step(cudaStream_t stream);  // clears the update norms / stats
-  osh_status run_wave(int w, const osh_muon_cfg& cfg, cudaStream_t stream);
+  osh_status run_wave(int w, const osh_muon_cfg& cfg, cudaStream_t stream);  // pre+ns+post
+  // The three phases of a wave. Ordering contract for overlapped schedules:
+  // run_pre(w) -> run_ns(w) -> run_post(w); run_pre / run_post of all waves on
+  // ONE stream in the order pre(0) pre(1) post(0) pre(2) post(1) ... (they
+  // share the tile-partial buffer); run_ns(w+1) may overlap run_post(w) and,
+  // with double buffering, run_pre(w+2) may not start before run_post(w).
+  osh_status run_pre(int w, const osh_muon_cfg& cfg, cudaStream_t stream);   // momentum + scales
+  osh_status run_ns(int w, const osh_muon_cfg& cfg, cudaStream_t stream);    // k x GRAM/POLY/UPDATE
+  osh_status run_post(int w, const osh_muon_cfg& cfg, cudaStream_t stream);  // apply + norms
+  bool double_buffered() const { return double_buffer_; }
 
   int num_waves() const { return static_cast<int>(waves_.size()); }
   int wave_first_bucket(int w) const { return waves_[w].first_bucket; }
@@ -70,7 +85,9 @@ class MuonEngine {
   const NsLaunchStats& stats() const { return stats_; }  // since begin_step()
   int num_tensors() const { return n_tensors_; }
 
-  // Per-launch CUDA-event timing of the GEMMs (roofline reporting).
+  // Per-launch CUDA-event timing of every launch (roofline reporting); the
+  // read_profile totals cover the GEMMs only, profile_text lists all launches
+  // (elementwise kernels report algorithmic bytes in the flops column).
   void set_profile(bool on) { profile_ = on; }
   void read_profile(int* launches, double* flops, double* exec_flops, double* ms, bool reset);
   // One line per recorded launch: "mode ms flops exec_flops shapes".
@@ -91,6 +108,7 @@ class MuonEngine {
     long long tiles = 0;
     int slot0 = 0, n_slots = 0;
     int vec0 = 0, n_vec = 0;
+    double elems_matrix = 0.0, elems_vector = 0.0;  // owned elements (profile bytes)
   };
   struct Timed {
     cudaEvent_t a, b;
@@ -101,6 +119,8 @@ class MuonEngine {
   };
   void release();
   cudaEvent_t take_event();
+  template <typename F>
+  cudaError_t timed_elementwise(int mode, double bytes, double elems, cudaStream_t s, F&& launch);
 
   int n_tensors_ = 0;
   int grad_dtype_ = kGradF32;
@@ -122,6 +142,7 @@ class MuonEngine {
   NsLaunchStats stats_;
   bool profile_ = false;
   bool symmetric_ = true;
+  bool double_buffer_ = false;
   std::vector<Timed> timed_;
   std::vector<cudaEvent_t> event_pool_;
 };

@@ -30,7 +30,10 @@ struct Cfg {
   static constexpr uint32_t kRowsB = kNsBN / CG;          // B rows (N) per CTA
   static constexpr uint32_t kStageA = kRowsA * kNsBK * 2; // 16 KiB
   static constexpr uint32_t kStageB = kRowsB * kNsBK * 2; // 32 or 16 KiB
-  static constexpr int kStages = CG == 1 ? 4 : 6;
+#ifndef OSH_CG2_STAGES
+#define OSH_CG2_STAGES 5  // 5 x 32 KiB leaves ~49 KiB for co-resident update kernels
+#endif
+  static constexpr int kStages = CG == 1 ? 4 : OSH_CG2_STAGES;
 };
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kEpiStageFloats = 32 * 33;  // per epilogue warp: 32x32 fp32 transpose tile

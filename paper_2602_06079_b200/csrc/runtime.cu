@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -97,6 +98,8 @@ void free_layout(osh_ctx* ctx) {
   destroy_events(ctx->rs_ev);
   destroy_events(ctx->wave_begin);
   destroy_events(ctx->wave_end);
+  destroy_events(ctx->pre_ev);
+  destroy_events(ctx->ns_ev);
   if (ctx->nvls) {
     osh::nvls_free(ctx);
   } else {
@@ -155,6 +158,9 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
   ctx->comm_mode = comm_mode;
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking));
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  int prio_low = 0, prio_high = 0;
+  OSH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+  OSH_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->gemm_stream, cudaStreamNonBlocking, prio_high));
   for (cudaEvent_t& e : ctx->ev) OSH_CUDA_TRY(cudaEventCreate(&e));
   if (comm_mode == OSH_COMM_NCCL && dp_size > 1) {
     if (nccl_uid == nullptr) return osh::fail(OSH_ERR_ARG, "nccl_uid required for dp_size > 1");
@@ -193,12 +199,14 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->compute);
   cudaStreamSynchronize(ctx->comm_stream);
+  cudaStreamSynchronize(ctx->gemm_stream);
   free_layout(ctx);
   if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
   if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->compute);
   cudaStreamDestroy(ctx->comm_stream);
+  cudaStreamDestroy(ctx->gemm_stream);
   delete ctx;
   return OSH_OK;
 }
@@ -387,16 +395,23 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     budget = std::min<size_t>(24ull << 30, free_b / 3);
   }
   ctx->engine = std::make_unique<osh::MuonEngine>();
-  const int min_waves =
-      ctx->min_waves > 0 ? ctx->min_waves : (reduce_out && ctx->tp_size == 1 ? 4 : 1);
-  // (NVLS: reduce_out is false -> one wave when the workspace allows)
-  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves); st != OSH_OK)
+  const char* ov = std::getenv("OSH_OVERLAP");
+  ctx->overlap = ctx->tp_size == 1 && !reduce_out && !(ov != nullptr && std::strcmp(ov, "0") == 0);
+  int min_waves = ctx->min_waves > 0 ? ctx->min_waves
+                  : (ctx->overlap || (reduce_out && ctx->tp_size == 1)) ? 4 : 1;
+  if (const char* mw = std::getenv("OSH_MIN_WAVES"); mw != nullptr && std::atoi(mw) > 0)
+    min_waves = std::atoi(mw);
+  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves, ctx->overlap);
+      st != OSH_OK)
     return st;
+  ctx->overlap = ctx->overlap && ctx->engine->double_buffered() && ctx->engine->num_waves() > 1;
   if (ctx->tp_size > 1)
     if (osh_status st = osh::tp_setup(ctx, static_cast<int64_t>(budget)); st != OSH_OK) return st;
   OSH_CUDA_TRY(make_events(ctx->rs_ev, ctx->cuts.size()));
   OSH_CUDA_TRY(make_events(ctx->wave_begin, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->wave_end, static_cast<size_t>(ctx->engine->num_waves())));
+  OSH_CUDA_TRY(make_events(ctx->pre_ev, static_cast<size_t>(ctx->engine->num_waves())));
+  OSH_CUDA_TRY(make_events(ctx->ns_ev, static_cast<size_t>(ctx->engine->num_waves())));
   // The zero-fills and table uploads above ran on the legacy stream, which the
   // ctx's non-blocking streams do not order against: finish them now.
   OSH_CUDA_TRY(cudaDeviceSynchronize());
@@ -551,6 +566,45 @@ osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float s
   return OSH_OK;
 }
 
+namespace {
+
+// Waves on `cs`, either back to back or overlapped: momentum(w+1) and
+// apply(w) on cs run while the GEMMs of wave w run on the high-priority
+// gemm_stream (MuonEngine::run_pre/run_ns/run_post ordering contract).
+osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
+  osh::MuonEngine& eng = *ctx->engine;
+  const int nw = eng.num_waves();
+  if (!ctx->overlap) {
+    for (int w = 0; w < nw; ++w) {
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
+      if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaGetLastError());
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    }
+    return OSH_OK;
+  }
+  cudaStream_t gs = ctx->gemm_stream;
+  OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[0], cs));
+  if (osh_status st = eng.run_pre(0, cfg, cs); st != OSH_OK) return st;
+  OSH_CUDA_TRY(cudaEventRecord(ctx->pre_ev[0], cs));
+  for (int w = 0; w < nw; ++w) {
+    if (w + 1 < nw) {
+      if (osh_status st = eng.run_pre(w + 1, cfg, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaEventRecord(ctx->pre_ev[w + 1], cs));
+    }
+    OSH_CUDA_TRY(cudaStreamWaitEvent(gs, ctx->pre_ev[w], 0));
+    if (osh_status st = eng.run_ns(w, cfg, gs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ns_ev[w], gs));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ns_ev[w], 0));
+    if (osh_status st = eng.run_post(w, cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaGetLastError());
+  }
+  OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[nw - 1], cs));
+  return OSH_OK;
+}
+
+}  // namespace
+
 osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
                     void* host_replica_out) {
   if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
@@ -576,12 +630,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     };
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
-    for (int w = 0; w < nw; ++w) {
-      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
-      if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
-      OSH_CUDA_TRY(cudaGetLastError());
-      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-    }
+    if (osh_status st = run_waves_local(ctx, *cfg, cs); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
@@ -630,19 +679,23 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     return OSH_OK;
   };
   int ag_next = 0;
-  for (int w = 0; w < nw; ++w) {
-    if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[eng.wave_last_bucket(w)], 0));
-    OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
-    if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaGetLastError());
-    OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-    if (dist && ctx->tp_size == 1) {
-      // buckets no later wave of this rank touches are final on this rank
-      const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
-      if (done >= ag_next) {
-        OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
-        for (; ag_next <= done; ++ag_next)
-          if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+  if (!dist && ctx->tp_size == 1) {
+    if (osh_status st = run_waves_local(ctx, *cfg, cs); st != OSH_OK) return st;
+  } else {
+    for (int w = 0; w < nw; ++w) {
+      if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[eng.wave_last_bucket(w)], 0));
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
+      if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaGetLastError());
+      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+      if (dist && ctx->tp_size == 1) {
+        // buckets no later wave of this rank touches are final on this rank
+        const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
+        if (done >= ag_next) {
+          OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
+          for (; ag_next <= done; ++ag_next)
+            if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+        }
       }
     }
   }
@@ -739,8 +792,11 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
   const bool dist = distributed(ctx);
   t.rs_ms = dist && !ctx->rs_ev.empty() ? span(ctx->ev[0], ctx->rs_ev.back()) : 0.f;
   t.compute_ms = 0.f;  // busy time of the waves (excludes waiting for the RS)
-  for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
-    t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
+  if (ctx->overlap && !ctx->wave_begin.empty())
+    t.compute_ms = span(ctx->wave_begin.front(), ctx->wave_end.back());
+  else
+    for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
+      t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
   t.ag_ms = ms(2, 3);  // all-gather tail exposed after the last wave
   t.d2h_ms = ms(3, 4);
   t.total_ms = ms(5, 4);

@@ -39,6 +39,7 @@ struct osh_ctx {
   int comm_mode = 0;  // OSH_COMM_NCCL or OSH_COMM_NONE (caller reduces; no all-gather)
   ncclComm_t comm = nullptr;
   cudaStream_t compute = nullptr, comm_stream = nullptr;
+  cudaStream_t gemm_stream = nullptr;   // high priority: NS GEMMs of overlapped schedules
   cudaEvent_t ev[8] = {};
 
   // layout
@@ -64,7 +65,12 @@ struct osh_ctx {
   std::vector<cudaEvent_t> rs_ev;       // per bucket: reduce-scatter landed
   std::vector<cudaEvent_t> wave_begin;  // per engine wave
   std::vector<cudaEvent_t> wave_end;
-  int min_waves = 0;                    // 0: auto (1 for R = 1 or NVLS, 4 with NCCL)
+  int min_waves = 0;                    // 0: auto (4 with NCCL or overlap, else 1)
+  // overlapped schedule (single rank or NVLS): momentum / apply of adjacent
+  // waves run on `compute` while the NS GEMMs of the current wave run on the
+  // high-priority gemm_stream (double-buffered NS workspace)
+  bool overlap = false;
+  std::vector<cudaEvent_t> pre_ev, ns_ev;  // per wave
   // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
   // the update kernels reduce / broadcast through their multicast addresses
   int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
