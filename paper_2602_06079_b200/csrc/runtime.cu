@@ -100,6 +100,8 @@ void free_layout(osh_ctx* ctx) {
   destroy_events(ctx->wave_end);
   destroy_events(ctx->pre_ev);
   destroy_events(ctx->ns_ev);
+  destroy_events(ctx->h2d_ev);
+  destroy_events(ctx->ag_ev);
   if (ctx->nvls) {
     osh::nvls_free(ctx);
   } else {
@@ -161,6 +163,8 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
   int prio_low = 0, prio_high = 0;
   OSH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
   OSH_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->gemm_stream, cudaStreamNonBlocking, prio_high));
+  OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+  OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
   for (cudaEvent_t& e : ctx->ev) OSH_CUDA_TRY(cudaEventCreate(&e));
   if (comm_mode == OSH_COMM_NCCL && dp_size > 1) {
     if (nccl_uid == nullptr) return osh::fail(OSH_ERR_ARG, "nccl_uid required for dp_size > 1");
@@ -200,6 +204,8 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   cudaStreamSynchronize(ctx->compute);
   cudaStreamSynchronize(ctx->comm_stream);
   cudaStreamSynchronize(ctx->gemm_stream);
+  cudaStreamSynchronize(ctx->h2d_stream);
+  cudaStreamSynchronize(ctx->d2h_stream);
   free_layout(ctx);
   if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
   if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);
@@ -207,6 +213,8 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   cudaStreamDestroy(ctx->compute);
   cudaStreamDestroy(ctx->comm_stream);
   cudaStreamDestroy(ctx->gemm_stream);
+  cudaStreamDestroy(ctx->h2d_stream);
+  cudaStreamDestroy(ctx->d2h_stream);
   delete ctx;
   return OSH_OK;
 }
@@ -398,7 +406,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   const char* ov = std::getenv("OSH_OVERLAP");
   ctx->overlap = ctx->tp_size == 1 && !reduce_out && !(ov != nullptr && std::strcmp(ov, "0") == 0);
   int min_waves = ctx->min_waves > 0 ? ctx->min_waves
-                  : (ctx->overlap || (reduce_out && ctx->tp_size == 1)) ? 4 : 1;
+                  : ctx->overlap ? 8 : (reduce_out && ctx->tp_size == 1) ? 4 : 1;
   if (const char* mw = std::getenv("OSH_MIN_WAVES"); mw != nullptr && std::atoi(mw) > 0)
     min_waves = std::atoi(mw);
   if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves, ctx->overlap);
@@ -411,6 +419,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   OSH_CUDA_TRY(make_events(ctx->wave_begin, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->wave_end, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->pre_ev, static_cast<size_t>(ctx->engine->num_waves())));
+  OSH_CUDA_TRY(make_events(ctx->h2d_ev, ctx->cuts.size()));
+  OSH_CUDA_TRY(make_events(ctx->ag_ev, ctx->cuts.size()));
   OSH_CUDA_TRY(make_events(ctx->ns_ev, static_cast<size_t>(ctx->engine->num_waves())));
   // The zero-fills and table uploads above ran on the legacy stream, which the
   // ctx's non-blocking streams do not order against: finish them now.
@@ -571,24 +581,60 @@ namespace {
 // Waves on `cs`, either back to back or overlapped: momentum(w+1) and
 // apply(w) on cs run while the GEMMs of wave w run on the high-priority
 // gemm_stream (MuonEngine::run_pre/run_ns/run_post ordering contract).
-osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
+// `pipelined`: the step's gradients arrive per bucket on h2d_stream (wave w
+// waits for the buckets it reads) and finished replica buckets leave on
+// d2h_stream after the wave that completes them.
+struct HostIo {
+  bool h2d = false;        // wait for h2d_ev before a wave's momentum
+  void* replica_out = nullptr;  // per-bucket D2H after each wave (nullptr: none)
+  int d2h_next = 0;
+};
+
+osh_status d2h_buckets(osh_ctx* ctx, HostIo& io, int upto, cudaEvent_t ready) {
+  if (io.replica_out == nullptr || upto < io.d2h_next) return OSH_OK;
+  OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ready, 0));
+  const int64_t b0 = ctx->bucket_base[io.d2h_next];
+  const int64_t b1 = upto + 1 < static_cast<int>(ctx->bucket_base.size()) ? ctx->bucket_base[upto + 1]
+                                                                          : ctx->total_numel;
+  OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<__nv_bfloat16*>(io.replica_out) + b0, ctx->replica + b0,
+                               2 * static_cast<size_t>(b1 - b0), cudaMemcpyDeviceToHost,
+                               ctx->d2h_stream));
+  io.d2h_next = upto + 1;
+  return OSH_OK;
+}
+
+osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs, HostIo& io) {
   osh::MuonEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
+  const int nb = static_cast<int>(ctx->cuts.size());
+  auto wait_input = [&](int w) -> osh_status {
+    if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[eng.wave_last_bucket(w)], 0));
+    return OSH_OK;
+  };
+  // after wave w every bucket before the next wave's first one is final
+  auto wave_done = [&](int w) -> osh_status {
+    OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    return d2h_buckets(ctx, io, w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1,
+                       ctx->wave_end[w]);
+  };
   if (!ctx->overlap) {
     for (int w = 0; w < nw; ++w) {
+      if (osh_status st = wait_input(w); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
       if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaGetLastError());
-      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+      if (osh_status st = wave_done(w); st != OSH_OK) return st;
     }
     return OSH_OK;
   }
   cudaStream_t gs = ctx->gemm_stream;
+  if (osh_status st = wait_input(0); st != OSH_OK) return st;
   OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[0], cs));
   if (osh_status st = eng.run_pre(0, cfg, cs); st != OSH_OK) return st;
   OSH_CUDA_TRY(cudaEventRecord(ctx->pre_ev[0], cs));
   for (int w = 0; w < nw; ++w) {
     if (w + 1 < nw) {
+      if (osh_status st = wait_input(w + 1); st != OSH_OK) return st;
       if (osh_status st = eng.run_pre(w + 1, cfg, cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaEventRecord(ctx->pre_ev[w + 1], cs));
     }
@@ -598,8 +644,8 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
     OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ns_ev[w], 0));
     if (osh_status st = eng.run_post(w, cfg, cs); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaGetLastError());
+    if (osh_status st = wave_done(w); st != OSH_OK) return st;
   }
-  OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[nw - 1], cs));
   return OSH_OK;
 }
 
@@ -613,8 +659,28 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   const bool dist = distributed(ctx);
   cudaStream_t cs = ctx->compute, ns = ctx->comm_stream;
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[5], cs));
-  if (host_grads != nullptr)
+  // Host I/O. NVLS and TP: whole-buffer copies on cs (a remote owner may read
+  // any bucket after the start barrier; TP groups need every shard). Else the
+  // gradient arrives bucket by bucket on h2d_stream and each wave / RS waits
+  // only for its own buckets; the replica leaves per finished bucket.
+  HostIo io;
+  const bool pipelined = !ctx->nvls && ctx->tp_size == 1;
+  if (host_grads != nullptr && pipelined) {
+    io.h2d = true;
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
+    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+      const size_t off = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->bucket_base[b]);
+      const size_t len = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->layout.buckets[b].numel);
+      OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->grad) + off,
+                                   static_cast<const uint8_t*>(host_grads) + off, len,
+                                   cudaMemcpyHostToDevice, ctx->h2d_stream));
+      OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_ev[b], ctx->h2d_stream));
+    }
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
+  } else if (host_grads != nullptr) {
     OSH_CUDA_TRY(cudaMemcpyAsync(ctx->grad, host_grads, gbytes, cudaMemcpyHostToDevice, cs));
+  }
+  if (host_replica_out != nullptr && pipelined) io.replica_out = host_replica_out;
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
   const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
   const size_t es = grad_esize(ctx->grad_dtype);
@@ -630,7 +696,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     };
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
-    if (osh_status st = run_waves_local(ctx, *cfg, cs); st != OSH_OK) return st;
+    if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
@@ -639,6 +705,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
                                    2 * static_cast<size_t>(ctx->total_numel),
                                    cudaMemcpyDeviceToHost, cs));
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
+    ctx->last_h2d_pipelined = false;
     const osh::NsLaunchStats& s = eng.stats();
     ctx->last_timing.gemm_launches = s.launches_gemm;
     ctx->last_timing.elementwise_launches = s.launches_elementwise;
@@ -651,6 +718,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     // sum of all ranks' slices in its grad_owned region (local grads intact).
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
     for (int b = 0; b < nb; ++b) {
+      if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->h2d_ev[b], 0));
       OSH_NCCL_TRY(ncclGroupStart());
       for (int r = 0; r < ctx->size; ++r) {
         const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
@@ -676,14 +744,16 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       OSH_NCCL_TRY(ncclBroadcast(p, p, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, ns));
     }
     OSH_NCCL_TRY(ncclGroupEnd());
-    return OSH_OK;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ag_ev[b], ns));
+    return d2h_buckets(ctx, io, b, ctx->ag_ev[b]);
   };
   int ag_next = 0;
   if (!dist && ctx->tp_size == 1) {
-    if (osh_status st = run_waves_local(ctx, *cfg, cs); st != OSH_OK) return st;
+    if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
   } else {
     for (int w = 0; w < nw; ++w) {
       if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[eng.wave_last_bucket(w)], 0));
+      else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[eng.wave_last_bucket(w)], 0));
       OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
       if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaGetLastError());
@@ -715,11 +785,18 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   } else {
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
   }
-  if (host_replica_out != nullptr)
+  if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[nb - 1], 0));
+  if (io.replica_out != nullptr) {
+    if (osh_status st = d2h_buckets(ctx, io, nb - 1, ctx->ev[3]); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->d2h_stream));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[6], 0));
+  } else if (host_replica_out != nullptr) {
     OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
                                  2 * static_cast<size_t>(ctx->total_numel),
                                  cudaMemcpyDeviceToHost, cs));
+  }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
+  ctx->last_h2d_pipelined = io.h2d;
   const osh::NsLaunchStats& s = ctx->engine->stats();
   ctx->last_timing.gemm_launches = s.launches_gemm;
   ctx->last_timing.elementwise_launches = s.launches_elementwise;
@@ -788,7 +865,10 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
     return cudaEventElapsedTime(&t, a, b) == cudaSuccess ? t : 0.f;
   };
   osh_step_timing t = ctx->last_timing;
-  t.h2d_ms = ms(5, 0);
+  // pipelined host I/O: h2d_ms = until the last bucket landed (overlaps the
+  // waves); d2h_ms = the D2H tail after the last wave / all-gather
+  t.h2d_ms = ctx->last_h2d_pipelined && !ctx->h2d_ev.empty() ? span(ctx->ev[5], ctx->h2d_ev.back())
+                                                              : ms(5, 0);
   const bool dist = distributed(ctx);
   t.rs_ms = dist && !ctx->rs_ev.empty() ? span(ctx->ev[0], ctx->rs_ev.back()) : 0.f;
   t.compute_ms = 0.f;  // busy time of the waves (excludes waiting for the RS)

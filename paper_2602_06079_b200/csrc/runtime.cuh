@@ -40,6 +40,9 @@ struct osh_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t compute = nullptr, comm_stream = nullptr;
   cudaStream_t gemm_stream = nullptr;   // high priority: NS GEMMs of overlapped schedules
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // osh_step host I/O, per bucket
+  std::vector<cudaEvent_t> h2d_ev, ag_ev;  // per bucket: gradient landed / all-gathered
+  bool last_h2d_pipelined = false;
   cudaEvent_t ev[8] = {};
 
   // layout
