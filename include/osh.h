@@ -165,15 +165,25 @@ typedef struct osh_gemm_problem {
   osh_matrix_ref b;   /* K-major: N x K ; MN-major: K x N */
   int32_t b_mn_major;
   int32_t reserved_;
-  osh_matrix_ref out; /* M x N bf16 */
+  osh_matrix_ref out; /* M x N bf16 (OSH_EPI_STAT: fp32) */
   osh_matrix_ref aux; /* M x N bf16 */
   const float* scale; /* per batch, nullable */
   const osh_final_target* final_targets;
-  int32_t symmetric;  /* GRAM / POLY with M == N: compute the upper triangle, mirror */
-  int32_t reserved2_;
+  int32_t symmetric;  /* GRAM / POLY / STAT / SPLIT with M == N: upper-triangle tiles, mirror */
+  int32_t out_seg;    /* OSH_EPI_SPLIT: segment width in elements (>= N) */
 } osh_gemm_problem;
 
-enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3 };
+/* Epilogues (acc = the fp32 tcgen05 accumulator, s = per-batch scale or 1):
+ *   GRAM   out = s*acc               POLY  out = alpha*aux + beta*acc
+ *   UPDATE out = s*(alpha*aux + acc) FINAL W -= lr*s*(alpha*aux + acc) (+ replica)
+ *   STAT   out(fp32) = alpha*out + s*acc   (Shampoo statistics, read-modify-write)
+ *   SPLIT  v = s*acc stored as bf16 hi = bf16(v), lo = bf16(v - hi) in five
+ *          segments [hi | lo | hi | hi | lo] of out_seg columns: columns
+ *          [0, 3*K) are the A view and [2*K, 5*K) the B view of a bf16x3
+ *          product hi*hi + lo*hi + hi*lo (fp32-accurate Newton iterations).
+ * alpha == 0 skips reading aux (aux may then be null). */
+enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3,
+       OSH_EPI_STAT = 4, OSH_EPI_SPLIT = 5 };
 
 /* UMMA CTA group of subsequent GEMM launches (process-wide): 2 = CTA pairs
  * (tcgen05.mma.cta_group::2, 256x256 tiles; default), 1 = single-CTA
@@ -234,6 +244,25 @@ osh_status osh_ctx_destroy(osh_ctx* ctx);
  *   OSH_COLL_AUTO  NVLS when available, else NCCL (default). */
 enum { OSH_COLL_AUTO = 0, OSH_COLL_NCCL = 1, OSH_COLL_NVLS = 2 };
 osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode);
+
+/* Optimizer run on the owned tensors (call before set_layout).
+ *   OSH_OPT_MUON     the Canzona/Muon step (default; verify.hpp:118-147)
+ *   OSH_OPT_SHAMPOO  builder-defined blocked Shampoo (the reference only costs
+ *                    it: cost.hpp:47-48,68-75 — specification and fp64 oracle
+ *                    in oracle/shampoo_oracle.py). osh_step's osh_muon_cfg
+ *                    supplies lr and beta (= beta1, momentum); ns_* are unused.
+ * Shampoo needs tp_size == 1. */
+typedef struct osh_shampoo_cfg {
+  double beta2;           /* statistics decay (0.95) */
+  double eps;             /* relative regularisation of the roots (1e-4) */
+  int32_t block;          /* max preconditioner dimension, multiple of 64 (1024) */
+  int32_t precond_every;  /* inverse-root refresh period in steps (10) */
+  int32_t newton_iters;   /* coupled-Newton iterations per root (16) */
+  int32_t reserved;
+} osh_shampoo_cfg;
+enum { OSH_OPT_MUON = 0, OSH_OPT_SHAMPOO = 1 };
+osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out);
+osh_status osh_ctx_set_optimizer(osh_ctx* ctx, int32_t kind, const osh_shampoo_cfg* cfg);
 
 /* Installs the parameter list (ids dense 0..n-1, declaration order), the
  * bucket capacity and the dp plan's cut vectors (n_buckets x (dp_size+1),

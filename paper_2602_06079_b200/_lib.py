@@ -70,6 +70,11 @@ class CtxInfo(ctypes.Structure):
                 ("reserved_", c_int32)]
 
 
+class ShampooCfgC(ctypes.Structure):
+    _fields_ = [("beta2", c_double), ("eps", c_double), ("block", c_int32),
+                ("precond_every", c_int32), ("newton_iters", c_int32), ("reserved", c_int32)]
+
+
 class StepTiming(ctypes.Structure):
     _fields_ = [("h2d_ms", c_float), ("rs_ms", c_float), ("compute_ms", c_float),
                 ("ag_ms", c_float), ("d2h_ms", c_float), ("total_ms", c_float),
@@ -86,7 +91,7 @@ class GemmProblem(ctypes.Structure):
     _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
                 ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
                 ("scale", c_void_p), ("final_targets", c_void_p), ("symmetric", c_int32),
-                ("reserved2_", c_int32)]
+                ("out_seg", c_int32)]
 
 
 _lib = None
@@ -145,6 +150,8 @@ def _declare(L: ctypes.CDLL) -> None:
          c_void_p, c_void_p, POINTER(c_void_p)),
         ("osh_ctx_set_tp_capacity", c_int32, c_void_p, c_uint64),
         ("osh_ctx_set_collectives", c_int32, c_void_p, c_int32),
+        ("osh_shampoo_cfg_default", c_int32, POINTER(ShampooCfgC)),
+        ("osh_ctx_set_optimizer", c_int32, c_void_p, c_int32, POINTER(ShampooCfgC)),
         ("osh_ctx_set_layout", c_int32, c_void_p, POINTER(ParamDesc), c_int32, c_int64,
          POINTER(c_int64), c_int32, c_int32, c_int64),
         ("osh_ctx_get_info", c_int32, c_void_p, POINTER(CtxInfo)),

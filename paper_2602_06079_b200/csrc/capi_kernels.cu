@@ -40,6 +40,7 @@ extern "C" osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* prob
     d[i].scale = p.scale;
     d[i].final_targets = reinterpret_cast<const osh::NsFinalTarget*>(p.final_targets);
     d[i].symmetric = p.symmetric;
+    d[i].out_seg = p.out_seg;
   }
   const cudaError_t e = osh::ns_gemm_launch(epilogue, d, n_problems, alpha, beta, lr,
                                             static_cast<cudaStream_t>(stream));

@@ -51,64 +51,13 @@ Shape shape_of(int rows, int cols) {
 
 }  // namespace
 
-MuonEngine::~MuonEngine() {
-  release();
-  for (const Timed& t : timed_) {
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
-  }
-  for (cudaEvent_t ev : event_pool_) cudaEventDestroy(ev);
-}
+MuonEngine::~MuonEngine() { release(); }
 
-cudaEvent_t MuonEngine::take_event() {
-  if (!event_pool_.empty()) {
-    cudaEvent_t ev = event_pool_.back();
-    event_pool_.pop_back();
-    return ev;
-  }
-  cudaEvent_t ev = nullptr;
-  cudaEventCreate(&ev);
-  return ev;
-}
-
-void MuonEngine::read_profile(int* launches, double* flops, double* exec_flops, double* ms,
-                              bool reset) {
-  *launches = 0;
-  *flops = *exec_flops = *ms = 0.0;
-  for (const Timed& t : timed_) {
-    float dt = 0.f;
-    if (t.mode >= kModeElementwise) continue;
-    cudaEventSynchronize(t.b);
-    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
-    ++*launches;
-    *flops += t.flops;
-    *exec_flops += t.exec_flops;
-    *ms += dt;
-  }
-  if (reset) {
-    for (const Timed& t : timed_) {
-      event_pool_.push_back(t.a);
-      event_pool_.push_back(t.b);
-    }
-    timed_.clear();
-  }
-}
-
-std::string MuonEngine::profile_text() const {
-  static const char* kNames[] = {"gram", "poly", "update", "final", "?", "?", "?", "?",
-                                 "momentum_vector", "momentum_matrix", "ns_scales",
-                                 "apply_update", "partial_sums"};
-  std::string out;
-  char line[512];
-  for (const Timed& t : timed_) {
-    float dt = 0.f;
-    cudaEventSynchronize(t.b);
-    if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
-    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", kNames[t.mode < 13 ? t.mode : 4], dt, t.flops,
-                  t.exec_flops, t.what.c_str());
-    out += line;
-  }
-  return out;
+const char* MuonEngine::elementwise_name(int mode) const {
+  static const char* kNames[] = {"momentum_vector", "momentum_matrix", "ns_scales", "apply_update",
+                                 "partial_sums"};
+  const int i = mode - kModeElementwise;
+  return i >= 0 && i < 5 ? kNames[i] : "elementwise";
 }
 
 void MuonEngine::release() {
@@ -345,29 +294,6 @@ osh_status MuonEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
 
 // profile mode: CUDA events around each elementwise launch; `bytes` is the
 // algorithmic HBM (or, NVLS, NVLink) traffic of the launch
-template <typename F>
-cudaError_t MuonEngine::timed_elementwise(int mode, double bytes, double elems, cudaStream_t s,
-                                          F&& launch) {
-  const bool rec = profile_ && timed_.size() < 100000;
-  Timed t{};
-  if (rec) {
-    t.a = take_event();
-    t.b = take_event();
-    t.flops = bytes;
-    t.exec_flops = 0.0;
-    t.mode = mode;
-    t.what = std::to_string(static_cast<long long>(elems));
-    cudaEventRecord(t.a, s);
-  }
-  const cudaError_t err = launch();
-  if (rec) {
-    cudaEventRecord(t.b, s);
-    timed_.push_back(std::move(t));
-  }
-  ++stats_.launches_elementwise;
-  return err;
-}
-
 osh_status MuonEngine::run_pre(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
   const Wave& w = waves_[wi];
   if (cfg.ns_steps < 1 && w.n_slots > 0)
@@ -419,29 +345,7 @@ osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
                              nullptr, 0};
     }
     const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b) {
-      const bool rec = profile_ && timed_.size() < 100000;
-      Timed t{};
-      if (rec) {
-        t.a = take_event();
-        t.b = take_event();
-        t.flops = ns_gemm_flops(pd, np);
-        t.exec_flops = ns_gemm_executed_flops(pd, np);
-        t.mode = mode;
-        for (int q = 0; q < np; ++q) {
-          if (q) t.what += "+";
-          t.what += std::to_string(pd[q].a.batch) + "x" + std::to_string(pd[q].a.rows) + "x" +
-                    std::to_string(pd[q].b_mn_major ? pd[q].b.cols : pd[q].b.rows) + "x" +
-                    std::to_string(pd[q].a.cols);
-        }
-        cudaEventRecord(t.a, s);
-      }
-      const cudaError_t err = ns_gemm_launch(mode, pd, np, a, b, 0.f, s);
-      if (rec) {
-        cudaEventRecord(t.b, s);
-        timed_.push_back(std::move(t));
-      }
-      stats_.gemm_flops += ns_gemm_flops(pd, np);
-      return err;
+      return timed_gemm(mode, pd, np, a, b, s);
     };
     cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f);
     if (e == cudaSuccess)
@@ -449,7 +353,6 @@ osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
     if (e == cudaSuccess) e = timed_launch(kEpiUpdate, upd, static_cast<float>(cfg.ns_a), 0.f);
     if (e != cudaSuccess)
       return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") + cudaGetErrorString(e));
-    stats_.launches_gemm += 3;
   }
   return OSH_OK;
 }

@@ -133,6 +133,52 @@ __device__ __forceinline__ void store_row32(__nv_bfloat16* dst, int col0, int n,
   }
 }
 
+// fp32 read-modify-write of 32 consecutive elements: dst = alpha * dst + v.
+__device__ __forceinline__ void rmw_row32(float* dst, int col0, int n, float alpha,
+                                          const float (&v)[32]) {
+  if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o = d4[q];
+      o.x = alpha * o.x + v[q * 4 + 0];
+      o.y = alpha * o.y + v[q * 4 + 1];
+      o.z = alpha * o.z + v[q * 4 + 2];
+      o.w = alpha * o.w + v[q * 4 + 3];
+      d4[q] = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < n) dst[j] = alpha * dst[j] + v[j];
+  }
+}
+
+// Symmetric fp32 read-modify-write (same single-writer rule as below).
+__device__ __forceinline__ void rmw_row32_sym(float* out, long long ld, int row, int col0, int n,
+                                              float alpha, const float (&v)[32]) {
+  if (col0 >= row) {
+    rmw_row32(out + row * ld + col0, col0, n, alpha, v);
+  } else if (col0 + 31 >= row) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j >= row && col0 + j < n) {
+        float* p = out + row * ld + col0 + j;
+        *p = alpha * *p + v[j];
+      }
+  }
+  if (col0 + 31 > row) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int c = col0 + j;
+      if (c > row && c < n) {
+        float* p = out + static_cast<long long>(c) * ld + row;
+        *p = alpha * *p + v[j];
+      }
+    }
+  }
+}
+
 // Symmetric output: element (row, c) is written directly when c >= row and
 // mirrored to (c, row) when c > row, so every element has exactly one writer.
 __device__ __forceinline__ void store_row32_sym(__nv_bfloat16* out, long long ld, int row,
@@ -310,7 +356,11 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           else
             store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiPoly) {
-          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+          if (P.alpha != 0.f)
+            load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+          else
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = P.alpha * v[j] + P.beta * __uint_as_float(r[j]);
           if (pr.symmetric)
@@ -318,10 +368,46 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           else
             store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiUpdate) {
-          load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+          if (P.alpha != 0.f)
+            load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
+          else
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = s * (P.alpha * v[j] + __uint_as_float(r[j]));
           store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
+        } else if constexpr (MODE == kEpiStat) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = s * __uint_as_float(r[j]);
+          float* o = pr.out32 + c.b * pr.out_bstride;
+          if (pr.symmetric)
+            rmw_row32_sym(o, pr.out_ld, row, col0, pr.N, P.alpha, v);
+          else
+            rmw_row32(o + row * pr.out_ld + col0, col0, pr.N, P.alpha, v);
+        } else if constexpr (MODE == kEpiSplit) {
+          float lo[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = s * __uint_as_float(r[j]);
+            v[j] = __bfloat162float(__float2bfloat16_rn(x));
+            lo[j] = x - v[j];
+          }
+          __nv_bfloat16* o = pr.out + c.b * pr.out_bstride;
+          const long long sg = pr.out_seg;
+          if (pr.symmetric) {
+            store_row32_sym(o, pr.out_ld, row, col0, pr.N, v);
+            store_row32_sym(o + sg, pr.out_ld, row, col0, pr.N, lo);
+            store_row32_sym(o + 2 * sg, pr.out_ld, row, col0, pr.N, v);
+            store_row32_sym(o + 3 * sg, pr.out_ld, row, col0, pr.N, v);
+            store_row32_sym(o + 4 * sg, pr.out_ld, row, col0, pr.N, lo);
+          } else {
+            __nv_bfloat16* d = o + row * pr.out_ld + col0;
+            store_row32(d, col0, pr.N, v);
+            store_row32(d + sg, col0, pr.N, lo);
+            store_row32(d + 2 * sg, col0, pr.N, v);
+            store_row32(d + 3 * sg, col0, pr.N, v);
+            store_row32(d + 4 * sg, col0, pr.N, lo);
+          }
         } else {  // kEpiFinal: every lane takes part (warp-level transpose below)
           float upd[32];
           if (row_ok) {
@@ -565,7 +651,11 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     }
     pr.tiles_m = (pr.M + P.tile_m - 1) / P.tile_m;
     pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
-    pr.symmetric = d.symmetric && pr.M == pr.N && (mode == kEpiGram || mode == kEpiPoly) ? 1 : 0;
+    pr.symmetric = d.symmetric && pr.M == pr.N &&
+                           (mode == kEpiGram || mode == kEpiPoly || mode == kEpiStat ||
+                            mode == kEpiSplit)
+                       ? 1
+                       : 0;
     if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
     pr.tiles_per_batch =
         pr.symmetric ? sym_tiles(pr.tiles_m, pr.tiles_n, P.tile_m) : pr.tiles_m * pr.tiles_n;
@@ -580,9 +670,19 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     pr.scale = d.scale;
     pr.final_targets = d.final_targets;
     if (mode == kEpiFinal && pr.final_targets == nullptr) return cudaErrorInvalidValue;
-    if ((mode == kEpiPoly || mode == kEpiUpdate || mode == kEpiFinal) && pr.aux == nullptr)
+    if ((mode == kEpiPoly || mode == kEpiUpdate || mode == kEpiFinal) && pr.aux == nullptr &&
+        alpha != 0.f)
       return cudaErrorInvalidValue;
-    if (mode != kEpiFinal && pr.out == nullptr) return cudaErrorInvalidValue;
+    pr.out32 = nullptr;
+    pr.out_seg = d.out_seg;
+    if (mode == kEpiStat) {
+      pr.out32 = static_cast<float*>(const_cast<void*>(d.out.ptr));
+      pr.out = nullptr;
+      if (pr.out32 == nullptr) return cudaErrorInvalidValue;
+    } else if (mode != kEpiFinal && pr.out == nullptr) {
+      return cudaErrorInvalidValue;
+    }
+    if (mode == kEpiSplit && d.out_seg < pr.N) return cudaErrorInvalidValue;
   }
   P.total_tiles = tiles;
   if (cg == 2) {
@@ -591,6 +691,8 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
       case kEpiPoly: return launch_mode<kEpiPoly, 2>(P, stream);
       case kEpiUpdate: return launch_mode<kEpiUpdate, 2>(P, stream);
       case kEpiFinal: return launch_mode<kEpiFinal, 2>(P, stream);
+      case kEpiStat: return launch_mode<kEpiStat, 2>(P, stream);
+      case kEpiSplit: return launch_mode<kEpiSplit, 2>(P, stream);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -599,6 +701,8 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     case kEpiPoly: return launch_mode<kEpiPoly, 1>(P, stream);
     case kEpiUpdate: return launch_mode<kEpiUpdate, 1>(P, stream);
     case kEpiFinal: return launch_mode<kEpiFinal, 1>(P, stream);
+    case kEpiStat: return launch_mode<kEpiStat, 1>(P, stream);
+    case kEpiSplit: return launch_mode<kEpiSplit, 1>(P, stream);
     default: return cudaErrorInvalidValue;
   }
 }

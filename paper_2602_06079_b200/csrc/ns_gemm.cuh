@@ -30,7 +30,16 @@ constexpr int kNsStages = 4;
 constexpr int kNsThreads = 256;  // warps 0-3: TMA / MMA / TMEM alloc / spare, 4-7: epilogue
 constexpr int kMaxProblems = 4;
 
-enum NsEpilogue : int { kEpiGram = 0, kEpiPoly = 1, kEpiUpdate = 2, kEpiFinal = 3 };
+enum NsEpilogue : int {
+  kEpiGram = 0,    // out = s * acc                                  (bf16)
+  kEpiPoly = 1,    // out = alpha * aux + beta * acc                 (bf16)
+  kEpiUpdate = 2,  // out = s * (alpha * aux + acc)                  (bf16)
+  kEpiFinal = 3,   // W -= lr * s * (alpha * aux + acc)              (fp32 master + replica)
+  kEpiStat = 4,    // out32 = alpha * out32 + s * acc                (fp32 read-modify-write)
+  kEpiSplit = 5,   // v = s * acc as bf16 hi/lo pairs in 5 segments of out_seg columns:
+                   //   [hi | lo | hi | hi | lo]; columns [0,3n) are the A-operand view and
+                   //   [2n,5n) the B-operand view of a bf16x3 product (hi*hi + lo*hi + hi*lo)
+};
 
 // Where the last Newton-Schulz step of one matrix lands: the fp32 master
 // weight (and its bf16 replica) in the tensor's ORIGINAL orientation.
@@ -58,6 +67,8 @@ struct alignas(64) NsGemmProblem {
   long long aux_ld, aux_bstride;
   const float* scale;                 // per-batch multiplier, nullable (= 1)
   const NsFinalTarget* final_targets; // per batch, kEpiFinal only
+  float* out32;                       // kEpiStat: fp32 output (ld / bstride as out)
+  long long out_seg;                  // kEpiSplit: segment width in elements
 };
 
 struct NsGemmParams {
@@ -84,7 +95,8 @@ struct NsProblemDesc {
   NsMatrixRef aux;      // M x N (bf16) or nullptr
   const float* scale;   // device, per batch
   const NsFinalTarget* final_targets;  // device, per batch
-  int symmetric = 0;    // GRAM / POLY: out = out^T, compute the upper triangle only
+  int symmetric = 0;    // GRAM / POLY / STAT / SPLIT: out = out^T, upper-triangle tiles only
+  long long out_seg = 0;  // kEpiSplit segment width (elements)
 };
 
 // Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).

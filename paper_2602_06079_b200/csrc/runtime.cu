@@ -198,6 +198,38 @@ osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode) {
   return OSH_OK;
 }
 
+osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out) {
+  if (out == nullptr) return osh::fail(OSH_ERR_ARG, "null output");
+  const osh::ShampooConfig d;
+  std::memset(out, 0, sizeof(*out));
+  out->beta2 = d.beta2;
+  out->eps = d.eps;
+  out->block = d.block;
+  out->precond_every = d.precond_every;
+  out->newton_iters = d.newton_iters;
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_optimizer(osh_ctx* ctx, int32_t kind, const osh_shampoo_cfg* cfg) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (kind != OSH_OPT_MUON && kind != OSH_OPT_SHAMPOO)
+    return osh::fail(OSH_ERR_ARG, "unknown optimizer");
+  if (kind == OSH_OPT_SHAMPOO && ctx->tp_size > 1)
+    return osh::fail(OSH_ERR_UNSUPPORTED, "Shampoo runs with tp_size == 1");
+  ctx->optimizer = kind;
+  if (cfg != nullptr) {
+    if (cfg->block < 64 || cfg->block % 64 != 0 || cfg->precond_every < 1 ||
+        cfg->newton_iters < 1 || !(cfg->beta2 >= 0.0 && cfg->beta2 <= 1.0) || !(cfg->eps > 0.0))
+      return osh::fail(OSH_ERR_CONFIG, "invalid osh_shampoo_cfg");
+    ctx->shampoo.beta2 = cfg->beta2;
+    ctx->shampoo.eps = cfg->eps;
+    ctx->shampoo.block = cfg->block;
+    ctx->shampoo.precond_every = cfg->precond_every;
+    ctx->shampoo.newton_iters = cfg->newton_iters;
+  }
+  return OSH_OK;
+}
+
 osh_status osh_ctx_destroy(osh_ctx* ctx) {
   if (ctx == nullptr) return OSH_OK;
   cudaSetDevice(ctx->device);
@@ -370,6 +402,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     const ParamSpec& ps = ctx->params[p];
     osh::MuonTensorDesc t;
     t.is_matrix = ps.is_matrix() ? 1 : 0;
+    t.vocab_space = ps.vocab_space ? 1 : 0;
     t.bucket = ctx->bucket_of[p];
     t.rows = static_cast<int>(ps.shape[0]);
     t.cols = ps.is_matrix() ? static_cast<int>(ps.shape[1]) : 1;
@@ -402,7 +435,10 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     cudaMemGetInfo(&free_b, &total_b);
     budget = std::min<size_t>(24ull << 30, free_b / 3);
   }
-  ctx->engine = std::make_unique<osh::MuonEngine>();
+  if (ctx->optimizer == OSH_OPT_SHAMPOO)
+    ctx->engine = std::make_unique<osh::ShampooEngine>(ctx->shampoo);
+  else
+    ctx->engine = std::make_unique<osh::MuonEngine>();
   const char* ov = std::getenv("OSH_OVERLAP");
   ctx->overlap = ctx->tp_size == 1 && !reduce_out && !(ov != nullptr && std::strcmp(ov, "0") == 0);
   int min_waves = ctx->min_waves > 0 ? ctx->min_waves
@@ -604,7 +640,7 @@ osh_status d2h_buckets(osh_ctx* ctx, HostIo& io, int upto, cudaEvent_t ready) {
 }
 
 osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs, HostIo& io) {
-  osh::MuonEngine& eng = *ctx->engine;
+  osh::OptimizerEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
   const int nb = static_cast<int>(ctx->cuts.size());
   auto wait_input = [&](int w) -> osh_status {
@@ -685,7 +721,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
   const size_t es = grad_esize(ctx->grad_dtype);
   const int nb = static_cast<int>(ctx->cuts.size());
-  osh::MuonEngine& eng = *ctx->engine;
+  osh::OptimizerEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
   if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
   if (ctx->nvls) {

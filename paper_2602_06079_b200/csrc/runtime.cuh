@@ -30,6 +30,7 @@
 #include <nccl.h>
 
 #include "ns_engine.cuh"
+#include "shampoo_engine.cuh"
 #include "optishard/optishard.hpp"
 #include "osh.h"
 
@@ -64,7 +65,7 @@ struct osh_ctx {
   __nv_bfloat16* replica = nullptr;
   float* w = nullptr;
   float* m = nullptr;
-  std::unique_ptr<osh::MuonEngine> engine;
+  std::unique_ptr<osh::OptimizerEngine> engine;
   std::vector<cudaEvent_t> rs_ev;       // per bucket: reduce-scatter landed
   std::vector<cudaEvent_t> wave_begin;  // per engine wave
   std::vector<cudaEvent_t> wave_end;
@@ -77,6 +78,8 @@ struct osh_ctx {
   // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
   // the update kernels reduce / broadcast through their multicast addresses
   int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
+  int optimizer = 0;                    // OSH_OPT_MUON / OSH_OPT_SHAMPOO
+  osh::ShampooConfig shampoo;
   bool nvls = false;
   void* nvls_state = nullptr;
   void* mc_grad = nullptr;              // multicast address of grad

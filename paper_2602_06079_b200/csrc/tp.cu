@@ -208,7 +208,7 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
     finalize_tiles(ctx->tp_unpack[g], &ctx->tp_unpack_tiles[g]);
     finalize_tiles(ctx->tp_pack[g], &ctx->tp_pack_tiles[g]);
     auto eng = std::make_unique<MuonEngine>();
-    if (osh_status st = eng->build(tensors, ctx->grad_dtype, static_cast<size_t>(budget), 1);
+    if (osh_status st = eng->build(tensors, ctx->grad_dtype, static_cast<size_t>(budget), 1, false);
         st != OSH_OK)
       return st;
     ctx->tp_engines.push_back(std::move(eng));

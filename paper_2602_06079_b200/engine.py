@@ -39,6 +39,22 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+@dataclass
+class ShampooConfig:
+    """Builder-defined blocked Shampoo (osh.h osh_shampoo_cfg; specification
+    oracle/shampoo_oracle.py). lr / beta1 come from OptimizerConfig."""
+    beta2: float = 0.95
+    eps: float = 1e-4
+    block: int = 1024
+    precond_every: int = 10
+    newton_iters: int = 16
+
+    def c(self) -> _lib.ShampooCfgC:
+        return _lib.ShampooCfgC(self.beta2, self.eps, self.block, self.precond_every,
+                                self.newton_iters, 0)
+
+
+OPTIMIZERS = {"muon": 0, "shampoo": 1}
 COLLECTIVES = {"auto": 0, "nccl": 1, "nvls": 2}
 COLLECTIVE_NAMES = {0: "none", 1: "nccl", 2: "nvls"}
 
@@ -53,7 +69,8 @@ class DistributedMuon:
                  nccl_uid: Optional[bytes] = None, grad_dtype: str = "f32",
                  workspace_bytes: int = 0, tp_rank: int = 0, tp_size: int = 1,
                  tp_uid: Optional[bytes] = None, tp_capacity: Optional[int] = None,
-                 collectives: str = "auto"):
+                 collectives: str = "auto", optimizer: str = "muon",
+                 shampoo: Optional[ShampooConfig] = None):
         """With tp_size > 1: ``params`` are the FULL tensors, ``plan`` /
         ``bucket_capacity`` describe the DP partition of the TP-sharded view
         (planner.apply_tp_sharding), ``rank`` is the DP rank.
@@ -61,7 +78,9 @@ class DistributedMuon:
         ``collectives`` (dp_size > 1): "nccl" = NCCL reduce-scatter /
         all-gather kernels overlapped with the update, "nvls" = reduction and
         broadcast fused into the update kernels through NVSwitch multicast
-        (OshError when the node cannot), "auto" = nvls when available."""
+        (OshError when the node cannot), "auto" = nvls when available.
+        ``optimizer``: "muon" (the reference's step) or "shampoo" (builder-
+        defined blocked Shampoo, ``shampoo`` = its ShampooConfig)."""
         L = _lib.lib()
         self.params = list(params)
         self.rank, self.world = rank, plan.ranks
@@ -79,6 +98,10 @@ class DistributedMuon:
         if tp_capacity is not None:
             _lib.check(L.osh_ctx_set_tp_capacity(ctx, tp_capacity))
         _lib.check(L.osh_ctx_set_collectives(ctx, COLLECTIVES[collectives]))
+        if optimizer != "muon" or shampoo is not None:
+            sc = (shampoo or ShampooConfig()).c()
+            _lib.check(L.osh_ctx_set_optimizer(ctx, OPTIMIZERS[optimizer], ctypes.byref(sc)))
+        self.optimizer = optimizer
         cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)
         _lib.check(L.osh_ctx_set_layout(ctx, _desc_array(self.params), len(self.params),
                                         bucket_capacity,

@@ -214,3 +214,85 @@ def test_poly_symmetric_tiles(batch, m):
     assert not torch.isnan(o).any() and torch.equal(o, o.transpose(1, 2))
     af = a.float()
     assert relerr(o, B * af + C * af @ af) < 1e-2
+
+
+def mref32(t):
+    """MatrixRef for a [batch][rows][ld] fp32 tensor (STAT output)."""
+    assert t.dtype == torch.float32 and t.is_cuda and t.dim() == 3
+    m = _lib.MatrixRef()
+    m.ptr = t.data_ptr()
+    m.batch, m.rows, m.cols = t.shape
+    m.ld = t.stride(1)
+    m.bstride = t.stride(0)
+    return m
+
+
+@pytest.mark.parametrize("sym", [1, 0])
+@pytest.mark.parametrize("batch,m,n", [(2, 256, 768), (1, 200, 328), (3, 512, 512)])
+def test_stat_fp32_accumulate(batch, m, n, sym):
+    """Shampoo statistics: L = beta2 * L + G G^T in fp32 (read-modify-write)."""
+    g = padded(batch, m, n, n + (-n) % 8, scale=0.3)
+    l0 = torch.randn(batch, m, m, device="cuda")
+    l0 = l0 + l0.transpose(1, 2)  # symmetric like a statistics matrix
+    out = l0.clone()
+    p = _lib.GemmProblem()
+    p.a = mref(g, cols=n)
+    p.b = mref(g, cols=n)
+    p.out = mref32(out)
+    p.symmetric = sym
+    run(4, [p], alpha=0.95)
+    gf = g[:, :, :n].float()
+    ref = 0.95 * l0 + gf @ gf.transpose(1, 2)
+    assert relerr(out, ref) < 1e-5
+    if sym:
+        assert torch.equal(out, out.transpose(1, 2))
+
+
+def split5(x):
+    """[hi | lo | hi | hi | lo] bf16 layout of an fp32 [b][n][n] matrix."""
+    hi = x.bfloat16()
+    lo = (x - hi.float()).bfloat16()
+    return torch.cat([hi, lo, hi, hi, lo], dim=2).contiguous()
+
+
+@pytest.mark.parametrize("sym", [1, 0])
+@pytest.mark.parametrize("batch,n", [(2, 256), (1, 320), (3, 512)])
+def test_split_bf16x3_product(batch, n, sym):
+    """bf16x3 product of split operands: fp32-level accuracy (the Shampoo
+    coupled-Newton iteration), output again in the split layout."""
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn(batch, n, n, device="cuda", generator=gen, dtype=torch.float64) / n ** 0.5
+    a = (a + a.transpose(1, 2)) / 2
+    b = a @ a + 0.1 * a  # commutes with a: a @ b is symmetric
+    sa, sb = split5(a.float()), split5(b.float())
+    out = torch.zeros(batch, n, 5 * n, device="cuda", dtype=torch.bfloat16)
+    p = _lib.GemmProblem()
+    p.a = mref(sa, cols=3 * n)                       # A view: columns [0, 3n)
+    p.b = mref(sa[:, :, 2 * n:], cols=3 * n)          # (unused below, shape check)
+    bview = sb[:, :, 2 * n:]
+    p.b = _lib.MatrixRef()
+    p.b.ptr, p.b.batch, p.b.rows, p.b.cols = bview.data_ptr(), batch, n, 3 * n
+    p.b.ld, p.b.bstride = sb.stride(1), sb.stride(0)  # B view: columns [2n, 5n)
+    p.out = mref(out, cols=n)
+    p.out_seg = n
+    p.symmetric = sym
+    run(5, [p])
+    ref = a @ b
+    got = out[:, :, :n].double() + out[:, :, n:2 * n].double()
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    assert err < 2e-5, err  # bf16 alone would be ~4e-3
+    assert torch.equal(out[:, :, :n], out[:, :, 2 * n:3 * n])
+    assert torch.equal(out[:, :, :n], out[:, :, 3 * n:4 * n])
+    assert torch.equal(out[:, :, n:2 * n], out[:, :, 4 * n:])
+
+
+def test_poly_alpha_zero_skips_aux():
+    x = padded(2, 256, 256, scale=0.1)
+    out = torch.zeros_like(x)
+    p = _lib.GemmProblem()
+    p.a = mref(x)
+    p.b = mref(x)
+    p.out = mref(out)
+    run(1, [p], alpha=0.0, beta=2.0)  # aux is null: must not be read
+    xf = x.float()
+    assert relerr(out, 2.0 * xf @ xf.transpose(1, 2)) < 1e-2

@@ -78,10 +78,10 @@ def test_host_buffers_equal_device_path(grad_dtype, pinned):
 
 def test_host_buffers_back_to_back_schedule():
     env = dict(os.environ, OSH_OVERLAP="0")
-    code = ("import sys; sys.path.insert(0, %r); import numpy as np; "
-            "from tests.test_gpu_host_io import run, params; ps = params(); "
+    code = ("import sys; sys.path[:0] = [%r, %r]; import numpy as np; "
+            "from test_gpu_host_io import run, params; ps = params(); "
             "a = run(ps, 4_200_000, 'bf16', False, False); b = run(ps, 4_200_000, 'bf16', True, True); "
-            "print('EQUAL' if np.array_equal(a, b) else 'DIFF')" % ROOT)
+            "print('EQUAL' if np.array_equal(a, b) else 'DIFF')" % (ROOT, os.path.join(ROOT, "tests")))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=ROOT, timeout=600)
     assert "EQUAL" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
