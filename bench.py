@@ -33,6 +33,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Muon optimizer step ms (Qwen3-8B shapes) at 1/2/4/8 B200; max/mean rank load"
+METRIC_SHAMPOO = ("Shampoo optimizer step ms (Qwen3-8B shapes, builder-defined blocked Shampoo; "
+                  "not the BASELINE metric); max/mean rank load")
 CONFIG = os.path.join(ROOT, "configs", "qwen3-8b-like.cfg")
 
 
@@ -54,6 +56,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workspace-gb", type=float, default=0.0)
+    ap.add_argument("--optimizer", default="muon", choices=["muon", "shampoo"],
+                    help="muon = the headline metric; shampoo = builder-defined blocked Shampoo")
+    ap.add_argument("--shampoo-block", type=int, default=1024)
+    ap.add_argument("--precond-every", type=int, default=10)
     ap.add_argument("--collectives", default="auto", choices=["auto", "nccl", "nvls"],
                     help="DP RS/AG path: NCCL kernels or NVLS multicast fused into the update")
     ap.add_argument("--tp", type=int, default=1,
@@ -234,7 +240,7 @@ def run_ours(a, dist: Dist):
 
     from paper_2602_06079_b200 import planner as P
     from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,
-                                              nccl_unique_id)
+                                              ShampooConfig, nccl_unique_id)
 
     N = dist.world
     T = a.tp
@@ -262,7 +268,9 @@ def run_ours(a, dist: Dist):
                           comm="nccl", nccl_uid=uid, grad_dtype=a.grad_dtype,
                           workspace_bytes=int(a.workspace_gb * (1 << 30)), tp_rank=t, tp_size=T,
                           tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None,
-                          collectives=a.collectives)
+                          collectives=a.collectives, optimizer=a.optimizer,
+                          shampoo=(ShampooConfig(block=a.shampoo_block, precond_every=a.precond_every)
+                                   if a.optimizer == "shampoo" else None))
     info = eng.info()
     coll_path = COLLECTIVE_NAMES[info["collectives"]]
     eng.fill_synthetic(42, "weights")
@@ -315,6 +323,36 @@ def run_ours(a, dist: Dist):
             print("launch", *rec, file=sys.stderr)
     last = eng.timing()
     clock = clocks.stop(torch.cuda.device_count()) if clocks else None
+    refresh_ms, refresh_modes = None, None
+    if a.optimizer == "shampoo":
+        # the timed steps avoid the root refresh (step index % precond_every != 0
+        # when warmup + steps < precond_every); time one refresh step on its own
+        done = a.warmup + a.steps
+        for _ in range((-done) % a.precond_every):
+            eng.step(ocfg)
+        eng.sync()
+        dist.barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.profile_gemm(True)
+        r0.record(stream)
+        eng.step(ocfg)
+        r1.record(stream)
+        r1.synchronize()
+        eng.sync()
+        refresh_ms = r0.elapsed_time(r1)
+        refresh_modes = {}
+        for mode, lms, fl, ex, what in eng.gemm_profile_launches():
+            d = refresh_modes.setdefault(mode, {"launches": 0, "ms": 0.0, "flops": 0.0})
+            d["launches"] += 1
+            d["ms"] += lms
+            d["flops"] += fl
+        for mode, d in refresh_modes.items():
+            if mode in GEMM_MODES and d["ms"] > 0:
+                d["tflops_alg"] = round(d["flops"] / (d["ms"] * 1e-3) / 1e12, 1)
+            d["ms"] = round(d["ms"], 2)
+            d.pop("flops")
+        eng.gemm_profile(reset=True)
+        eng.profile_gemm(False)
 
     # e2e through the C ABI with host buffers (pinned)
     e2e = None
@@ -343,7 +381,11 @@ def run_ours(a, dist: Dist):
         del hg, hr
 
     rec = {"ms": ms, "prof": prof, "by_mode": by_mode, "last": last, "info": info, "e2e": e2e,
-           "owned_numel": info["owned_numel"], "ns_flops": info["ns_flops_per_iter"] * 5}
+           "owned_numel": info["owned_numel"],
+           "ns_flops": (info["ns_flops_per_iter"] * 5 if a.optimizer == "muon"
+                        else float(last["gemm_flops"])),
+           "refresh_ms": refresh_ms,
+           "refresh_modes": refresh_modes if a.optimizer == "shampoo" else None}
     allrec = dist.gather(rec)
     eng.close()
     if dist.rank != 0:
@@ -364,7 +406,7 @@ def run_ours(a, dist: Dist):
     achieved_exec = p0["exec_flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     out = {
-        "metric": METRIC,
+        "metric": METRIC if a.optimizer == "muon" else METRIC_SHAMPOO,
         "value": round(ms_max, 3),
         "unit": "ms",
         "n_gpus": N,
@@ -427,7 +469,17 @@ def run_ours(a, dist: Dist):
         out["e2e"] = {"value": round(e, 3), "unit": "ms",
                       "h2d_bytes_per_step": allrec[0]["e2e"]["h2d"],
                       "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"]}
-    if N == 1 and not a.no_cpu_baseline:
+    if a.optimizer == "shampoo":
+        rms = max(r["refresh_ms"] for r in allrec)
+        out["shampoo"] = {"block": a.shampoo_block, "precond_every": a.precond_every,
+                          "newton_iters": 16, "refresh_step_ms": round(rms, 3),
+                          "refresh_by_mode_rank0": allrec[0]["refresh_modes"],
+                          "amortized_step_ms": round(ms_max + (rms - ms_max) / a.precond_every, 3),
+                          "note": "value = a step without the inverse-root refresh; the refresh "
+                                  "step (coupled Newton, bf16x3 split GEMMs) is timed separately"}
+        out["config"]["workload"] = out["config"]["workload"].replace("Muon step", "Shampoo step")
+        out["roofline"]["kernel"] = "ns_gemm_kernel (STAT / UPDATE / GRAM GEMMs of the step)"
+    if N == 1 and not a.no_cpu_baseline and a.optimizer == "muon":
         cb = cpu_reference_step(params, plan, owners, 1)
         out["cpu_baseline"] = {"value": round(cb["critical_path_ms"], 1), "unit": "ms",
                                "cores": cb["cores"], "kind": "port", "sample": cb["sample"],
@@ -468,7 +520,7 @@ def run_reference(a, dist: Dist):
     }
 
 
-GEMM_MODES = ("gram", "poly", "update", "final")
+GEMM_MODES = ("gram", "poly", "update", "final", "stat", "split")
 
 
 def main():

@@ -177,10 +177,11 @@ typedef struct osh_gemm_problem {
  *   GRAM   out = s*acc               POLY  out = alpha*aux + beta*acc
  *   UPDATE out = s*(alpha*aux + acc) FINAL W -= lr*s*(alpha*aux + acc) (+ replica)
  *   STAT   out(fp32) = alpha*out + s*acc   (Shampoo statistics, read-modify-write)
- *   SPLIT  v = s*acc stored as bf16 hi = bf16(v), lo = bf16(v - hi) in five
- *          segments [hi | lo | hi | hi | lo] of out_seg columns: columns
- *          [0, 3*K) are the A view and [2*K, 5*K) the B view of a bf16x3
- *          product hi*hi + lo*hi + hi*lo (fp32-accurate Newton iterations).
+ *   SPLIT  v = s*acc stored as bf16 hi = bf16(v), lo = bf16(v - hi) in four
+ *          segments [hi | lo | hi | hi] of out_seg columns: columns
+ *          [0, 3*seg) = (hi, lo, hi) are the A view and [seg, 4*seg) =
+ *          (lo, hi, hi) the B view of a bf16x3 product hi*lo + lo*hi + hi*hi
+ *          (fp32-accurate Newton iterations).
  * alpha == 0 skips reading aux (aux may then be null). */
 enum { OSH_EPI_GRAM = 0, OSH_EPI_POLY = 1, OSH_EPI_UPDATE = 2, OSH_EPI_FINAL = 3,
        OSH_EPI_STAT = 4, OSH_EPI_SPLIT = 5 };

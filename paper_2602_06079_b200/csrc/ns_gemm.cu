@@ -134,27 +134,36 @@ __device__ __forceinline__ void store_row32(__nv_bfloat16* dst, int col0, int n,
 }
 
 // fp32 read-modify-write of 32 consecutive elements: dst = alpha * dst + v.
+// All loads are issued before any store (no load-after-store chain).
 __device__ __forceinline__ void rmw_row32(float* dst, int col0, int n, float alpha,
                                           const float (&v)[32]) {
   if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     float4* d4 = reinterpret_cast<float4*>(dst);
+    float4 o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = d4[q];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float4 o = d4[q];
-      o.x = alpha * o.x + v[q * 4 + 0];
-      o.y = alpha * o.y + v[q * 4 + 1];
-      o.z = alpha * o.z + v[q * 4 + 2];
-      o.w = alpha * o.w + v[q * 4 + 3];
-      d4[q] = o;
+      o[q].x = alpha * o[q].x + v[q * 4 + 0];
+      o[q].y = alpha * o[q].y + v[q * 4 + 1];
+      o[q].z = alpha * o[q].z + v[q * 4 + 2];
+      o[q].w = alpha * o[q].w + v[q * 4 + 3];
+      d4[q] = o[q];
     }
   } else {
+    float o[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = col0 + j < n ? dst[j] : 0.f;
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (col0 + j < n) dst[j] = alpha * dst[j] + v[j];
+      if (col0 + j < n) dst[j] = alpha * o[j] + v[j];
   }
 }
 
-// Symmetric fp32 read-modify-write (same single-writer rule as below).
+// Symmetric fp32 read-modify-write (same single-writer rule as below). The
+// mirrored part reads its 32 old values first: for a fixed j the warp's lanes
+// touch 32 consecutive floats of row col0 + j (coalesced), and no store sits
+// between the loads.
 __device__ __forceinline__ void rmw_row32_sym(float* out, long long ld, int row, int col0, int n,
                                               float alpha, const float (&v)[32]) {
   if (col0 >= row) {
@@ -168,13 +177,16 @@ __device__ __forceinline__ void rmw_row32_sym(float* out, long long ld, int row,
       }
   }
   if (col0 + 31 > row) {
+    float o[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int c = col0 + j;
-      if (c > row && c < n) {
-        float* p = out + static_cast<long long>(c) * ld + row;
-        *p = alpha * *p + v[j];
-      }
+      o[j] = (c > row && c < n) ? out[static_cast<long long>(c) * ld + row] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int c = col0 + j;
+      if (c > row && c < n) out[static_cast<long long>(c) * ld + row] = alpha * o[j] + v[j];
     }
   }
 }
@@ -399,14 +411,12 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             store_row32_sym(o + sg, pr.out_ld, row, col0, pr.N, lo);
             store_row32_sym(o + 2 * sg, pr.out_ld, row, col0, pr.N, v);
             store_row32_sym(o + 3 * sg, pr.out_ld, row, col0, pr.N, v);
-            store_row32_sym(o + 4 * sg, pr.out_ld, row, col0, pr.N, lo);
           } else {
             __nv_bfloat16* d = o + row * pr.out_ld + col0;
             store_row32(d, col0, pr.N, v);
             store_row32(d + sg, col0, pr.N, lo);
             store_row32(d + 2 * sg, col0, pr.N, v);
             store_row32(d + 3 * sg, col0, pr.N, v);
-            store_row32(d + 4 * sg, col0, pr.N, lo);
           }
         } else {  // kEpiFinal: every lane takes part (warp-level transpose below)
           float upd[32];

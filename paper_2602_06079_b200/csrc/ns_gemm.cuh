@@ -36,9 +36,10 @@ enum NsEpilogue : int {
   kEpiUpdate = 2,  // out = s * (alpha * aux + acc)                  (bf16)
   kEpiFinal = 3,   // W -= lr * s * (alpha * aux + acc)              (fp32 master + replica)
   kEpiStat = 4,    // out32 = alpha * out32 + s * acc                (fp32 read-modify-write)
-  kEpiSplit = 5,   // v = s * acc as bf16 hi/lo pairs in 5 segments of out_seg columns:
-                   //   [hi | lo | hi | hi | lo]; columns [0,3n) are the A-operand view and
-                   //   [2n,5n) the B-operand view of a bf16x3 product (hi*hi + lo*hi + hi*lo)
+  kEpiSplit = 5,   // v = s * acc as bf16 hi/lo pairs in 4 segments of out_seg columns:
+                   //   [hi | lo | hi | hi]; columns [0,3n) = (hi, lo, hi) are the A-operand view
+                   //   and [n,4n) = (lo, hi, hi) the B-operand view of a bf16x3 product
+                   //   (hi*lo + lo*hi + hi*hi)
 };
 
 // Where the last Newton-Schulz step of one matrix lands: the fp32 master

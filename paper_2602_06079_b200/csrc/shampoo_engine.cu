@@ -56,8 +56,8 @@ int seg_of(int n) { return static_cast<int>(rup(static_cast<size_t>(n), 8)); }
 size_t block_ws(int p, int q) {
   const size_t ldp = rup(p, 64), ldq = rup(q, 64);
   const size_t sp = seg_of(p), sq = seg_of(q);
-  return rup(2 * p * ldq, 256) * 3 + rup(2 * q * ldp, 256) + 7 * rup(2 * p * 5 * sp, 256) +
-         7 * rup(2 * q * 5 * sq, 256);
+  return rup(2 * p * ldq, 256) * 3 + rup(2 * q * ldp, 256) + 7 * rup(2 * p * 4 * sp, 256) +
+         7 * rup(2 * q * 4 * sq, 256);
 }
 
 }  // namespace
@@ -213,7 +213,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
       k.gbt = off; off += gtp * k.nb;
       k.u1 = off; off += gq * k.nb;
       k.u = off; off += gq * k.nb;
-      const size_t s5p = rup(2ull * k.p * 5 * seg_of(k.p), 256), s5q = rup(2ull * k.q * 5 * seg_of(k.q), 256);
+      const size_t s5p = rup(2ull * k.p * 4 * seg_of(k.p), 256), s5q = rup(2ull * k.q * 4 * seg_of(k.q), 256);
       for (size_t* z : {&k.xl[0], &k.xl[1], &k.ml[0], &k.ml[1], &k.tl, &k.t2l, &k.t4l}) {
         *z = off;
         off += s5p * k.nb;
@@ -304,7 +304,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
         const int n = side == 0 ? k.p : k.q;
         const int ldn = side == 0 ? k.ldp : k.ldq;
         const int sg = seg_of(n);
-        const size_t s5 = rup(2ull * n * 5 * sg, 256);
+        const size_t s5 = rup(2ull * n * 4 * sg, 256);
         const size_t Sb = rup(4ull * n * ldn, 256), Pb = rup(2ull * n * ldn, 256);
         for (int i = 0; i < k.nb; ++i) {
           const int stat = k.stat0 + side * k.nb + i;
@@ -327,7 +327,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
           r.lds = ldn;
           r.a5 = static_cast<__nv_bfloat16*>(off_ptr((side == 0 ? k.ml[0] : k.mr[0]) + s5 * i));
           r.x5 = static_cast<__nv_bfloat16*>(off_ptr((side == 0 ? k.xl[0] : k.xr[0]) + s5 * i));
-          r.ld5 = 5ll * sg;
+          r.ld5 = 4ll * sg;
           r.n = n;
           r.sumsq = reinterpret_cast<const double*>(static_cast<uintptr_t>(stat));  // patched
           r.tile_start = rt;
@@ -345,8 +345,8 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
             nt.src5 = static_cast<const __nv_bfloat16*>(
                 off_ptr((side == 0 ? k.ml[par] : k.mr[par]) + s5 * i));
             nt.dst = static_cast<__nv_bfloat16*>(off_ptr((side == 0 ? k.tl : k.tr) + s5 * i));
-            nt.ld5 = 5ll * sg;
-            nt.ldd = 5ll * sg;
+            nt.ld5 = 4ll * sg;
+            nt.ldd = 4ll * sg;
             nt.n = n;
             nt.tile_start = rt;
             nt.tiles_c = (n + kTile - 1) / kTile;
@@ -357,7 +357,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
           et.src5 = static_cast<const __nv_bfloat16*>(
               off_ptr((side == 0 ? k.xl[fin] : k.xr[fin]) + s5 * i));
           et.dst = static_cast<__nv_bfloat16*>(off_ptr((side == 0 ? k.PL : k.PR) + Pb * i));
-          et.ld5 = 5ll * sg;
+          et.ld5 = 4ll * sg;
           et.ldd = ldn;
           et.n = n;
           et.tile_start = rt;
@@ -628,14 +628,14 @@ osh_status ShampooEngine::run_wave(int wi, const osh_muon_cfg& mcfg, cudaStream_
         for (const Cls& k : w.cls) {
           auto split_ref = [&](size_t base, int n, bool bview) {
             const int sg = seg_of(n);
-            const long long bs = static_cast<long long>(rup(2ull * n * 5 * sg, 256) / 2);
-            return mref(static_cast<__nv_bfloat16*>(at(base)) + (bview ? 2 * sg : 0), k.nb, n,
-                        3 * sg, 5ll * sg, bs);
+            const long long bs = static_cast<long long>(rup(2ull * n * 4 * sg, 256) / 2);
+            return mref(static_cast<__nv_bfloat16*>(at(base)) + (bview ? sg : 0), k.nb, n,
+                        3 * sg, 4ll * sg, bs);
           };
           auto out_ref = [&](size_t base, int n) {
             const int sg = seg_of(n);
-            const long long bs = static_cast<long long>(rup(2ull * n * 5 * sg, 256) / 2);
-            return mref(at(base), k.nb, n, n, 5ll * sg, bs);
+            const long long bs = static_cast<long long>(rup(2ull * n * 4 * sg, 256) / 2);
+            return mref(at(base), k.nb, n, n, 4ll * sg, bs);
           };
           auto prob = [&](size_t a, size_t b, size_t o, int n) {
             NsProblemDesc d{};

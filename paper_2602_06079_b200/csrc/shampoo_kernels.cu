@@ -116,14 +116,13 @@ __global__ void __launch_bounds__(256) sh_sumsq_kernel(const ShMatTask<E>* tasks
 }
 
 // ---------------------------------------------------------------- roots
-__device__ __forceinline__ void store_split5(__nv_bfloat16* row_base, long long seg, int c, float v) {
+__device__ __forceinline__ void store_split4(__nv_bfloat16* row_base, long long seg, int c, float v) {
   const __nv_bfloat16 hi = __float2bfloat16_rn(v);
   const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
   row_base[c] = hi;
   row_base[seg + c] = lo;
   row_base[2 * seg + c] = hi;
   row_base[3 * seg + c] = hi;
-  row_base[4 * seg + c] = lo;
 }
 
 __global__ void __launch_bounds__(256) sh_root_init_kernel(const ShRootTask* tasks, int n,
@@ -147,16 +146,16 @@ __global__ void __launch_bounds__(256) sh_root_init_kernel(const ShRootTask* tas
       if (c >= T.n) continue;
       const float d = r == c ? 1.f : 0.f;
       const float a = zero ? d : T.s[static_cast<size_t>(r) * T.lds + c] * inv_c + eps * d;
-      store_split5(arow, T.ld5 / 5, c, a);  // segment width = n rounded up to 8
-      store_split5(xrow, T.ld5 / 5, c, d);
+      store_split4(arow, T.ld5 / 4, c, a);  // segment width = n rounded up to 8
+      store_split4(xrow, T.ld5 / 4, c, d);
     }
   }
-  const int seg = static_cast<int>(T.ld5 / 5);
+  const int seg = static_cast<int>(T.ld5 / 4);
   if (seg > T.n && c0 + kTile >= T.n) {  // last column tile: zero the pad columns
     const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
-    for (int i = threadIdx.x; i < kTile * 5 * (seg - T.n); i += 256) {
-      const int r = r0 + i / (5 * (seg - T.n));
-      const int k = i % (5 * (seg - T.n));
+    for (int i = threadIdx.x; i < kTile * 4 * (seg - T.n); i += 256) {
+      const int r = r0 + i / (4 * (seg - T.n));
+      const int k = i % (4 * (seg - T.n));
       if (r >= T.n) continue;
       const size_t off = static_cast<size_t>(r) * T.ld5 + (k / (seg - T.n)) * seg + T.n + k % (seg - T.n);
       T.a5[off] = z;
@@ -188,9 +187,9 @@ __global__ void __launch_bounds__(256) sh_newton_t_kernel(const ShNewtonTask* ta
     for (int j = 0; j < kTile / 32; ++j) {
       const int c = c0 + tx + 32 * j;
       if (c >= T.n) continue;
-      const long long seg = T.ld5 / 5;
+      const long long seg = T.ld5 / 4;
       const float m = __bfloat162float(mrow[c]) + __bfloat162float(mrow[seg + c]);
-      store_split5(trow, seg, c, ((r == c ? 5.f : 0.f) - m) * 0.25f);
+      store_split4(trow, seg, c, ((r == c ? 5.f : 0.f) - m) * 0.25f);
     }
   }
 }

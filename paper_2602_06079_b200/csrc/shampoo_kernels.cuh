@@ -10,7 +10,7 @@
 //                  tile sums of g^2
 //   sh_sumsq       tile sums of x^2 of an fp32 or bf16 matrix
 //   sh_root_init   A = S/||S|| + eps I and X = I in the split-bf16 layout
-//                  [hi | lo | hi | hi | lo] (identity when S = 0)
+//                  [hi | lo | hi | hi] (identity when S = 0)
 //   sh_root_scale  c^(-1/4) per statistics matrix (1 when S = 0)
 //   sh_newton_t    T = (5 I - M) / 4 in the split layout
 //   sh_extract     hi segment of the converged root -> compact bf16 P
@@ -50,7 +50,7 @@ struct ShMatTask {        // a plain n_rows x n_cols matrix (sumsq / extract / r
   double* partial;
 };
 
-struct ShRootTask {       // one statistics matrix of size n (split layout ld5 = 5n)
+struct ShRootTask {       // one statistics matrix of size n (split layout ld5 = 4 * seg)
   const float* s;         // fp32 statistics [n][lds]
   long long lds;
   __nv_bfloat16* a5;      // M0 = A (split)

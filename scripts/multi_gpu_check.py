@@ -1,6 +1,6 @@
 """N-GPU correctness of the real NCCL path (RS-v -> owner Muon -> AG-v).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps] [auto|nccl|nvls]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps] [auto|nccl|nvls] [muon|shampoo]
 
 The optional second argument selects the DP collective path (engine.py
 ``collectives``); the JSON line reports the path the runtime actually took.
@@ -26,15 +26,18 @@ sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
 from paper_2602_06079_b200 import planner as P  # noqa: E402
+from oracle import shampoo_oracle as S  # noqa: E402
 from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,  # noqa: E402
-                                          nccl_unique_id)
+                                          ShampooConfig, nccl_unique_id)
 
 SEED = 42
+SCFG = ShampooConfig(block=512, precond_every=2)
 
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     coll = sys.argv[2] if len(sys.argv) > 2 else "auto"
+    opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     td.init_process_group("gloo")
@@ -48,7 +51,8 @@ def main():
     uid = [nccl_unique_id() if rank == 0 else None]
     td.broadcast_object_list(uid, src=0)
     eng = DistributedMuon(params, cap, plan, rank=rank, device=local, comm="nccl", nccl_uid=uid[0],
-                          grad_dtype="f32", collectives=coll)
+                          grad_dtype="f32", collectives=coll, optimizer=opt,
+                          shampoo=SCFG if opt == "shampoo" else None)
     path = COLLECTIVE_NAMES[eng.info()["collectives"]]
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
@@ -77,10 +81,18 @@ def main():
     w = {p.id: O.init_weight(p.shape, p.id, SEED) for p in params}
     mom = {p.id: np.zeros_like(w[p.id]) for p in params}
     rnorms = np.zeros((steps, len(params)))
+    if opt == "shampoo":
+        scfg = S.ShampooConfig(lr=cfg.lr, beta1=cfg.beta, beta2=SCFG.beta2, eps=SCFG.eps,
+                               block=SCFG.block, precond_every=SCFG.precond_every,
+                               newton_iters=SCFG.newton_iters)
+        st = {p.id: S.ShampooTensorState(w[p.id].shape, scfg, S.is_preconditioned(p)) for p in params}
     for s in range(steps):
         for p in params:
             g = O.reduced_gradient(p.shape, p.id, SEED, s, world)
-            rnorms[s, p.id] = O.muon_apply(p.is_matrix, cfg, w[p.id], mom[p.id], g)
+            if opt == "shampoo":
+                rnorms[s, p.id] = S.shampoo_apply(st[p.id], scfg, w[p.id], g.reshape(w[p.id].shape), s)
+            else:
+                rnorms[s, p.id] = O.muon_apply(p.is_matrix, cfg, w[p.id], mom[p.id], g)
     report, ok = {}, True
     for p in params:
         got, ref = weights[p.id].reshape(-1), w[p.id].reshape(-1)
@@ -88,6 +100,8 @@ def main():
         e_n = float(np.max(np.abs(gnorms[:, p.id] - rnorms[:, p.id]) / rnorms[:, p.id]))
         tol_w = 2.5e-3 if p.is_matrix else 1e-5
         tol_n = (3e-2 if min(p.shape) >= 64 else 1e-1) if p.is_matrix else 1e-5
+        if opt == "shampoo" and p.is_matrix:
+            tol_n = 5e-2
         rep_ok = all(np.array_equal(g[2][p.id].reshape(-1),
                                     torch.tensor(weights[p.id].reshape(-1)).float().bfloat16().float().numpy())
                      for g in gathered)
@@ -95,7 +109,8 @@ def main():
         ok &= good
         report[p.name] = {"owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
-    print(json.dumps({"world": world, "steps": steps, "collectives": path, "ok": ok, "params": report}))
+    print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt, "ok": ok,
+                      "params": report}))
     return 0 if ok else 1
 
 

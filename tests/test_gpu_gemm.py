@@ -248,11 +248,11 @@ def test_stat_fp32_accumulate(batch, m, n, sym):
         assert torch.equal(out, out.transpose(1, 2))
 
 
-def split5(x):
-    """[hi | lo | hi | hi | lo] bf16 layout of an fp32 [b][n][n] matrix."""
+def split4(x):
+    """[hi | lo | hi | hi] bf16 layout of an fp32 [b][n][n] matrix."""
     hi = x.bfloat16()
     lo = (x - hi.float()).bfloat16()
-    return torch.cat([hi, lo, hi, hi, lo], dim=2).contiguous()
+    return torch.cat([hi, lo, hi, hi], dim=2).contiguous()
 
 
 @pytest.mark.parametrize("sym", [1, 0])
@@ -264,15 +264,14 @@ def test_split_bf16x3_product(batch, n, sym):
     a = torch.randn(batch, n, n, device="cuda", generator=gen, dtype=torch.float64) / n ** 0.5
     a = (a + a.transpose(1, 2)) / 2
     b = a @ a + 0.1 * a  # commutes with a: a @ b is symmetric
-    sa, sb = split5(a.float()), split5(b.float())
-    out = torch.zeros(batch, n, 5 * n, device="cuda", dtype=torch.bfloat16)
+    sa, sb = split4(a.float()), split4(b.float())
+    out = torch.zeros(batch, n, 4 * n, device="cuda", dtype=torch.bfloat16)
     p = _lib.GemmProblem()
-    p.a = mref(sa, cols=3 * n)                       # A view: columns [0, 3n)
-    p.b = mref(sa[:, :, 2 * n:], cols=3 * n)          # (unused below, shape check)
-    bview = sb[:, :, 2 * n:]
+    p.a = mref(sa, cols=3 * n)                       # A view: columns [0, 3n) = (hi, lo, hi)
+    bview = sb[:, :, n:]
     p.b = _lib.MatrixRef()
     p.b.ptr, p.b.batch, p.b.rows, p.b.cols = bview.data_ptr(), batch, n, 3 * n
-    p.b.ld, p.b.bstride = sb.stride(1), sb.stride(0)  # B view: columns [2n, 5n)
+    p.b.ld, p.b.bstride = sb.stride(1), sb.stride(0)  # B view: columns [n, 4n) = (lo, hi, hi)
     p.out = mref(out, cols=n)
     p.out_seg = n
     p.symmetric = sym
@@ -280,10 +279,9 @@ def test_split_bf16x3_product(batch, n, sym):
     ref = a @ b
     got = out[:, :, :n].double() + out[:, :, n:2 * n].double()
     err = ((got - ref).abs().max() / ref.abs().max()).item()
-    assert err < 2e-5, err  # bf16 alone would be ~4e-3
+    assert err < 5e-5, err  # bf16 alone would be ~4e-3
     assert torch.equal(out[:, :, :n], out[:, :, 2 * n:3 * n])
     assert torch.equal(out[:, :, :n], out[:, :, 3 * n:4 * n])
-    assert torch.equal(out[:, :, n:2 * n], out[:, :, 4 * n:])
 
 
 def test_poly_alpha_zero_skips_aux():

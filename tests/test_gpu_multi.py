@@ -60,6 +60,11 @@ def test_dp2_tp2_micro_groups_match_oracle():
     _run(4, "multi_gpu_check_tp.py", 2, 2, 3)
 
 
+def test_dp2_shampoo_matches_spec():
+    res = _run(2, "multi_gpu_check.py", 3, "auto", "shampoo")
+    assert res["optimizer"] == "shampoo"
+
+
 def test_dp4_nccl_matches_oracle():
     _run(4, "multi_gpu_check.py", 3, "nccl")
 
