@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <string>
 
@@ -76,6 +78,8 @@ void MuonEngine::release() {
   d_mtasks_ = nullptr;
   d_atasks_ = nullptr;
   d_vtasks_ = nullptr;
+  for (int* p : sched_mem_) cudaFree(p);
+  sched_mem_.clear();
   chunks_.clear();
   waves_.clear();
 }
@@ -276,6 +280,33 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
   OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
   OSH_CUDA_TRY(upload(&d_slot_tensor_, slot_tensor));
+  // cost-balanced (LPT) tile schedules of the three GEMMs of every wave
+  const char* lpt = std::getenv("OSH_GEMM_LPT");
+  lpt_ = !(lpt != nullptr && std::strcmp(lpt, "0") == 0);
+  sched_symmetric_ = symmetric_;
+  for (Wave& w : waves_) {
+    if (w.n_tasks == 0 || !lpt_) continue;
+    NsProblemDesc pd[3][kMaxProblems];
+    problems(w, 0, pd[0], pd[1], pd[2]);
+    const int modes[3] = {kEpiGram, kEpiPoly, kEpiUpdate};
+    for (int m = 0; m < 3; ++m) {
+      std::vector<int> tl, off;
+      int total = 0;
+      const int units = ns_gemm_schedule(modes[m], pd[m], static_cast<int>(w.chunks.size()), &tl, &off, &total);
+      if (units == 0) continue;
+      int* d_tl = nullptr;
+      int* d_off = nullptr;
+      OSH_CUDA_TRY(upload(&d_tl, tl));
+      OSH_CUDA_TRY(upload(&d_off, off));
+      sched_mem_.push_back(d_tl);
+      sched_mem_.push_back(d_off);
+      NsSchedule& sc = w.sched[modes[m]];
+      sc.tiles = d_tl;
+      sc.off = d_off;
+      sc.units = units;
+      sc.total_tiles = total;
+    }
+  }
   OSH_CUDA_TRY(cudaDeviceSynchronize());
   return OSH_OK;
 }
@@ -320,32 +351,39 @@ osh_status MuonEngine::run_pre(int wi, const osh_muon_cfg& cfg, cudaStream_t s) 
   return OSH_OK;
 }
 
+void MuonEngine::problems(const Wave& w, int it, NsProblemDesc* gram, NsProblemDesc* poly,
+                          NsProblemDesc* upd) const {
+  const bool first = it == 0;
+  const int np = static_cast<int>(w.chunks.size());
+  for (int q = 0; q < np; ++q) {
+    const Chunk& c = chunks_[w.chunks[q]];
+    const Shape sh = shape_of(c.m, c.n);
+    uint8_t* xin = d_ws_ + ((it & 1) ? c.x1 : c.x0);
+    uint8_t* xout = d_ws_ + ((it & 1) ? c.x0 : c.x1);
+    const long long xbs = static_cast<long long>(sh.xb / 2), abs = static_cast<long long>(sh.ab / 2);
+    const NsMatrixRef X = ref(xin, c.batch, c.m, c.n, c.ldn, xbs);
+    const NsMatrixRef Xo = ref(xout, c.batch, c.m, c.n, c.ldn, xbs);
+    const NsMatrixRef Am = ref(d_ws_ + c.a, c.batch, c.m, c.m, c.ldm, abs);
+    const NsMatrixRef Bm = ref(d_ws_ + c.b, c.batch, c.m, c.m, c.ldm, abs);
+    const int sym = symmetric_ ? 1 : 0;
+    gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{},
+                            first ? d_scale_gram_ + c.slot0 : nullptr, nullptr, sym};
+    poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, sym};
+    upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
+                           nullptr, 0};
+  }
+}
+
 osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
   const Wave& w = waves_[wi];
   if (w.n_tasks == 0) return OSH_OK;
   const int np = static_cast<int>(w.chunks.size());
   for (int it = 0; it < cfg.ns_steps; ++it) {
-    const bool first = it == 0;
     NsProblemDesc gram[kMaxProblems], poly[kMaxProblems], upd[kMaxProblems];
-    for (int q = 0; q < np; ++q) {
-      const Chunk& c = chunks_[w.chunks[q]];
-      const Shape sh = shape_of(c.m, c.n);
-      uint8_t* xin = d_ws_ + ((it & 1) ? c.x1 : c.x0);
-      uint8_t* xout = d_ws_ + ((it & 1) ? c.x0 : c.x1);
-      const long long xbs = static_cast<long long>(sh.xb / 2), abs = static_cast<long long>(sh.ab / 2);
-      const NsMatrixRef X = ref(xin, c.batch, c.m, c.n, c.ldn, xbs);
-      const NsMatrixRef Xo = ref(xout, c.batch, c.m, c.n, c.ldn, xbs);
-      const NsMatrixRef Am = ref(d_ws_ + c.a, c.batch, c.m, c.m, c.ldm, abs);
-      const NsMatrixRef Bm = ref(d_ws_ + c.b, c.batch, c.m, c.m, c.ldm, abs);
-      const int sym = symmetric_ ? 1 : 0;
-      gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{},
-                              first ? d_scale_gram_ + c.slot0 : nullptr, nullptr, sym};
-      poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, sym};
-      upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
-                             nullptr, 0};
-    }
+    problems(w, it, gram, poly, upd);
     const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b) {
-      return timed_gemm(mode, pd, np, a, b, s);
+      const NsSchedule* sc = lpt_ && sched_symmetric_ == symmetric_ ? &w.sched[mode] : nullptr;
+      return timed_gemm(mode, pd, np, a, b, s, sc);
     };
     cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f);
     if (e == cudaSuccess)

@@ -79,9 +79,12 @@ class MuonEngine : public OptimizerEngine {
     int slot0 = 0, n_slots = 0;
     int vec0 = 0, n_vec = 0;
     double elems_matrix = 0.0, elems_vector = 0.0;  // owned elements (profile bytes)
+    NsSchedule sched[4];  // per GEMM mode (kEpiGram / kEpiPoly / kEpiUpdate)
   };
   void release();
   const char* elementwise_name(int mode) const override;
+  void problems(const Wave& w, int it, NsProblemDesc* gram, NsProblemDesc* poly,
+                NsProblemDesc* upd) const;
 
   int n_tensors_ = 0;
   int grad_dtype_ = kGradF32;
@@ -102,6 +105,9 @@ class MuonEngine : public OptimizerEngine {
   MomentumVectorTask* d_vtasks_ = nullptr;
   bool symmetric_ = true;
   bool double_buffer_ = false;
+  bool lpt_ = true;               // cost-balanced tile schedules (OSH_GEMM_LPT=0: striding)
+  bool sched_symmetric_ = true;   // symmetric_ when the schedules were built
+  std::vector<int*> sched_mem_;
 };
 
 }  // namespace osh

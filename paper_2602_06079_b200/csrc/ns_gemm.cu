@@ -233,6 +233,12 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = leader of the pair
   const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;  // tiles are per cluster
+  // tile sequence of this unit: the host's cost-balanced schedule when one is
+  // attached for this grid, else static striding (t = unit, unit + n_units, ...)
+  const bool sched = P.sched != nullptr && P.sched_units == n_units;
+  const int it_begin = sched ? P.sched_off[unit] : unit;
+  const int it_end = sched ? P.sched_off[unit + 1] : P.total_tiles;
+  const int it_step = sched ? 1 : n_units;
 
   if (warp == 0 && lane == 0) {
     for (int p = 0; p < P.num_problems; ++p) {
@@ -267,7 +273,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         if constexpr (CG == 2) tma_load_3d_cg2(dst, map, &full_bar[stage], c0, c1, c2);
         else tma_load_3d(dst, map, &full_bar[stage], c0, c1, c2);
       };
-      for (int t = unit; t < P.total_tiles; t += n_units) {
+      for (int it = it_begin; it < it_end; it += it_step) {
+        const int t = sched ? __ldg(P.sched + it) : it;
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
         const int nkb = (pr.K + kNsBK - 1) / kNsBK;
@@ -299,7 +306,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const uint32_t idesc_k = idesc_bf16_f32(C::kTileM, kNsBN, false, false);
       const uint32_t idesc_mn = idesc_bf16_f32(C::kTileM, kNsBN, false, true);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int t = unit; t < P.total_tiles; t += n_units) {
+      for (int it = it_begin; it < it_end; it += it_step) {
+        const int t = sched ? __ldg(P.sched + it) : it;
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
         const int nkb = (pr.K + kNsBK - 1) / kNsBK;
@@ -340,7 +348,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     uint32_t acc = 0, acc_phase = 0;
-    for (int t = unit; t < P.total_tiles; t += n_units) {
+    for (int it = it_begin; it < it_end; it += it_step) {
+        const int t = sched ? __ldg(P.sched + it) : it;
       const TileCoord c = decode_tile(P, t);
       const NsGemmProblem& pr = P.prob[c.p];
       const int row_base = c.tm * C::kTileM + rank * C::kRowsA;
@@ -631,8 +640,48 @@ double ns_gemm_flops(const NsProblemDesc* probs, int num_problems) {
   return f;
 }
 
+int ns_gemm_schedule(int mode, const NsProblemDesc* probs, int num_problems,
+                     std::vector<int>* tiles_out, std::vector<int>* off_out, int* total_out) {
+  if (num_problems < 1 || num_problems > kMaxProblems) return 0;
+  const int cg = cta_group();
+  const int tile_m = 128 * cg;
+  std::vector<std::pair<long long, int>> cost;  // (cost, linear tile)
+  int t = 0;
+  for (int i = 0; i < num_problems; ++i) {
+    const NsProblemDesc& d = probs[i];
+    const int M = d.a.rows, K = d.a.cols, N = d.b_mn_major ? d.b.cols : d.b.rows;
+    const bool sym = d.symmetric && M == N &&
+                     (mode == kEpiGram || mode == kEpiPoly || mode == kEpiStat || mode == kEpiSplit);
+    const int tm = (M + tile_m - 1) / tile_m, tn = (N + kNsBN - 1) / kNsBN;
+    const int per = sym ? sym_tiles(tm, tn, tile_m) : tm * tn;
+    const long long c = (K + kNsBK - 1) / kNsBK + 2;  // K blocks + epilogue
+    for (int k = 0; k < d.a.batch * per; ++k) cost.emplace_back(c, t++);
+  }
+  const int units = std::min(t, cg == 2 ? sm_count() / 2 : sm_count());
+  if (units < 1) return 0;
+  std::stable_sort(cost.begin(), cost.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<long long> load(units, 0);
+  std::vector<std::vector<int>> lists(units);
+  for (const auto& ct : cost) {
+    int u = 0;
+    for (int v = 1; v < units; ++v)
+      if (load[v] < load[u]) u = v;
+    load[u] += ct.first;
+    lists[u].push_back(ct.second);
+  }
+  tiles_out->clear();
+  off_out->assign(1, 0);
+  for (const auto& l : lists) {
+    tiles_out->insert(tiles_out->end(), l.begin(), l.end());
+    off_out->push_back(static_cast<int>(tiles_out->size()));
+  }
+  *total_out = t;
+  return units;
+}
+
 cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
-                           float beta, float lr, cudaStream_t stream) {
+                           float beta, float lr, cudaStream_t stream, const NsSchedule* sched) {
   if (num_problems < 1 || num_problems > kMaxProblems) return cudaErrorInvalidValue;
   NsGemmParams P{};
   P.num_problems = num_problems;
@@ -695,6 +744,12 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     if (mode == kEpiSplit && d.out_seg < pr.N) return cudaErrorInvalidValue;
   }
   P.total_tiles = tiles;
+  if (sched != nullptr && sched->tiles != nullptr && sched->total_tiles == tiles &&
+      sched->units == std::min(tiles, cg == 2 ? sm_count() / 2 : sm_count())) {
+    P.sched = sched->tiles;
+    P.sched_off = sched->off;
+    P.sched_units = sched->units;
+  }
   if (cg == 2) {
     switch (mode) {
       case kEpiGram: return launch_mode<kEpiGram, 2>(P, stream);

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -76,6 +77,9 @@ struct NsGemmParams {
   NsGemmProblem prob[kMaxProblems];
   int num_problems;
   int total_tiles;
+  const int* sched;      // optional: tiles of unit u are sched[sched_off[u] .. sched_off[u+1])
+  const int* sched_off;
+  int sched_units;       // units (clusters / CTAs) the schedule was built for
   int tile_m;  // output rows per tile: 128 (cta_group::1) or 256 (cta_group::2)
   float alpha, beta, lr;
 };
@@ -100,9 +104,27 @@ struct NsProblemDesc {
   long long out_seg = 0;  // kEpiSplit segment width (elements)
 };
 
+// A cost-balanced static tile schedule for one grouped launch (device arrays).
+struct NsSchedule {
+  const int* tiles = nullptr;
+  const int* off = nullptr;
+  int units = 0;
+  int total_tiles = 0;
+};
+
 // Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).
+// `sched` (optional) must come from ns_gemm_schedule for the same problem
+// shapes; it is ignored if the grid or tile count does not match.
 cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
-                           float beta, float lr, cudaStream_t stream);
+                           float beta, float lr, cudaStream_t stream,
+                           const NsSchedule* sched = nullptr);
+
+// Host-side LPT schedule of a grouped launch: every tile costs its problem's
+// K-block count; tiles are taken heaviest first and given to the least-loaded
+// unit (ties: lowest unit), so long-K problems (vocabulary Grams) do not form
+// a tail. Fills per-unit tile lists; returns the unit count (0 on error).
+int ns_gemm_schedule(int mode, const NsProblemDesc* probs, int num_problems,
+                     std::vector<int>* tiles, std::vector<int>* off, int* total_tiles);
 
 // UMMA CTA group used by subsequent launches: 2 (default; CTA pairs, 256x256
 // tiles) or 1 (single-CTA 128x256 tiles). OSH_GEMM_CTA_GROUP=1 overrides.
