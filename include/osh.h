@@ -354,6 +354,18 @@ osh_status osh_read_param(osh_ctx* ctx, int32_t param_id, int32_t which, float* 
  * OSH_READ_MASTER / OSH_READ_MOMENTUM; owner only; replica untouched). */
 osh_status osh_write_state(osh_ctx* ctx, int32_t param_id, int32_t which, const float* values);
 
+/* Sharded optimizer-state checkpoint keyed by the plan (the
+ * reference's plan files, serialize.hpp:252-430, say WHAT a rank owns — this
+ * file holds that state). Each rank saves its owned fp32 master + momentum
+ * (and hosted TP-plane tensors, and the optimizer's extra state: Shampoo
+ * statistics, roots, step counter) behind a header with the rank / world /
+ * optimizer and a 64-bit hash of the model shapes and the plan's cut vectors.
+ * load_state on a ctx with a different plan, model, rank or optimizer fails
+ * with OSH_ERR_FORMAT; on success the owned replica slots are rewritten and
+ * the replica all-gathered (tp_size == 1), so training resumes bit-exactly. */
+osh_status osh_ctx_save_state(osh_ctx* ctx, const char* path);
+osh_status osh_ctx_load_state(osh_ctx* ctx, const char* path);
+
 #ifdef __cplusplus
 }
 #endif

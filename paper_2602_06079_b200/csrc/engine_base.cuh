@@ -61,6 +61,13 @@ class OptimizerEngine {
   virtual size_t workspace_bytes() const = 0;
   virtual int num_tensors() const = 0;
   virtual void set_symmetric(bool) {}
+  // Optimizer state beyond the per-tensor master / momentum (checkpointing):
+  // a device buffer whose layout is a pure function of the tensors and the
+  // configuration, plus the engine's step counter.
+  virtual void* extra_state() { return nullptr; }
+  virtual size_t extra_state_bytes() const { return 0; }
+  virtual long long step_counter() const { return 0; }
+  virtual void set_step_counter(long long) {}
 
   const NsLaunchStats& stats() const { return stats_; }  // since begin_step()
   // Per-launch CUDA-event timing of every launch (roofline reporting); the

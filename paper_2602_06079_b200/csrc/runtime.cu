@@ -122,6 +122,38 @@ void free_layout(osh_ctx* ctx) {
 
 }  // namespace
 
+namespace osh {
+
+// The bf16 replica from the owners' fp32 masters: every rank casts the
+// tensors it owns into its replica slots, then each bucket slice is
+// broadcast from its owner (tp_size == 1; with TP the next step refreshes it).
+osh_status refresh_replica(osh_ctx* ctx) {
+  cudaStream_t cs = ctx->compute;
+  for (size_t p = 0; p < ctx->params.size(); ++p) {
+    if (ctx->owned_off[p] < 0) continue;
+    const long long n = ctx->params[p].numel;
+    cast_f32_bf16_kernel<<<grid_for(n), 256, 0, cs>>>(ctx->w + ctx->owned_off[p],
+                                                     ctx->replica + ctx->flat_off[p], n);
+  }
+  OSH_CUDA_TRY(cudaGetLastError());
+  if (distributed(ctx) && ctx->tp_size == 1) {
+    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+      OSH_NCCL_TRY(ncclGroupStart());
+      for (int r = 0; r < ctx->size; ++r) {
+        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
+        if (cnt == 0) continue;
+        __nv_bfloat16* ptr = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
+        OSH_NCCL_TRY(ncclBroadcast(ptr, ptr, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, cs));
+      }
+      OSH_NCCL_TRY(ncclGroupEnd());
+    }
+  }
+  OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+  return OSH_OK;
+}
+
+}  // namespace osh
+
 extern "C" {
 
 osh_status osh_nccl_unique_id(uint8_t out[128]) {

@@ -123,6 +123,7 @@ osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
 osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);
+osh_status refresh_replica(osh_ctx* ctx);  // runtime.cu (checkpoint load)
 // NVLS helpers (nvls.cu)
 osh_status nvls_setup(osh_ctx* ctx, size_t grad_bytes, size_t replica_bytes, bool required);
 void nvls_free(osh_ctx* ctx);

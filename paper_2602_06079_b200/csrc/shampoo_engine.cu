@@ -68,7 +68,7 @@ void ShampooEngine::release() {
   for (void* p : {static_cast<void*>(d_ws_), static_cast<void*>(d_state_),
                   static_cast<void*>(d_partial_), static_cast<void*>(d_gsq_),
                   static_cast<void*>(d_usq_), static_cast<void*>(d_ssq_),
-                  static_cast<void*>(d_sroot_), static_cast<void*>(d_graft_),
+                  static_cast<void*>(d_graft_),
                   static_cast<void*>(d_update_sq_), static_cast<void*>(d_prep_),
                   static_cast<void*>(d_usq_tasks_), static_cast<void*>(d_ssq_tasks_),
                   static_cast<void*>(d_root_), static_cast<void*>(d_newton_),
@@ -471,6 +471,8 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
     waves_.push_back(std::move(w));
   }
   n_stats_total_ = n_stats;
+  const size_t sroot_off = rup(state_off, 256);  // root scales live in the state buffer too
+  state_off = sroot_off + rup(sizeof(float) * std::max(n_stats, 1), 256);
   state_bytes_ = state_off;
 
   // ---- allocate and patch
@@ -483,7 +485,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_usq_), sizeof(double) * std::max(n_blocks, 1)));
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_graft_), sizeof(float) * std::max(n_blocks, 1)));
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_ssq_), sizeof(double) * std::max(n_stats, 1)));
-  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_sroot_), sizeof(float) * std::max(n_stats, 1)));
+  d_sroot_ = reinterpret_cast<float*>(d_state_ + sroot_off);  // part of the checkpointed state
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_update_sq_), sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(cudaMemset(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1)));
   auto ws = [&](const void* p) { return d_ws_ + reinterpret_cast<uintptr_t>(p); };

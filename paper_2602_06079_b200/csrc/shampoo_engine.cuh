@@ -47,14 +47,18 @@ class ShampooEngine : public OptimizerEngine {
   int num_tensors() const override { return n_tensors_; }
   size_t state_bytes() const { return state_bytes_; }
   long long step_index() const { return step_; }
+  void* extra_state() override { return d_state_; }
+  size_t extra_state_bytes() const override { return state_bytes_; }
+  long long step_counter() const override { return step_; }
+  void set_step_counter(long long s) override { step_ = s; }
 
  private:
   struct Cls {                 // blocks of one (p, q) inside one wave
     int p = 0, q = 0, ldp = 0, ldq = 0, nb = 0, block0 = 0;
     size_t L = 0, R = 0, PL = 0, PR = 0;             // state offsets (bytes)
     size_t gb = 0, gbt = 0, u1 = 0, u = 0;           // workspace offsets (bytes)
-    size_t xl[2] = {0, 0}, ml[2] = {0, 0}, tl = 0, t2l = 0, t4l = 0;  // split, [nb][p][5p]
-    size_t xr[2] = {0, 0}, mr[2] = {0, 0}, tr = 0, t2r = 0, t4r = 0;  // split, [nb][q][5q]
+    size_t xl[2] = {0, 0}, ml[2] = {0, 0}, tl = 0, t2l = 0, t4l = 0;  // split, [nb][p][4 seg]
+    size_t xr[2] = {0, 0}, mr[2] = {0, 0}, tr = 0, t2r = 0, t4r = 0;  // split, [nb][q][4 seg]
     int stat0 = 0;             // first statistics-matrix index (L of block i = stat0 + i,
                                // R of block i = stat0 + nb + i)
   };
@@ -85,7 +89,7 @@ class ShampooEngine : public OptimizerEngine {
   double* d_gsq_ = nullptr;      // per block
   double* d_usq_ = nullptr;      // per block
   double* d_ssq_ = nullptr;      // per statistics matrix
-  float* d_sroot_ = nullptr;     // per statistics matrix: ||S||^(-1/4)
+  float* d_sroot_ = nullptr;     // per statistics matrix: ||S||^(-1/4) (inside d_state_)
   float* d_graft_ = nullptr;     // per block
   double* d_update_sq_ = nullptr;
   ShPrepTask* d_prep_ = nullptr;

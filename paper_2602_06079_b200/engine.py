@@ -211,6 +211,15 @@ class DistributedMuon:
         _lib.check(_lib.lib().osh_gemm_profile_read(self._ctx, ctypes.byref(p), 1 if reset else 0))
         return {"launches": p.launches, "flops": p.flops, "exec_flops": p.exec_flops, "ms": p.ms}
 
+    def save_state(self, path: str) -> None:
+        """This rank's optimizer state (osh_ctx_save_state; one file per rank)."""
+        _lib.check(_lib.lib().osh_ctx_save_state(self._ctx, path.encode()))
+
+    def load_state(self, path: str) -> None:
+        """Restore a state saved under the same plan/model/rank (else OshError,
+        code 7 = OSH_ERR_FORMAT); rewrites and all-gathers the replica."""
+        _lib.check(_lib.lib().osh_ctx_load_state(self._ctx, path.encode()))
+
     def update_norms(self) -> np.ndarray:
         out = np.zeros(len(self.params))
         _lib.check(_lib.lib().osh_update_norms(
