@@ -311,6 +311,14 @@ osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float s
  * Either host pointer may be NULL (device-resident data). */
 osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
                     void* host_replica_out);
+/* Gradient bucket `bucket` is complete in the grad buffer (its writes were
+ * enqueued on `stream`, a cudaStream_t; NULL = the ctx stream). Backward-pass
+ * overlap: on the NCCL path the bucket's
+ * RS-v starts at once on the comm stream while the caller keeps producing the
+ * other buckets; single-rank / NVLS steps wait per bucket. Either announce
+ * EVERY bucket (any order, the same order on every rank) before osh_step —
+ * which then only waits for them — or none. */
+osh_status osh_bucket_ready(osh_ctx* ctx, int32_t bucket, void* stream);
 osh_status osh_ctx_sync(osh_ctx* ctx);
 /* The ctx's compute stream (cudaStream_t): the step's last event is recorded
  * on it, so events recorded here bracket whole steps. */

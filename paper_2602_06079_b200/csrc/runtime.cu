@@ -152,6 +152,27 @@ osh_status refresh_replica(osh_ctx* ctx) {
   return OSH_OK;
 }
 
+// RS-v of bucket b on the comm stream: the owner of each slice receives the
+// sum of all ranks' slices in its grad_owned region (local grads intact).
+osh_status issue_rs(osh_ctx* ctx, int b) {
+  const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
+  const size_t es = grad_esize(ctx->grad_dtype);
+  OSH_NCCL_TRY(ncclGroupStart());
+  for (int r = 0; r < ctx->size; ++r) {
+    const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
+    if (cnt == 0) continue;
+    const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) +
+                         es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
+    uint8_t* dst = static_cast<uint8_t*>(ctx->grad_owned) +
+                   es * static_cast<size_t>(ctx->owned_slice_off[b]);
+    OSH_NCCL_TRY(ncclReduce(src, r == ctx->rank ? dst : nullptr, static_cast<size_t>(cnt), gtype,
+                            ncclSum, r, ctx->comm, ctx->comm_stream));
+  }
+  OSH_NCCL_TRY(ncclGroupEnd());
+  OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ctx->comm_stream));
+  return OSH_OK;
+}
+
 }  // namespace osh
 
 extern "C" {
@@ -488,6 +509,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   OSH_CUDA_TRY(make_events(ctx->wave_end, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->pre_ev, static_cast<size_t>(ctx->engine->num_waves())));
   OSH_CUDA_TRY(make_events(ctx->h2d_ev, ctx->cuts.size()));
+  ctx->bucket_marked.assign(ctx->cuts.size(), 0);
+  ctx->n_marked = 0;
   OSH_CUDA_TRY(make_events(ctx->ag_ev, ctx->cuts.size()));
   OSH_CUDA_TRY(make_events(ctx->ns_ev, static_cast<size_t>(ctx->engine->num_waves())));
   // The zero-fills and table uploads above ran on the legacy stream, which the
@@ -676,7 +699,9 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   const int nw = eng.num_waves();
   const int nb = static_cast<int>(ctx->cuts.size());
   auto wait_input = [&](int w) -> osh_status {
-    if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[eng.wave_last_bucket(w)], 0));
+    if (io.h2d)  // every bucket of the wave (announced buckets may land out of order)
+      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b)
+        OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
     return OSH_OK;
   };
   // after wave w every bucket before the next wave's first one is final
@@ -733,7 +758,20 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   // only for its own buckets; the replica leaves per finished bucket.
   HostIo io;
   const bool pipelined = !ctx->nvls && ctx->tp_size == 1;
-  if (host_grads != nullptr && pipelined) {
+  const int n_buckets = static_cast<int>(ctx->cuts.size());
+  const bool marked = ctx->n_marked > 0;  // gradients announced per bucket (osh_bucket_ready)
+  const int n_marked = ctx->n_marked;
+  std::fill(ctx->bucket_marked.begin(), ctx->bucket_marked.end(), 0);  // reset even on error
+  ctx->n_marked = 0;
+  if (marked && (n_marked != n_buckets || host_grads != nullptr)) {
+    if (distributed(ctx) && !ctx->nvls) cudaStreamSynchronize(ctx->comm_stream);  // drain issued RS
+    return osh::fail(OSH_ERR_ARG, "osh_step: osh_bucket_ready must cover every bucket (" +
+                                      std::to_string(n_marked) + " of " +
+                                      std::to_string(n_buckets) + ") and excludes host_grads");
+  }
+  if (marked) {
+    io.h2d = true;  // waves / barriers wait for the announced buckets
+  } else if (host_grads != nullptr && pipelined) {
     io.h2d = true;
     OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
     for (size_t b = 0; b < ctx->cuts.size(); ++b) {
@@ -750,7 +788,6 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   }
   if (host_replica_out != nullptr && pipelined) io.replica_out = host_replica_out;
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
-  const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
   const size_t es = grad_esize(ctx->grad_dtype);
   const int nb = static_cast<int>(ctx->cuts.size());
   osh::OptimizerEngine& eng = *ctx->engine;
@@ -762,9 +799,12 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       OSH_NCCL_TRY(ncclAllReduce(ctx->bar, ctx->bar, 1, ncclFloat32, ncclSum, ctx->comm, cs));
       return OSH_OK;
     };
+    if (marked)
+      for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+    HostIo nvls_io;  // (the barrier above already covers every bucket)
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
-    if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
+    if (osh_status st = run_waves_local(ctx, *cfg, cs, nvls_io); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
     if (osh_status st = barrier(); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
@@ -781,25 +821,12 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
     return OSH_OK;
   }
-  if (dist) {
-    // RS-v, bucket by bucket: the owner of slice r of bucket b receives the
-    // sum of all ranks' slices in its grad_owned region (local grads intact).
+  if (dist && !marked) {
+    // RS-v, bucket by bucket (osh_bucket_ready issued them already otherwise)
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
     for (int b = 0; b < nb; ++b) {
       if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->h2d_ev[b], 0));
-      OSH_NCCL_TRY(ncclGroupStart());
-      for (int r = 0; r < ctx->size; ++r) {
-        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
-        if (cnt == 0) continue;
-        const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) +
-                             es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
-        uint8_t* dst = static_cast<uint8_t*>(ctx->grad_owned) +
-                       es * static_cast<size_t>(ctx->owned_slice_off[b]);
-        OSH_NCCL_TRY(ncclReduce(src, r == ctx->rank ? dst : nullptr, static_cast<size_t>(cnt),
-                                gtype, ncclSum, r, ctx->comm, ns));
-      }
-      OSH_NCCL_TRY(ncclGroupEnd());
-      OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ns));
+      if (osh_status st = osh::issue_rs(ctx, b); st != OSH_OK) return st;
     }
   }
   auto all_gather = [&](int b) -> osh_status {
@@ -820,8 +847,10 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
   } else {
     for (int w = 0; w < nw; ++w) {
-      if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[eng.wave_last_bucket(w)], 0));
-      else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[eng.wave_last_bucket(w)], 0));
+      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b) {
+        if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
+        else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+      }
       OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
       if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaGetLastError());
@@ -840,7 +869,8 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   if (ctx->tp_size > 1) {
     // micro groups need every reduced shard of the TP plane: wait for the
     // whole reduce-scatter, then gather / compute / scatter group by group
-    if (dist && nb > 0) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[nb - 1], 0));
+    if (dist)
+      for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
     if (osh_status st = osh::tp_step(ctx, *cfg, cs); st != OSH_OK) return st;
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
@@ -853,7 +883,8 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   } else {
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
   }
-  if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[nb - 1], 0));
+  if (io.h2d)
+    for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
   if (io.replica_out != nullptr) {
     if (osh_status st = d2h_buckets(ctx, io, nb - 1, ctx->ev[3]); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->d2h_stream));
@@ -870,6 +901,26 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   ctx->last_timing.elementwise_launches = s.launches_elementwise;
   ctx->last_timing.gemm_flops = s.gemm_flops;
   if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+  return OSH_OK;
+}
+
+osh_status osh_bucket_ready(osh_ctx* ctx, int32_t bucket, void* stream) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  const int nb = static_cast<int>(ctx->cuts.size());
+  if (bucket < 0 || bucket >= nb) return osh::fail(OSH_ERR_ARG, "osh_bucket_ready: bucket out of range");
+  if (ctx->bucket_marked[bucket])
+    return osh::fail(OSH_ERR_ARG, "osh_bucket_ready: bucket marked twice in one step");
+  cudaStream_t us = stream != nullptr ? static_cast<cudaStream_t>(stream) : ctx->compute;
+  OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_ev[bucket], us));  // "gradient of bucket b landed"
+  if (distributed(ctx) && !ctx->nvls) {
+    // reduce now, overlapping the rest of the backward pass; the previous
+    // step must be done with grad_owned first
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[4], 0));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->h2d_ev[bucket], 0));
+    if (osh_status st = osh::issue_rs(ctx, bucket); st != OSH_OK) return st;
+  }
+  ctx->bucket_marked[bucket] = 1;
+  ++ctx->n_marked;
   return OSH_OK;
 }
 

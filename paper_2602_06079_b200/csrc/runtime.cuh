@@ -44,6 +44,8 @@ struct osh_ctx {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // osh_step host I/O, per bucket
   std::vector<cudaEvent_t> h2d_ev, ag_ev;  // per bucket: gradient landed / all-gathered
   bool last_h2d_pipelined = false;
+  std::vector<char> bucket_marked;     // osh_bucket_ready marks of the coming step
+  int n_marked = 0;
   cudaEvent_t ev[8] = {};
 
   // layout

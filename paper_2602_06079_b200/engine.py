@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .planner import DpPartitionPlan, ParamSpec, _desc_array
+from .planner import DpPartitionPlan, ParamSpec, _desc_array, apply_tp_sharding, build_buffer_layout
 
 GRAD_DTYPES = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
 READ = {"master": 0, "momentum": 1, "replica": 2}
@@ -102,6 +102,8 @@ class DistributedMuon:
             sc = (shampoo or ShampooConfig()).c()
             _lib.check(L.osh_ctx_set_optimizer(ctx, OPTIMIZERS[optimizer], ctypes.byref(sc)))
         self.optimizer = optimizer
+        view = apply_tp_sharding(self.params, tp_size) if tp_size > 1 else self.params
+        self._bucket_params = [list(b) for b in build_buffer_layout(view, bucket_capacity).buckets]
         cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)
         _lib.check(L.osh_ctx_set_layout(ctx, _desc_array(self.params), len(self.params),
                                         bucket_capacity,
@@ -210,6 +212,16 @@ class DistributedMuon:
         p = _lib.GemmProfile()
         _lib.check(_lib.lib().osh_gemm_profile_read(self._ctx, ctypes.byref(p), 1 if reset else 0))
         return {"launches": p.launches, "flops": p.flops, "exec_flops": p.exec_flops, "ms": p.ms}
+
+    def bucket_ready(self, bucket: int, stream: Optional[int] = None) -> None:
+        """Announce that gradient bucket ``bucket`` is complete (work on
+        ``stream``, a raw cudaStream_t; None = the ctx stream). NCCL path: its
+        reduce-scatter starts now, overlapping the rest of the backward pass."""
+        _lib.check(_lib.lib().osh_bucket_ready(self._ctx, bucket, stream))
+
+    def bucket_params(self) -> list:
+        """Parameter ids of every bucket (declaration order, planner layout)."""
+        return self._bucket_params
 
     def save_state(self, path: str) -> None:
         """This rank's optimizer state (osh_ctx_save_state; one file per rank)."""

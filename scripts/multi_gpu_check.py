@@ -38,6 +38,7 @@ def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     coll = sys.argv[2] if len(sys.argv) > 2 else "auto"
     opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
+    announce = len(sys.argv) > 4 and sys.argv[4] == "buckets"  # osh_bucket_ready, reverse order
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     td.init_process_group("gloo")
@@ -45,7 +46,7 @@ def main():
     shapes = [(1024, 3072), (1024, 1024), (3072, 1024), (1024,), (4000, 1024), (200, 328),
               (333, 96), (1024,), (64, 64), (512, 1536), (1536, 512), (512,)]
     params = [P.ParamSpec(i, f"t{i}", s) for i, s in enumerate(shapes)]
-    cap = 5_000_000
+    cap = int(os.environ.get("OSH_CHECK_CAP", 5_000_000))
     plan = P.plan_dp(params, cap, world, "alpha-balanced", "numel", 1.0)
     owners = P.param_owners(params, cap, plan)
     uid = [nccl_unique_id() if rank == 0 else None]
@@ -58,8 +59,14 @@ def main():
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
     norms = []
     for step in range(steps):
-        for p in params:
-            eng.write_grad(p.id, O.synth_gradient(p.shape, p.id, SEED, step, rank))
+        if announce:
+            for b in reversed(range(len(eng.bucket_params()))):
+                for pid in eng.bucket_params()[b]:
+                    eng.write_grad(pid, O.synth_gradient(params[pid].shape, pid, SEED, step, rank))
+                eng.bucket_ready(b)
+        else:
+            for p in params:
+                eng.write_grad(p.id, O.synth_gradient(p.shape, p.id, SEED, step, rank))
         eng.step(OptimizerConfig())
         eng.sync()
         norms.append(eng.update_norms())
@@ -109,7 +116,8 @@ def main():
         ok &= good
         report[p.name] = {"owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
-    print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt, "ok": ok,
+    print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt,
+                      "bucket_ready": announce, "ok": ok,
                       "params": report}))
     return 0 if ok else 1
 

@@ -60,6 +60,13 @@ def test_dp2_tp2_micro_groups_match_oracle():
     _run(4, "multi_gpu_check_tp.py", 2, 2, 3)
 
 
+def test_dp2_nccl_bucket_ready_matches_oracle():
+    # gradients announced bucket by bucket in reverse order: the RS-v of each
+    # bucket starts before the next one is written (backward overlap)
+    res = _run(2, "multi_gpu_check.py", 3, "nccl", "muon", "buckets")
+    assert res["bucket_ready"]
+
+
 def test_dp2_shampoo_matches_spec():
     res = _run(2, "multi_gpu_check.py", 3, "auto", "shampoo")
     assert res["optimizer"] == "shampoo"
