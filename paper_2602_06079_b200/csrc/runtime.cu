@@ -677,12 +677,26 @@ namespace {
 // d2h_stream after the wave that completes them.
 struct HostIo {
   bool h2d = false;        // wait for h2d_ev before a wave's momentum
+  const std::vector<cudaEvent_t>* wait_ev = nullptr;  // per-bucket events to wait instead
   void* replica_out = nullptr;  // per-bucket D2H after each wave (nullptr: none)
   int d2h_next = 0;
+  bool nvls_out = false;   // NVLS: a cross-rank barrier per bucket precedes its D2H
 };
 
 osh_status d2h_buckets(osh_ctx* ctx, HostIo& io, int upto, cudaEvent_t ready) {
   if (io.replica_out == nullptr || upto < io.d2h_next) return OSH_OK;
+  if (io.nvls_out) {
+    // every rank's multicast stores into these buckets must have landed: one
+    // barrier per bucket on the comm stream (same count and order on every
+    // rank, since all ranks share the bucket layout), then the copy
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ready, 0));
+    for (int b = io.d2h_next; b <= upto; ++b) {
+      OSH_NCCL_TRY(ncclAllReduce(ctx->bar + 1, ctx->bar + 1, 1, ncclFloat32, ncclSum, ctx->comm,
+                                 ctx->comm_stream));
+      OSH_CUDA_TRY(cudaEventRecord(ctx->ag_ev[b], ctx->comm_stream));
+    }
+    ready = ctx->ag_ev[upto];
+  }
   OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ready, 0));
   const int64_t b0 = ctx->bucket_base[io.d2h_next];
   const int64_t b1 = upto + 1 < static_cast<int>(ctx->bucket_base.size()) ? ctx->bucket_base[upto + 1]
@@ -699,9 +713,11 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   const int nw = eng.num_waves();
   const int nb = static_cast<int>(ctx->cuts.size());
   auto wait_input = [&](int w) -> osh_status {
-    if (io.h2d)  // every bucket of the wave (announced buckets may land out of order)
+    const std::vector<cudaEvent_t>* ev = io.wait_ev != nullptr ? io.wait_ev
+                                         : io.h2d ? &ctx->h2d_ev : nullptr;
+    if (ev != nullptr)  // every bucket of the wave (announced buckets may land out of order)
       for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b)
-        OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+        OSH_CUDA_TRY(cudaStreamWaitEvent(cs, (*ev)[b], 0));
     return OSH_OK;
   };
   // after wave w every bucket before the next wave's first one is final
@@ -783,7 +799,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_ev[b], ctx->h2d_stream));
     }
     OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
-  } else if (host_grads != nullptr) {
+  } else if (host_grads != nullptr && !ctx->nvls) {  // (NVLS: copied in its branch)
     OSH_CUDA_TRY(cudaMemcpyAsync(ctx->grad, host_grads, gbytes, cudaMemcpyHostToDevice, cs));
   }
   if (host_replica_out != nullptr && pipelined) io.replica_out = host_replica_out;
@@ -794,26 +810,59 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   const int nw = eng.num_waves();
   if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
   if (ctx->nvls) {
-    // barrier -> waves (reduce / broadcast inside the kernels) -> barrier
-    auto barrier = [&]() -> osh_status {
-      OSH_NCCL_TRY(ncclAllReduce(ctx->bar, ctx->bar, 1, ncclFloat32, ncclSum, ctx->comm, cs));
+    // barrier -> waves (reduce / broadcast inside the kernels) -> barrier.
+    // With host buffers the barriers go per bucket on the comm stream: bucket b
+    // is "in" once every rank's H2D of b landed, and "out" once every owner's
+    // multicast stores into b did, so copies overlap the waves.
+    auto barrier = [&](cudaStream_t st) -> osh_status {
+      OSH_NCCL_TRY(ncclAllReduce(ctx->bar, ctx->bar, 1, ncclFloat32, ncclSum, ctx->comm, st));
       return OSH_OK;
     };
-    if (marked)
-      for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
-    HostIo nvls_io;  // (the barrier above already covers every bucket)
-    if (osh_status st = barrier(); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
+    HostIo nvls_io;
+    const bool pipe_in = host_grads != nullptr && !marked;
+    if (pipe_in) {
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[5], 0));
+      const size_t ges = grad_esize(ctx->grad_dtype);
+      for (int b = 0; b < nb; ++b) {
+        const size_t off = ges * static_cast<size_t>(ctx->bucket_base[b]);
+        const size_t len = ges * static_cast<size_t>(ctx->layout.buckets[b].numel);
+        OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->grad) + off,
+                                     static_cast<const uint8_t*>(host_grads) + off, len,
+                                     cudaMemcpyHostToDevice, ctx->h2d_stream));
+        OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_ev[b], ctx->h2d_stream));
+        OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->h2d_ev[b], 0));
+        if (osh_status st = barrier(ns); st != OSH_OK) return st;
+        OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ns));
+      }
+      nvls_io.wait_ev = &ctx->rs_ev;
+    } else {
+      if (host_grads != nullptr)  // (with announced buckets host_grads was rejected above)
+        OSH_CUDA_TRY(cudaMemcpyAsync(ctx->grad, host_grads, gbytes, cudaMemcpyHostToDevice, cs));
+      if (marked)
+        for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+      if (osh_status st = barrier(cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
+    }
+    if (host_replica_out != nullptr) {
+      nvls_io.replica_out = host_replica_out;
+      nvls_io.nvls_out = true;
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
+    }
     if (osh_status st = run_waves_local(ctx, *cfg, cs, nvls_io); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
-    if (osh_status st = barrier(); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], cs));
-    if (host_replica_out != nullptr)
-      OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
-                                   2 * static_cast<size_t>(ctx->total_numel),
-                                   cudaMemcpyDeviceToHost, cs));
+    // end barrier on the comm stream (after any per-bucket barriers there)
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
+    if (osh_status st = barrier(ns); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
+    if (host_replica_out != nullptr) {
+      if (osh_status st = d2h_buckets(ctx, nvls_io, nb - 1, ctx->ev[3]); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->d2h_stream));
+      OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[6], 0));
+    }
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
-    ctx->last_h2d_pipelined = false;
+    ctx->last_h2d_pipelined = pipe_in;
     const osh::NsLaunchStats& s = eng.stats();
     ctx->last_timing.gemm_launches = s.launches_gemm;
     ctx->last_timing.elementwise_launches = s.launches_elementwise;

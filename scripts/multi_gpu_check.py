@@ -39,6 +39,7 @@ def main():
     coll = sys.argv[2] if len(sys.argv) > 2 else "auto"
     opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
     announce = len(sys.argv) > 4 and sys.argv[4] == "buckets"  # osh_bucket_ready, reverse order
+    host = len(sys.argv) > 4 and sys.argv[4] == "host"  # e2e entry: host gradients / replica
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     td.init_process_group("gloo")
@@ -58,7 +59,17 @@ def main():
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
     norms = []
+    total = sum(p.numel for p in params)
+    hrep = torch.empty(total, dtype=torch.bfloat16).pin_memory() if host else None
     for step in range(steps):
+        if host:
+            hg = torch.from_numpy(np.concatenate(
+                [O.synth_gradient(p.shape, p.id, SEED, step, rank).reshape(-1) for p in params])
+                .astype(np.float32)).pin_memory()
+            eng.step(OptimizerConfig(), host_grads=hg.data_ptr(), host_replica_out=hrep.data_ptr())
+            eng.sync()
+            norms.append(eng.update_norms())
+            continue
         if announce:
             for b in reversed(range(len(eng.bucket_params()))):
                 for pid in eng.bucket_params()[b]:
@@ -73,6 +84,11 @@ def main():
     mine = {p.id: eng.read_param(p.id, "master").astype(np.float64)
             for p in params if owners[p.id] == rank}
     replica = {p.id: eng.read_param(p.id, "replica") for p in params}
+    if host:  # the replica the step copied out must equal the device replica
+        off = 0
+        for p in params:
+            assert np.array_equal(hrep[off:off + p.numel].float().numpy(), replica[p.id].reshape(-1))
+            off += p.numel
     gathered = [None] * world
     td.all_gather_object(gathered, (mine, norms, replica))
     eng.close()
@@ -117,7 +133,7 @@ def main():
         report[p.name] = {"owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
     print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt,
-                      "bucket_ready": announce, "ok": ok,
+                      "bucket_ready": announce, "host_buffers": host, "ok": ok,
                       "params": report}))
     return 0 if ok else 1
 

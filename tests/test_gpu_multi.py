@@ -67,6 +67,13 @@ def test_dp2_nccl_bucket_ready_matches_oracle():
     assert res["bucket_ready"]
 
 
+def test_dp2_host_buffers_nvls_and_nccl():
+    # the e2e entry (host gradients in, replica out) on both collective paths
+    for coll in ("auto", "nccl"):
+        res = _run(2, "multi_gpu_check.py", 2, coll, "muon", "host")
+        assert res["host_buffers"]
+
+
 def test_dp2_shampoo_matches_spec():
     res = _run(2, "multi_gpu_check.py", 3, "auto", "shampoo")
     assert res["optimizer"] == "shampoo"
