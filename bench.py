@@ -60,6 +60,9 @@ def parse_args():
                     help="muon = the headline metric; shampoo = builder-defined blocked Shampoo")
     ap.add_argument("--shampoo-block", type=int, default=1024)
     ap.add_argument("--precond-every", type=int, default=10)
+    ap.add_argument("--strategy", default="sharded", choices=["sharded", "sc", "nv-layerwise"],
+                    help="sharded = the plan's owners (LB-ASC with --method alpha-balanced); "
+                         "sc / nv-layerwise = the paper's baselines executed for real")
     ap.add_argument("--collectives", default="auto", choices=["auto", "nccl", "nvls"],
                     help="DP RS/AG path: NCCL kernels or NVLS multicast fused into the update")
     ap.add_argument("--tp", type=int, default=1,
@@ -268,7 +271,7 @@ def run_ours(a, dist: Dist):
                           comm="nccl", nccl_uid=uid, grad_dtype=a.grad_dtype,
                           workspace_bytes=int(a.workspace_gb * (1 << 30)), tp_rank=t, tp_size=T,
                           tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None,
-                          collectives=a.collectives, optimizer=a.optimizer,
+                          collectives=a.collectives, optimizer=a.optimizer, strategy=a.strategy,
                           shampoo=(ShampooConfig(block=a.shampoo_block, precond_every=a.precond_every)
                                    if a.optimizer == "shampoo" else None))
     info = eng.info()
@@ -424,6 +427,7 @@ def run_ours(a, dist: Dist):
             "plan": (f"alpha-balanced alpha={a.alpha}" if a.method == "alpha-balanced"
                      else a.method) + f" cost={a.cost}",
             "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype, "collectives": coll_path,
+            "strategy": a.strategy,
             "parallelism": ((f"dp{N} (ZeRO-1 variable-size RS/AG fused into the update kernels: "
                              "multimem.ld_reduce / multimem.st over NVSwitch)" if coll_path == "nvls"
                              else f"dp{N} (ZeRO-1 variable-size RS/AG over NCCL)") if T == 1 else

@@ -262,6 +262,26 @@ typedef struct osh_shampoo_cfg {
   int32_t reserved;
 } osh_shampoo_cfg;
 enum { OSH_OPT_MUON = 0, OSH_OPT_SHAMPOO = 1 };
+
+/* Data-parallel optimizer strategy (simulate.hpp:33-39 made executable, the
+ * paper's baselines measured on the GPU). Call before
+ * set_layout.
+ *   OSH_STRAT_SHARDED       the plan's owners (LB-ASC with an α-balanced plan,
+ *                           ASC with an atomic-ownership plan): RS-v, owner
+ *                           update, AG-v (default)
+ *   OSH_STRAT_SC            replicated: all-reduce the gradients, every rank
+ *                           updates every tensor, no redistribution
+ *   OSH_STRAT_NV_LAYERWISE  whole-layer ownership by LPT over layer costs
+ *                           (layerwise_rank_loads, simulate.hpp:140-157):
+ *                           all-reduce the gradients, the owner updates its
+ *                           layers, then broadcasts them (kBroadcast
+ *                           redistribution, simulate.hpp:58-59)
+ * layer_of: per parameter, its layer group id (ids in first-appearance
+ * order of the name segment before the first '.', simulate.hpp:130-135);
+ * required for NV_LAYERWISE. cost: the execution cost model of the LPT. */
+enum { OSH_STRAT_SHARDED = 0, OSH_STRAT_SC = 1, OSH_STRAT_NV_LAYERWISE = 2 };
+osh_status osh_ctx_set_strategy(osh_ctx* ctx, int32_t strategy, const int32_t* layer_of,
+                                int32_t n, const osh_cost_model* cost);
 osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out);
 osh_status osh_ctx_set_optimizer(osh_ctx* ctx, int32_t kind, const osh_shampoo_cfg* cfg);
 

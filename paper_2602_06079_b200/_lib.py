@@ -154,6 +154,7 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_ctx_set_optimizer", c_int32, c_void_p, c_int32, POINTER(ShampooCfgC)),
         ("osh_ctx_save_state", c_int32, c_void_p, c_char_p),
         ("osh_bucket_ready", c_int32, c_void_p, c_int32, c_void_p),
+        ("osh_ctx_set_strategy", c_int32, c_void_p, c_int32, c_void_p, c_int32, c_void_p),
         ("osh_ctx_load_state", c_int32, c_void_p, c_char_p),
         ("osh_ctx_set_layout", c_int32, c_void_p, POINTER(ParamDesc), c_int32, c_int64,
          POINTER(c_int64), c_int32, c_int32, c_int64),

@@ -251,6 +251,30 @@ osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode) {
   return OSH_OK;
 }
 
+osh_status osh_ctx_set_strategy(osh_ctx* ctx, int32_t strategy, const int32_t* layer_of,
+                                int32_t n, const osh_cost_model* cost) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (strategy < OSH_STRAT_SHARDED || strategy > OSH_STRAT_NV_LAYERWISE)
+    return osh::fail(OSH_ERR_CONFIG, "unknown strategy");
+  if (strategy != OSH_STRAT_SHARDED && ctx->tp_size > 1)
+    return osh::fail(OSH_ERR_UNSUPPORTED, "SC / NV-layerwise baselines run with tp_size == 1");
+  if (strategy == OSH_STRAT_NV_LAYERWISE && (layer_of == nullptr || n < 1))
+    return osh::fail(OSH_ERR_ARG, "NV-layerwise needs the layer group of every parameter");
+  ctx->strategy = strategy;
+  ctx->layer_of.clear();
+  if (layer_of != nullptr) ctx->layer_of.assign(layer_of, layer_of + n);
+  ctx->strategy_cost = CostModel{};
+  if (cost != nullptr) {
+    if (cost->kind < OSH_COST_NUMEL || cost->kind > OSH_COST_BYTES)
+      return osh::fail(OSH_ERR_CONFIG, "unknown cost kind");
+    ctx->strategy_cost.kind = static_cast<CostKind>(cost->kind);
+    ctx->strategy_cost.ns_steps = cost->ns_steps;
+    ctx->strategy_cost.shampoo_coeff = cost->shampoo_coeff;
+    ctx->strategy_cost.soap_coeff = cost->soap_coeff;
+  }
+  return OSH_OK;
+}
+
 osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out) {
   if (out == nullptr) return osh::fail(OSH_ERR_ARG, "null output");
   const osh::ShampooConfig d;
@@ -387,8 +411,31 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     ctx->total_numel = base;
     ctx->owned_numel = 0;
     int64_t alloc = 0;
+    // strategy baselines: SC replicates every tensor; NV-layerwise assigns whole
+    // layers by LPT (min_heap_balance over the layer costs, simulate.hpp:140-157)
+    std::vector<int> layer_owner;
+    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE) {
+      if (ctx->layer_of.size() != np) throw PlanError("layer_of must cover every parameter");
+      std::vector<Cost> layer_cost;
+      for (size_t p = 0; p < np; ++p) {
+        const size_t l = static_cast<size_t>(ctx->layer_of[p]);
+        if (layer_cost.size() <= l) layer_cost.resize(l + 1, 0);
+        layer_cost[l] += param_cost(ctx->params[p], ctx->strategy_cost);
+      }
+      std::vector<TpItem> items;
+      for (size_t l = 0; l < layer_cost.size(); ++l) items.push_back({static_cast<int>(l), layer_cost[l]});
+      const HeapAssignment a = min_heap_balance(items, ctx->size);
+      layer_owner.assign(layer_cost.size(), 0);
+      for (size_t rr = 0; rr < a.rank_params.size(); ++rr)
+        for (const int l : a.rank_params[rr]) layer_owner[static_cast<size_t>(l)] = static_cast<int>(rr);
+    }
     for (size_t p = 0; p < np; ++p) {
-      ctx->owner[p] = param_owner(plan, ctx->layout, static_cast<int>(p));
+      if (ctx->strategy == OSH_STRAT_SC)
+        ctx->owner[p] = ctx->rank;
+      else if (ctx->strategy == OSH_STRAT_NV_LAYERWISE)
+        ctx->owner[p] = layer_owner[static_cast<size_t>(ctx->layer_of[p])];
+      else
+        ctx->owner[p] = param_owner(plan, ctx->layout, static_cast<int>(p));
       if (ctx->owner[p] == ctx->rank && !is_tp_item(ctx, p)) {
         ctx->owned_off[p] = alloc;
         alloc += (ctx->params[p].numel + kOwnedAlign - 1) / kOwnedAlign * kOwnedAlign;
@@ -410,7 +457,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   const size_t es = grad_esize(grad_dtype);
   // NVLS needs every tensor on the 16-byte vector layout (decided from the
   // model alone, so every rank takes the same branch of the collective setup)
-  bool nvls_layout = distributed(ctx) && ctx->tp_size == 1;
+  bool nvls_layout = distributed(ctx) && ctx->tp_size == 1 && ctx->strategy == OSH_STRAT_SHARDED;
   for (size_t p = 0; p < ctx->params.size() && nvls_layout; ++p) {
     const ParamSpec& ps = ctx->params[p];
     const int64_t inner = ps.is_matrix() ? ps.shape[1] : ps.numel;
@@ -434,7 +481,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   OSH_CUDA_TRY(cudaMemset(ctx->replica, 0, 2 * static_cast<size_t>(ctx->total_numel)));
   if (distributed(ctx)) OSH_CUDA_TRY(osh::dev_alloc(reinterpret_cast<void**>(&ctx->bar), 16));
   // Reduced-gradient slices of this rank (NCCL mode): bucket after bucket.
-  const bool reduce_out = distributed(ctx) && !ctx->nvls;
+  // (SC / NV-layerwise all-reduce the whole buffer in place instead.)
+  const bool reduce_out = distributed(ctx) && !ctx->nvls && ctx->strategy == OSH_STRAT_SHARDED;
   ctx->owned_slice_off.assign(ctx->cuts.size(), 0);
   int64_t slice_total = 0;
   for (size_t b = 0; b < ctx->cuts.size(); ++b) {
@@ -870,6 +918,61 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
     return OSH_OK;
   }
+  if (dist && ctx->strategy != OSH_STRAT_SHARDED) {
+    // SC / NV-layerwise baselines: all-reduce every bucket in place, then the
+    // waves (each waits for its buckets), then NV-layerwise broadcasts every
+    // tensor from its layer owner. Reduction per bucket overlaps the waves.
+    if (marked) return osh::fail(OSH_ERR_UNSUPPORTED, "osh_bucket_ready with SC / NV-layerwise");
+    const ncclDataType_t gt = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
+    for (int b = 0; b < nb; ++b) {
+      if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->h2d_ev[b], 0));
+      uint8_t* base = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->bucket_base[b]);
+      OSH_NCCL_TRY(ncclAllReduce(base, base, static_cast<size_t>(ctx->layout.buckets[b].numel), gt,
+                                 ncclSum, ctx->comm, ns));
+      OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ns));
+    }
+    HostIo bio;
+    bio.wait_ev = &ctx->rs_ev;
+    if (ctx->strategy == OSH_STRAT_SC) {  // replica complete locally after each wave
+      bio.replica_out = io.replica_out;
+      if (bio.replica_out != nullptr)
+        OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
+    }
+    if (osh_status st = run_waves_local(ctx, *cfg, cs, bio); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
+    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE) {
+      OSH_NCCL_TRY(ncclGroupStart());
+      for (size_t p = 0; p < ctx->params.size(); ++p) {
+        __nv_bfloat16* ptr = ctx->replica + ctx->flat_off[p];
+        OSH_NCCL_TRY(ncclBroadcast(ptr, ptr, static_cast<size_t>(ctx->params[p].numel), ncclBfloat16,
+                                   ctx->owner[p], ctx->comm, ns));
+      }
+      OSH_NCCL_TRY(ncclGroupEnd());
+    }
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
+    if (io.h2d)
+      for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+    if (bio.replica_out != nullptr) {
+      if (osh_status st = d2h_buckets(ctx, bio, nb - 1, ctx->ev[3]); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->d2h_stream));
+      OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[6], 0));
+    } else if (host_replica_out != nullptr) {
+      OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
+                                   2 * static_cast<size_t>(ctx->total_numel),
+                                   cudaMemcpyDeviceToHost, cs));
+    }
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[4], cs));
+    ctx->last_h2d_pipelined = io.h2d;
+    const osh::NsLaunchStats& s = eng.stats();
+    ctx->last_timing.gemm_launches = s.launches_gemm;
+    ctx->last_timing.elementwise_launches = s.launches_elementwise;
+    ctx->last_timing.gemm_flops = s.gemm_flops;
+    if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+    return OSH_OK;
+  }
   if (dist && !marked) {
     // RS-v, bucket by bucket (osh_bucket_ready issued them already otherwise)
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
@@ -959,6 +1062,8 @@ osh_status osh_bucket_ready(osh_ctx* ctx, int32_t bucket, void* stream) {
   if (bucket < 0 || bucket >= nb) return osh::fail(OSH_ERR_ARG, "osh_bucket_ready: bucket out of range");
   if (ctx->bucket_marked[bucket])
     return osh::fail(OSH_ERR_ARG, "osh_bucket_ready: bucket marked twice in one step");
+  if (ctx->strategy != OSH_STRAT_SHARDED)
+    return osh::fail(OSH_ERR_UNSUPPORTED, "osh_bucket_ready needs the sharded strategy");
   cudaStream_t us = stream != nullptr ? static_cast<cudaStream_t>(stream) : ctx->compute;
   OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_ev[bucket], us));  // "gradient of bucket b landed"
   if (distributed(ctx) && !ctx->nvls) {

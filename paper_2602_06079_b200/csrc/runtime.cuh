@@ -81,6 +81,9 @@ struct osh_ctx {
   // the update kernels reduce / broadcast through their multicast addresses
   int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
   int optimizer = 0;                    // OSH_OPT_MUON / OSH_OPT_SHAMPOO
+  int strategy = 0;                     // OSH_STRAT_SHARDED / _SC / _NV_LAYERWISE
+  std::vector<int32_t> layer_of;        // NV_LAYERWISE: layer group per parameter
+  optishard::CostModel strategy_cost;
   osh::ShampooConfig shampoo;
   bool nvls = false;
   void* nvls_state = nullptr;

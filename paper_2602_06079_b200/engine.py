@@ -55,6 +55,17 @@ class ShampooConfig:
 
 
 OPTIMIZERS = {"muon": 0, "shampoo": 1}
+STRATEGIES = {"sharded": 0, "sc": 1, "nv-layerwise": 2}
+
+
+def layer_groups(params) -> np.ndarray:
+    """Layer group id per parameter: the name segment before the first '.',
+    ids in first-appearance order (simulate.hpp:130-135,140-152)."""
+    ids, out = {}, []
+    for p in params:
+        key = p.name.split(".", 1)[0]
+        out.append(ids.setdefault(key, len(ids)))
+    return np.asarray(out, dtype=np.int32)
 COLLECTIVES = {"auto": 0, "nccl": 1, "nvls": 2}
 COLLECTIVE_NAMES = {0: "none", 1: "nccl", 2: "nvls"}
 
@@ -70,7 +81,8 @@ class DistributedMuon:
                  workspace_bytes: int = 0, tp_rank: int = 0, tp_size: int = 1,
                  tp_uid: Optional[bytes] = None, tp_capacity: Optional[int] = None,
                  collectives: str = "auto", optimizer: str = "muon",
-                 shampoo: Optional[ShampooConfig] = None):
+                 shampoo: Optional[ShampooConfig] = None, strategy: str = "sharded",
+                 strategy_cost: str = "numel"):
         """With tp_size > 1: ``params`` are the FULL tensors, ``plan`` /
         ``bucket_capacity`` describe the DP partition of the TP-sharded view
         (planner.apply_tp_sharding), ``rank`` is the DP rank.
@@ -80,7 +92,11 @@ class DistributedMuon:
         broadcast fused into the update kernels through NVSwitch multicast
         (OshError when the node cannot), "auto" = nvls when available.
         ``optimizer``: "muon" (the reference's step) or "shampoo" (builder-
-        defined blocked Shampoo, ``shampoo`` = its ShampooConfig)."""
+        defined blocked Shampoo, ``shampoo`` = its ShampooConfig).
+        ``strategy``: "sharded" (the plan's owners: LB-ASC / ASC), or the
+        paper's baselines "sc" (replicated update after an all-reduce) and
+        "nv-layerwise" (whole-layer LPT owners over ``strategy_cost``,
+        all-reduce, owner update, broadcast)."""
         L = _lib.lib()
         self.params = list(params)
         self.rank, self.world = rank, plan.ranks
@@ -102,6 +118,14 @@ class DistributedMuon:
             sc = (shampoo or ShampooConfig()).c()
             _lib.check(L.osh_ctx_set_optimizer(ctx, OPTIMIZERS[optimizer], ctypes.byref(sc)))
         self.optimizer = optimizer
+        if strategy != "sharded":
+            from .planner import cost_model
+            lay = layer_groups(self.params)
+            cm = cost_model(strategy_cost)
+            _lib.check(L.osh_ctx_set_strategy(ctx, STRATEGIES[strategy],
+                                              lay.ctypes.data_as(ctypes.c_void_p), len(lay),
+                                              ctypes.byref(cm)))
+        self.strategy = strategy
         view = apply_tp_sharding(self.params, tp_size) if tp_size > 1 else self.params
         self._bucket_params = [list(b) for b in build_buffer_layout(view, bucket_capacity).buckets]
         cuts = np.ascontiguousarray(plan.cut_vectors, dtype=np.int64)

@@ -40,6 +40,7 @@ def main():
     opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
     announce = len(sys.argv) > 4 and sys.argv[4] == "buckets"  # osh_bucket_ready, reverse order
     host = len(sys.argv) > 4 and sys.argv[4] == "host"  # e2e entry: host gradients / replica
+    strategy = sys.argv[5] if len(sys.argv) > 5 else "sharded"  # or the sc / nv-layerwise baselines
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     td.init_process_group("gloo")
@@ -54,7 +55,7 @@ def main():
     td.broadcast_object_list(uid, src=0)
     eng = DistributedMuon(params, cap, plan, rank=rank, device=local, comm="nccl", nccl_uid=uid[0],
                           grad_dtype="f32", collectives=coll, optimizer=opt,
-                          shampoo=SCFG if opt == "shampoo" else None)
+                          shampoo=SCFG if opt == "shampoo" else None, strategy=strategy)
     path = COLLECTIVE_NAMES[eng.info()["collectives"]]
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
@@ -81,8 +82,12 @@ def main():
         eng.step(OptimizerConfig())
         eng.sync()
         norms.append(eng.update_norms())
-    mine = {p.id: eng.read_param(p.id, "master").astype(np.float64)
-            for p in params if owners[p.id] == rank}
+    mine = {}
+    for p in params:  # whatever this rank owns under its strategy
+        try:
+            mine[p.id] = eng.read_param(p.id, "master").astype(np.float64)
+        except Exception:
+            pass
     replica = {p.id: eng.read_param(p.id, "replica") for p in params}
     if host:  # the replica the step copied out must equal the device replica
         off = 0
@@ -130,10 +135,10 @@ def main():
                      for g in gathered)
         good = e_w <= tol_w and e_n <= tol_n and rep_ok
         ok &= good
-        report[p.name] = {"owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
+        report[p.name] = {"plan_owner": int(owners[p.id]), "w": f"{e_w:.2e}", "norm": f"{e_n:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
     print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt,
-                      "bucket_ready": announce, "host_buffers": host, "ok": ok,
+                      "bucket_ready": announce, "host_buffers": host, "strategy": strategy, "ok": ok,
                       "params": report}))
     return 0 if ok else 1
 

@@ -74,6 +74,13 @@ def test_dp2_host_buffers_nvls_and_nccl():
         assert res["host_buffers"]
 
 
+@pytest.mark.parametrize("strategy", ["sc", "nv-layerwise"])
+def test_dp2_baseline_strategies_match_oracle(strategy):
+    # the paper's baselines executed for real: same trajectory as the oracle
+    res = _run(2, "multi_gpu_check.py", 2, "auto", "muon", "-", strategy)
+    assert res["strategy"] == strategy
+
+
 def test_dp2_shampoo_matches_spec():
     res = _run(2, "multi_gpu_check.py", 3, "auto", "shampoo")
     assert res["optimizer"] == "shampoo"
