@@ -45,6 +45,22 @@ struct NvlsState {
   bool devcomm_ok = false;
 };
 
+// Every rank learns whether every rank succeeded (min over ranks), so a
+// failure on one GPU makes all of them fall back together instead of
+// leaving the others blocked in a collective registration.
+bool agree(osh_ctx* ctx, bool ok) {
+  int32_t* d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(int32_t)) != cudaSuccess) return false;
+  const int32_t mine = ok ? 1 : 0;
+  int32_t all = 0;
+  bool good = cudaMemcpy(d, &mine, sizeof(mine), cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllReduce(d, d, 1, ncclInt32, ncclMin, ctx->comm, ctx->compute) == ncclSuccess &&
+              cudaStreamSynchronize(ctx->compute) == cudaSuccess &&
+              cudaMemcpy(&all, d, sizeof(all), cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(d);
+  return good && all == 1;
+}
+
 }  // namespace
 
 // Allocates grad / replica as symmetric multicast-capable buffers. Returns
@@ -66,31 +82,33 @@ osh_status nvls_setup(osh_ctx* ctx, size_t grad_bytes, size_t replica_bytes, boo
     if (required) return fail(OSH_ERR_UNSUPPORTED, "NVLS collectives unavailable: " + why);
     return OSH_OK;
   };
-  if (ncclMemAlloc(&ctx->grad, grad_bytes) != ncclSuccess) return give_up("ncclMemAlloc(grad)");
-  if (ncclMemAlloc(reinterpret_cast<void**>(&ctx->replica), replica_bytes) != ncclSuccess)
-    return give_up("ncclMemAlloc(replica)");
-  if (ncclCommWindowRegister(ctx->comm, ctx->grad, grad_bytes, &st->win_grad,
-                             NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess)
-    return give_up("window registration (grad)");
-  if (ncclCommWindowRegister(ctx->comm, ctx->replica, replica_bytes, &st->win_rep,
-                             NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess)
-    return give_up("window registration (replica)");
+  // each phase ends with an agreement so all ranks take the same branch
+  bool ok = ncclMemAlloc(&ctx->grad, grad_bytes) == ncclSuccess &&
+            ncclMemAlloc(reinterpret_cast<void**>(&ctx->replica), replica_bytes) == ncclSuccess;
+  if (!agree(ctx, ok)) return give_up("ncclMemAlloc on some rank");
+  ok = ncclCommWindowRegister(ctx->comm, ctx->grad, grad_bytes, &st->win_grad,
+                              NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess;
+  ok = ncclCommWindowRegister(ctx->comm, ctx->replica, replica_bytes, &st->win_rep,
+                              NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess && ok;
+  if (!agree(ctx, ok)) return give_up("symmetric window registration on some rank");
   ncclDevCommRequirements req;
   std::memset(&req, 0, sizeof(req));
   req.lsaMultimem = true;
-  if (ncclDevCommCreate(ctx->comm, &req, &st->devcomm) != ncclSuccess)
-    return give_up(std::string("ncclDevCommCreate(lsaMultimem): ") +
+  ok = ncclDevCommCreate(ctx->comm, &req, &st->devcomm) == ncclSuccess;
+  st->devcomm_ok = ok;
+  if (!agree(ctx, ok))
+    return give_up(std::string("ncclDevCommCreate(lsaMultimem) on some rank: ") +
                    ncclGetLastError(ctx->comm));
-  st->devcomm_ok = true;
   void** d_out = nullptr;
-  if (cudaMalloc(reinterpret_cast<void**>(&d_out), 2 * sizeof(void*)) != cudaSuccess)
-    return give_up("cudaMalloc");
-  multicast_base_kernel<<<1, 1>>>(st->win_grad, st->win_rep, st->devcomm, d_out);
   void* h[2] = {nullptr, nullptr};
-  const cudaError_t e = cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
-  cudaFree(d_out);
-  if (e != cudaSuccess || h[0] == nullptr || h[1] == nullptr)
-    return give_up("multicast pointer lookup failed");
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d_out), 2 * sizeof(void*));
+  if (e == cudaSuccess) {
+    multicast_base_kernel<<<1, 1>>>(st->win_grad, st->win_rep, st->devcomm, d_out);
+    e = cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d_out);
+  }
+  if (!agree(ctx, e == cudaSuccess && h[0] != nullptr && h[1] != nullptr))
+    return give_up("multicast pointer lookup failed on some rank");
   ctx->mc_grad = h[0];
   ctx->mc_replica = static_cast<__nv_bfloat16*>(h[1]);
   ctx->nvls_state = st;

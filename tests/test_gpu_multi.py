@@ -81,6 +81,14 @@ def test_dp2_baseline_strategies_match_oracle(strategy):
     assert res["strategy"] == strategy
 
 
+def test_dp2_bf16_gradients_both_paths():
+    # bf16 gradients: NVLS multimem.ld_reduce (bf16x8, fp32 accumulation in
+    # the switch) and NCCL's bf16 reduce against the fp64 oracle
+    for coll in ("auto", "nccl"):
+        res = _run(2, "multi_gpu_check.py", 2, coll, "muon", "-", "sharded", "bf16")
+        assert res["grad_dtype"] == "bf16"
+
+
 def test_dp2_shampoo_matches_spec():
     res = _run(2, "multi_gpu_check.py", 3, "auto", "shampoo")
     assert res["optimizer"] == "shampoo"
