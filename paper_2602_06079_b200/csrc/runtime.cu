@@ -232,6 +232,9 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
     ncclUniqueId id;
     std::memcpy(&id, tp_uid, sizeof(id));
     OSH_NCCL_TRY(ncclCommInitRank(&ctx->tp_comm, tp_size, id, tp_rank));
+    OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->tp_stream, cudaStreamNonBlocking));
+    OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_start_ev, cudaEventDisableTiming));
+    OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_done_ev, cudaEventDisableTiming));
   }
   *out = ctx.release();
   return OSH_OK;
@@ -318,6 +321,12 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   free_layout(ctx);
   if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
   if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);
+  if (ctx->tp_stream != nullptr) {
+    cudaStreamSynchronize(ctx->tp_stream);
+    cudaStreamDestroy(ctx->tp_stream);
+    cudaEventDestroy(ctx->tp_start_ev);
+    cudaEventDestroy(ctx->tp_done_ev);
+  }
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->compute);
   cudaStreamDestroy(ctx->comm_stream);

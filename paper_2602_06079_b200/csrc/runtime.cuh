@@ -99,6 +99,9 @@ struct osh_ctx {
   // the reference run_partitioned, verify.hpp:235-286)
   int tp_rank = 0, tp_size = 1;
   ncclComm_t tp_comm = nullptr;
+  cudaStream_t tp_stream = nullptr;       // TP gathers / scatters (overlap the group GEMMs)
+  cudaEvent_t tp_start_ev = nullptr, tp_done_ev = nullptr;
+  std::vector<cudaEvent_t> tp_gather_ev, tp_pack_ev;  // per micro group
   uint64_t tp_c_max = 268435456ull;  // 512 MiB of bf16 (optishard_cli.cpp:77-82,198)
   std::vector<optishard::ParamSpec> params_full;  // full shapes; `params` is the shard view
   struct TpItem {

@@ -84,7 +84,12 @@ void* grad_ptr(osh_ctx* ctx, int pid) {
 }
 
 void tp_free(osh_ctx* ctx) {
+  if (ctx->tp_stream != nullptr) cudaStreamSynchronize(ctx->tp_stream);
   ctx->tp_engines.clear();
+  for (cudaEvent_t e : ctx->tp_gather_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->tp_pack_ev) cudaEventDestroy(e);
+  ctx->tp_gather_ev.clear();
+  ctx->tp_pack_ev.clear();
   for (CopyTask* p : ctx->d_tp_unpack) cudaFree(p);
   for (CopyTask* p : ctx->d_tp_pack) cudaFree(p);
   ctx->d_tp_unpack.clear();
@@ -213,6 +218,12 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
       return st;
     ctx->tp_engines.push_back(std::move(eng));
   }
+  ctx->tp_gather_ev.assign(ctx->tp_groups, nullptr);
+  ctx->tp_pack_ev.assign(ctx->tp_groups, nullptr);
+  for (int g = 0; g < ctx->tp_groups; ++g) {
+    OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_gather_ev[g], cudaEventDisableTiming));
+    OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_pack_ev[g], cudaEventDisableTiming));
+  }
   for (int g = 0; g < ctx->tp_groups; ++g) {
     CopyTask* u = nullptr;
     CopyTask* p = nullptr;
@@ -227,6 +238,14 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
 osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
   const int T = ctx->tp_size, me = ctx->tp_rank;
   const size_t es = gsize(ctx);
+  // The TP transfers run on their own stream: all gathers are issued first
+  // (group order), the compute of group g waits only for gather g, and the
+  // scatter of group g follows its pack — so the gathers / scatters of other
+  // groups overlap the Newton-Schulz GEMMs. Every TP rank issues the same
+  // collective sequence on tp_comm (gathers 0..G-1, then scatters 0..G-1).
+  cudaStream_t ts = ctx->tp_stream;
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_start_ev, cs));
+  OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_start_ev, 0));
   for (int g = 0; g < ctx->tp_groups; ++g) {
     // ---- gather reduced-gradient shards to the hosts
     TP_NCCL(ncclGroupStart());
@@ -234,17 +253,21 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
       if (it.group != g) continue;
       const size_t shard = static_cast<size_t>(it.full_rows * it.full_cols / T);
       if (it.host != me) {
-        TP_NCCL(ncclSend(grad_ptr(ctx, it.pid), shard, gtype(ctx), it.host, ctx->tp_comm, cs));
+        TP_NCCL(ncclSend(grad_ptr(ctx, it.pid), shard, gtype(ctx), it.host, ctx->tp_comm, ts));
         continue;
       }
       for (int t = 0; t < T; ++t) {
         if (t == me) continue;
         uint8_t* dst = it.split_dim == 0 ? static_cast<uint8_t*>(it.g_full) + es * t * shard
                                          : it.stage + es * t * shard;
-        TP_NCCL(ncclRecv(dst, shard, gtype(ctx), t, ctx->tp_comm, cs));
+        TP_NCCL(ncclRecv(dst, shard, gtype(ctx), t, ctx->tp_comm, ts));
       }
     }
     TP_NCCL(ncclGroupEnd());
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_gather_ev[g], ts));
+  }
+  for (int g = 0; g < ctx->tp_groups; ++g) {
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
     OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
                                     ctx->tp_unpack_tiles[g], cs));
     // ---- full-matrix Muon on the host
@@ -254,6 +277,8 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
       if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
     OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
                                     ctx->tp_pack_tiles[g], cs));
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
     // ---- scatter updated bf16 shards into every rank's replica slot
     TP_NCCL(ncclGroupStart());
     for (osh_ctx::TpItem& it : ctx->tp_items) {
@@ -261,7 +286,7 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
       const size_t shard = static_cast<size_t>(it.full_rows * it.full_cols / T);
       if (it.host != me) {
         TP_NCCL(ncclRecv(ctx->replica + ctx->flat_off[it.pid], shard, ncclBfloat16, it.host,
-                         ctx->tp_comm, cs));
+                         ctx->tp_comm, ts));
         continue;
       }
       for (int t = 0; t < T; ++t) {
@@ -270,11 +295,13 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
                               ? static_cast<const void*>(it.rep_full + t * shard)
                               : static_cast<const void*>(reinterpret_cast<__nv_bfloat16*>(it.stage) +
                                                          t * shard);
-        TP_NCCL(ncclSend(src, shard, ncclBfloat16, t, ctx->tp_comm, cs));
+        TP_NCCL(ncclSend(src, shard, ncclBfloat16, t, ctx->tp_comm, ts));
       }
     }
     TP_NCCL(ncclGroupEnd());
   }
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ts));
+  OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_done_ev, 0));
   return OSH_OK;
 }
 
