@@ -37,7 +37,8 @@ cudaEvent_t OptimizerEngine::take_event() {
 }
 
 cudaError_t OptimizerEngine::timed_gemm(int mode, const NsProblemDesc* pd, int np, float alpha,
-                                        float beta, cudaStream_t s, const NsSchedule* sched) {
+                                        float beta, cudaStream_t s, const NsSchedule* sched,
+                                        float lr) {
   const bool rec = profile_ && timed_.size() < 100000;
   Timed t{};
   if (rec) {
@@ -54,7 +55,7 @@ cudaError_t OptimizerEngine::timed_gemm(int mode, const NsProblemDesc* pd, int n
     }
     cudaEventRecord(t.a, s);
   }
-  const cudaError_t err = ns_gemm_launch(mode, pd, np, alpha, beta, 0.f, s, sched);
+  const cudaError_t err = ns_gemm_launch(mode, pd, np, alpha, beta, lr, s, sched);
   if (rec) {
     cudaEventRecord(t.b, s);
     timed_.push_back(std::move(t));

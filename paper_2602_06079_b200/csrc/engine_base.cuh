@@ -88,7 +88,7 @@ class OptimizerEngine {
   cudaEvent_t take_event();
   // one grouped GEMM launch, timed when profiling, counted in stats_
   cudaError_t timed_gemm(int mode, const NsProblemDesc* pd, int np, float alpha, float beta,
-                         cudaStream_t s, const NsSchedule* sched = nullptr);
+                         cudaStream_t s, const NsSchedule* sched = nullptr, float lr = 0.f);
   template <typename F>
   cudaError_t timed_elementwise(int mode, double bytes, double elems, cudaStream_t s, F&& launch) {
     const bool rec = profile_ && timed_.size() < 100000;

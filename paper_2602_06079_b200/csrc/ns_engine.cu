@@ -281,6 +281,8 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
   OSH_CUDA_TRY(upload(&d_slot_tensor_, slot_tensor));
   // cost-balanced (LPT) tile schedules of the three GEMMs of every wave
+  const char* aux = std::getenv("OSH_NS_AUX");
+  fold_a_ = !(aux != nullptr && std::strcmp(aux, "1") == 0);
   const char* lpt = std::getenv("OSH_GEMM_LPT");
   lpt_ = !(lpt != nullptr && std::strcmp(lpt, "0") == 0);
   sched_symmetric_ = symmetric_;
@@ -381,14 +383,19 @@ osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
   for (int it = 0; it < cfg.ns_steps; ++it) {
     NsProblemDesc gram[kMaxProblems], poly[kMaxProblems], upd[kMaxProblems];
     problems(w, it, gram, poly, upd);
-    const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b) {
+    const auto timed_launch = [&](int mode, const NsProblemDesc* pd, float a, float b, float l) {
       const NsSchedule* sc = lpt_ && sched_symmetric_ == symmetric_ ? &w.sched[mode] : nullptr;
-      return timed_gemm(mode, pd, np, a, b, s, sc);
+      return timed_gemm(mode, pd, np, a, b, s, sc, l);
     };
-    cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f);
+    // B' = a I + b A + c A^2 in the POLY epilogue, X' = s B' X: the UPDATE
+    // epilogue then reads no aux (one fewer pass over X per iteration);
+    // OSH_NS_AUX=1 restores X' = s (a X + B X) with the aux read
+    cudaError_t e = timed_launch(kEpiGram, gram, 0.f, 0.f, 0.f);
     if (e == cudaSuccess)
-      e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b), static_cast<float>(cfg.ns_c));
-    if (e == cudaSuccess) e = timed_launch(kEpiUpdate, upd, static_cast<float>(cfg.ns_a), 0.f);
+      e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b), static_cast<float>(cfg.ns_c),
+                       fold_a_ ? static_cast<float>(cfg.ns_a) : 0.f);
+    if (e == cudaSuccess)
+      e = timed_launch(kEpiUpdate, upd, fold_a_ ? 0.f : static_cast<float>(cfg.ns_a), 0.f, 0.f);
     if (e != cudaSuccess)
       return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") + cudaGetErrorString(e));
   }

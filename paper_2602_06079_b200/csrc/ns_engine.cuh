@@ -106,6 +106,7 @@ class MuonEngine : public OptimizerEngine {
   bool symmetric_ = true;
   bool double_buffer_ = false;
   bool lpt_ = true;               // cost-balanced tile schedules (OSH_GEMM_LPT=0: striding)
+  bool fold_a_ = true;            // a*I folded into B (OSH_NS_AUX=1: aux read in UPDATE)
   bool sched_symmetric_ = true;   // symmetric_ when the schedules were built
   std::vector<int*> sched_mem_;
 };

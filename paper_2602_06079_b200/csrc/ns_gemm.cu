@@ -384,6 +384,12 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = P.alpha * v[j] + P.beta * __uint_as_float(r[j]);
+          // + lr * I (the Newton-Schulz 'a' folded into B, so UPDATE needs no aux read)
+          if (P.lr != 0.f && row >= col0 && row < col0 + 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j == row) v[j] += P.lr;
+          }
           if (pr.symmetric)
             store_row32_sym(pr.out + c.b * pr.out_bstride, pr.out_ld, row, col0, pr.N, v);
           else

@@ -33,7 +33,7 @@ constexpr int kMaxProblems = 4;
 
 enum NsEpilogue : int {
   kEpiGram = 0,    // out = s * acc                                  (bf16)
-  kEpiPoly = 1,    // out = alpha * aux + beta * acc                 (bf16)
+  kEpiPoly = 1,    // out = alpha * aux + beta * acc + lr * I         (bf16)
   kEpiUpdate = 2,  // out = s * (alpha * aux + acc)                  (bf16)
   kEpiFinal = 3,   // W -= lr * s * (alpha * aux + acc)              (fp32 master + replica)
   kEpiStat = 4,    // out32 = alpha * out32 + s * acc                (fp32 read-modify-write)

@@ -35,12 +35,18 @@ oa = torch.empty_like(a); ox = torch.empty_like(x)
 g = _lib.GemmProblem(); g.a = mref(x); g.b = mref(x); g.out = mref(oa)
 u = _lib.GemmProblem(); u.a = mref(a); u.b = mref(x); u.b_mn_major = 1; u.out = mref(ox); u.aux = mref(x)
 gs = _lib.GemmProblem(); gs.a = mref(x); gs.b = mref(x); gs.out = mref(oa); gs.symmetric = 1
+xt = x.transpose(1, 2).contiguous()
+uk = _lib.GemmProblem(); uk.a = mref(a); uk.b = mref(xt); uk.b_mn_major = 0; uk.out = mref(ox)
 F = 2.0 * bt * m * m * n
 res = {}
 for name, fn in [("ours_gram", lambda: run(0, g)), ("ours_update", lambda: run(2, u, 3.4445)),
+                 ("ours_update_noaux", lambda: run(2, u, 0.0)),
+                 ("ours_update_kmajor_b", lambda: run(2, uk, 0.0)),
                  ("ours_gram_sym(alg flops)", lambda: run(0, gs)),
                  ("cublas_gram", lambda: torch.matmul(x, x.transpose(1, 2), out=oa)),
                  ("cublas_update", lambda: torch.matmul(a, x, out=ox))]:
     tf, sm, pw = clocks_during(loop(fn, F), 4.0)
-    res[name] = {"tflops": round(tf, 1), "sm_mhz_median": sm, "power_w_median": pw}
+    res[name] = {"tflops": round(tf, 1), "sm_mhz_median": sm, "power_w_median": pw,
+                 "tflops_per_mhz": round(tf / sm, 4) if sm else None,
+                 "gflop_per_joule": round(tf * 1e3 / pw, 1) if pw else None}
 print(json.dumps(res, indent=1))

@@ -294,3 +294,21 @@ def test_poly_alpha_zero_skips_aux():
     run(1, [p], alpha=0.0, beta=2.0)  # aux is null: must not be read
     xf = x.float()
     assert relerr(out, 2.0 * xf @ xf.transpose(1, 2)) < 1e-2
+
+
+def test_poly_diagonal_add():
+    """POLY's lr * I term (the Newton-Schulz 'a' folded into B)."""
+    a = padded(2, 256, 256, scale=0.1)
+    a = ((a.float() + a.float().transpose(1, 2)) / 2).bfloat16().contiguous()
+    out = torch.zeros_like(a)
+    for sym in (1, 0):
+        p = _lib.GemmProblem()
+        p.a = mref(a)
+        p.b = mref(a)
+        p.out = mref(out)
+        p.aux = mref(a)
+        p.symmetric = sym
+        run(1, [p], alpha=B, beta=C, lr=A)
+        af = a.float()
+        ref = B * af + C * af @ af + A * torch.eye(256, device="cuda")
+        assert relerr(out, ref) < 1e-2
