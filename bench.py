@@ -45,7 +45,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)
-    ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--alpha", default="auto",
+                    help="alpha of the alpha-balanced plan, or 'auto': the alpha of {1, .75, .5, "
+                         ".25, 0} with the lowest planned per-rank NS-flop max/mean (ties keep 1)")
     ap.add_argument("--method", default="alpha-balanced",
                     choices=["alpha-balanced", "atomic-ownership"],
                     help="executable (atomic) partition; equal-chunk splits tensors, see "
@@ -237,6 +239,16 @@ def cpu_reference_step(params, plan, owners, ranks, threads=None):
 
 
 # ------------------------------------------------------------------ our arm
+def resolve_alpha(P, a, params, cap, ranks):
+    """--alpha auto: the planner's own choice (planner.choose_alpha)."""
+    a.alpha_auto = a.alpha == "auto"
+    if not a.alpha_auto:
+        return float(a.alpha)
+    if a.method != "alpha-balanced" or a.optimizer != "muon":
+        return 1.0
+    return P.choose_alpha(params, cap, ranks, a.cost)[0]
+
+
 def run_ours(a, dist: Dist):
     import numpy as np
     import torch
@@ -257,6 +269,7 @@ def run_ours(a, dist: Dist):
     view = P.apply_tp_sharding(params, T)     # the DP partition is over the TP shards
     cap = cfg.bucket_capacity // T
     t_plan = time.perf_counter()
+    a.alpha = resolve_alpha(P, a, view, cap, D)
     plan = P.plan_dp(view, cap, D, a.method, a.cost, a.alpha)
     plan_us = (time.perf_counter() - t_plan) * 1e6
     owners = P.param_owners(view, cap, plan)
@@ -408,6 +421,7 @@ def run_ours(a, dist: Dist):
     achieved = p0["flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
     achieved_exec = p0["exec_flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    alpha_src = " (auto: lowest planned NS-flop max/mean of {1,.75,.5,.25,0})" if a.alpha_auto else ""
     out = {
         "metric": METRIC if a.optimizer == "muon" else METRIC_SHAMPOO,
         "value": round(ms_max, 3),
@@ -424,7 +438,7 @@ def run_ours(a, dist: Dist):
         "config": {
             "workload": "qwen3-8b-like Muon step (L36 h4096 f12288 v151936: 183 tensors, "
                         f"{info['total_numel']} params, {info['n_buckets']} buckets cap {cap})",
-            "plan": (f"alpha-balanced alpha={a.alpha}" if a.method == "alpha-balanced"
+            "plan": (f"alpha-balanced alpha={a.alpha}{alpha_src}" if a.method == "alpha-balanced"
                      else a.method) + f" cost={a.cost}",
             "ranks": N, "ns_steps": 5, "grad_dtype": a.grad_dtype, "collectives": coll_path,
             "strategy": a.strategy,
@@ -500,6 +514,7 @@ def run_reference(a, dist: Dist):
     cfg = P.load_config(a.config)
     params = P.generate_transformer_params(cfg)
     N = dist.world
+    a.alpha = resolve_alpha(P, a, params, cfg.bucket_capacity, N)
     plan = P.plan_dp(params, cfg.bucket_capacity, N, a.method, a.cost, a.alpha)
     owners = P.param_owners(params, cfg.bucket_capacity, plan)
     threads = os.cpu_count()

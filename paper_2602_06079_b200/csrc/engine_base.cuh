@@ -61,6 +61,10 @@ class OptimizerEngine {
   virtual size_t workspace_bytes() const = 0;
   virtual int num_tensors() const = 0;
   virtual void set_symmetric(bool) {}
+  // Waves may run in any order (no bucket-ordered collective or host copy
+  // depends on it): build() then puts small waves first and last, so the
+  // exposed momentum of the first wave and update of the last are short.
+  virtual void set_wave_reorder(bool) {}
   // Optimizer state beyond the per-tensor master / momentum (checkpointing):
   // a device buffer whose layout is a pure function of the tensors and the
   // configuration, plus the engine's step counter.

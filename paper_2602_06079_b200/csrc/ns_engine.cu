@@ -105,7 +105,9 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   // momentum can run while wave w's GEMMs still read theirs
   double_buffer_ = double_buffer && largest <= budget / 2;
   size_t cap = double_buffer_ ? budget / 2 : budget;
-  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total_ws + min_waves - 1) / min_waves));
+  // a matrix larger than the wave target (a vocabulary matrix of a rank that
+  // owns few others) forms a wave of its own; the rest keep the target size
+  if (min_waves > 1) cap = std::min(cap, (total_ws + min_waves - 1) / min_waves);
 
   std::vector<std::vector<int>> wave_members(1);
   std::vector<std::vector<std::pair<int, int>>> wave_classes(1);
@@ -134,6 +136,25 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   }
   if (wave_members.back().empty()) wave_members.pop_back();
   half = (std::max(half, used) + 1023) / 1024 * 1024;
+  if (reorder_ && wave_members.size() >= 3) {
+    // The overlapped schedule exposes the momentum of the first wave and the
+    // update of the last one (runtime.cu run_waves_local): run the smallest
+    // wave first and the second smallest last, the rest in bucket order.
+    std::vector<double> elems(wave_members.size(), 0.0);
+    for (size_t wi = 0; wi < wave_members.size(); ++wi)
+      for (const int ti : wave_members[wi])
+        elems[wi] += static_cast<double>(tensors[ti].rows) * tensors[ti].cols;
+    std::vector<size_t> idx(wave_members.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return elems[a] < elems[b]; });
+    const size_t first = idx[0], last = idx[1];
+    std::vector<std::vector<int>> ordered;
+    ordered.push_back(wave_members[first]);
+    for (size_t wi = 0; wi < wave_members.size(); ++wi)
+      if (wi != first && wi != last) ordered.push_back(wave_members[wi]);
+    ordered.push_back(wave_members[last]);
+    wave_members.swap(ordered);
+  }
 
   // ---- chunks (one per class per wave), slots, tables
   std::vector<MomentumMatrixTask> mtasks;

@@ -64,6 +64,7 @@ class MuonEngine : public OptimizerEngine {
   int num_tensors() const override { return n_tensors_; }
 
   void set_symmetric(bool on) override { symmetric_ = on; }
+  void set_wave_reorder(bool on) override { reorder_ = on; }
 
  private:
   struct Chunk {
@@ -105,6 +106,7 @@ class MuonEngine : public OptimizerEngine {
   MomentumVectorTask* d_vtasks_ = nullptr;
   bool symmetric_ = true;
   bool double_buffer_ = false;
+  bool reorder_ = false;          // small waves first and last (set_wave_reorder)
   bool lpt_ = true;               // cost-balanced tile schedules (OSH_GEMM_LPT=0: striding)
   bool fold_a_ = true;            // a*I folded into B (OSH_NS_AUX=1: aux read in UPDATE)
   bool sched_symmetric_ = true;   // symmetric_ when the schedules were built

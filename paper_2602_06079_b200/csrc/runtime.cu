@@ -555,9 +555,41 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
                   : ctx->overlap ? 8 : (reduce_out && ctx->tp_size == 1) ? 4 : 1;
   if (const char* mw = std::getenv("OSH_MIN_WAVES"); mw != nullptr && std::atoi(mw) > 0)
     min_waves = std::atoi(mw);
+  // waves in any order where nothing bucket-ordered waits on them: one rank,
+  // or NVLS (the step barrier covers every bucket; collectives are inside the
+  // kernels). NCCL RS-v / AG-v, SC / NV-layerwise and TP keep bucket order.
+  const char* ro = std::getenv("OSH_WAVE_REORDER");
+  const bool reorder = ctx->tp_size == 1 && ctx->strategy == OSH_STRAT_SHARDED &&
+                       (!distributed(ctx) || ctx->nvls) && !(ro != nullptr && std::strcmp(ro, "0") == 0);
+  ctx->engine->set_wave_reorder(reorder);
   if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves, ctx->overlap);
       st != OSH_OK)
     return st;
+  {
+    const int nw = ctx->engine->num_waves();
+    const int nbk = static_cast<int>(ctx->cuts.size());
+    std::vector<int> done_at(static_cast<size_t>(nbk), -1);
+    ctx->h2d_bucket_order.clear();
+    std::vector<char> queued(static_cast<size_t>(nbk), 0);
+    for (int w = 0; w < nw; ++w)
+      for (int b = ctx->engine->wave_first_bucket(w); b <= ctx->engine->wave_last_bucket(w); ++b) {
+        done_at[static_cast<size_t>(b)] = std::max(done_at[static_cast<size_t>(b)], w);
+        if (!queued[static_cast<size_t>(b)]) {
+          queued[static_cast<size_t>(b)] = 1;
+          ctx->h2d_bucket_order.push_back(b);
+        }
+      }
+    for (int b = 0; b < nbk; ++b)
+      if (!queued[static_cast<size_t>(b)]) ctx->h2d_bucket_order.push_back(b);
+    if (!reorder || distributed(ctx))  // NCCL RS-v waits per bucket in bucket order
+      for (int b = 0; b < nbk; ++b) ctx->h2d_bucket_order[static_cast<size_t>(b)] = b;
+    ctx->wave_final_upto.assign(static_cast<size_t>(nw), -1);
+    for (int w = 0; w < nw; ++w) {
+      int upto = -1;
+      while (upto + 1 < nbk && done_at[static_cast<size_t>(upto + 1)] <= w) ++upto;
+      ctx->wave_final_upto[static_cast<size_t>(w)] = upto;
+    }
+  }
   ctx->overlap = ctx->overlap && ctx->engine->double_buffered() && ctx->engine->num_waves() > 1;
   if (ctx->tp_size > 1)
     if (osh_status st = osh::tp_setup(ctx, static_cast<int64_t>(budget)); st != OSH_OK) return st;
@@ -780,7 +812,7 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   // after wave w every bucket before the next wave's first one is final
   auto wave_done = [&](int w) -> osh_status {
     OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-    return d2h_buckets(ctx, io, w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1,
+    return d2h_buckets(ctx, io, w + 1 < nw ? ctx->wave_final_upto[static_cast<size_t>(w)] : nb - 1,
                        ctx->wave_end[w]);
   };
   if (!ctx->overlap) {
@@ -847,7 +879,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   } else if (host_grads != nullptr && pipelined) {
     io.h2d = true;
     OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
-    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
+    for (const int b : ctx->h2d_bucket_order) {  // the order the waves need them
       const size_t off = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->bucket_base[b]);
       const size_t len = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->layout.buckets[b].numel);
       OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->grad) + off,

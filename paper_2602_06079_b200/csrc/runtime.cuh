@@ -77,6 +77,12 @@ struct osh_ctx {
   // high-priority gemm_stream (double-buffered NS workspace)
   bool overlap = false;
   std::vector<cudaEvent_t> pre_ev, ns_ev;  // per wave
+  // waves may run out of bucket order (single rank / NVLS, MuonEngine
+  // set_wave_reorder): per wave, the last bucket index B such that every
+  // bucket <= B is final once the wave is done; and the order in which a
+  // single rank's pipelined H2D copies the buckets (first need first)
+  std::vector<int> wave_final_upto;
+  std::vector<int> h2d_bucket_order;
   // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
   // the update kernels reduce / broadcast through their multicast addresses
   int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
