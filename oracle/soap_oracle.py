@@ -1,0 +1,168 @@
+"""fp64 oracle of the BUILDER-DEFINED blocked SOAP step (TEST INFRASTRUCTURE ONLY).
+
+The reference has no SOAP mathematics — only its planning cost
+(proj/include/optishard/cost.hpp:47-48,68-75; SPEC.md:8 puts optimizer
+internals out of scope), so parity is UNPINNED against the reference: this
+file is the specification the GPU path (paper_2602_06079_b200/csrc/soap*.cu)
+is checked against, written in plain numpy fp64 from the published algorithm
+(Vyas et al. 2024, "SOAP: Improving and Stabilizing Shampoo using Adam",
+Algorithm 3: Adam in the eigenbasis of Shampoo's preconditioner, the basis
+refreshed every `precond_every` steps by one step of power iteration + QR).
+
+Per 2-D tensor that is not vocabulary-space (SURVEY.md §8 A19 policy), the
+tensor W is cut into blocks of at most `block` rows and columns (ragged last
+blocks). For each block with gradient G (p x q), at step s (t = s + 1):
+
+    L <- bs L + (1 - bs) G G^T        R <- bs R + (1 - bs) G^T G      (fp32 state)
+    if s % precond_every == 0:        for (S, Q) in ((L, Q_L), (R, Q_R)):
+        c = shift * ||S||_F           (c == 0: the basis is kept)
+        Y = S Q + c Q                 est_j = (Q^T Y)_jj
+        order = stable argsort of -est
+        Q <- qr(Y[:, order])          (R with a positive diagonal)
+        V <- V[order, :] (L side) / V[:, order] (R side)
+    G' = Q_L^T G Q_R
+    M  <- b1 M + (1 - b1) G                           (original space)
+    V  <- b2 V + (1 - b2) G'^2                        (eigenbasis)
+    N' = (Q_L^T M Q_R / (1 - b1^t)) / (sqrt(V / (1 - b2^t)) + eps)
+    W  <- W - lr * Q_L N' Q_R^T
+
+Q_L, Q_R start as the identity; the first refresh (s = 0) runs
+`init_iters` power-iteration steps instead of one (V is still 0 then, so the
+permutations are free). The shift keeps the power iteration well defined
+when S is rank deficient (non-square blocks, early steps): the columns of Q
+in S's null space stay the previous basis, orthogonalised against the range,
+instead of being whatever rounding noise a QR of a singular matrix returns —
+this is what makes the basis a deterministic function of the inputs on both
+the fp64 oracle and the fp32 GPU path.
+
+Vectors and vocabulary-space matrices: elementwise Adam with the same b1,
+b2, eps and bias correction.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+
+@dataclass
+class SoapConfig:
+    lr: float = 0.02
+    beta1: float = 0.9
+    beta2: float = 0.95
+    shampoo_beta: float = 0.95
+    eps: float = 1e-8
+    block: int = 1024
+    precond_every: int = 10
+    init_iters: int = 4
+    shift: float = 1e-3
+
+
+def blocks(rows: int, cols: int, b: int) -> List[Tuple[int, int, int, int]]:
+    """(r0, p, c0, q) of every block, row-major block order."""
+    out = []
+    for r0 in range(0, rows, b):
+        for c0 in range(0, cols, b):
+            out.append((r0, min(b, rows - r0), c0, min(b, cols - c0)))
+    return out
+
+
+def qr_pos(y: np.ndarray) -> np.ndarray:
+    """Q of y = Q R with diag(R) >= 0 (the QR the GPU's CholeskyQR2 returns)."""
+    q, r = np.linalg.qr(y)
+    d = np.sign(np.diag(r))
+    d[d == 0] = 1.0
+    return q * d
+
+
+def refresh_basis(s: np.ndarray, q: np.ndarray, cfg: SoapConfig, iters: int
+                  ) -> Tuple[np.ndarray, np.ndarray]:
+    """One (or `iters`) shifted power-iteration steps; returns (Q, order of
+    the LAST step) — the permutation V must follow."""
+    n = s.shape[0]
+    order = np.arange(n)
+    c = cfg.shift * float(np.linalg.norm(s))
+    if c == 0.0:
+        return q, order
+    for _ in range(iters):
+        y = s @ q + c * q
+        est = np.einsum("ij,ij->j", q, y)
+        order = np.argsort(-est, kind="stable")
+        q = qr_pos(y[:, order])
+    return q, order
+
+
+class SoapTensorState:
+    def __init__(self, shape, cfg: SoapConfig, preconditioned: bool):
+        self.shape = tuple(shape)
+        self.m = np.zeros(self.shape)
+        self.v = np.zeros(self.shape)  # vectors / vocabulary matrices (elementwise Adam)
+        self.pre = preconditioned
+        self.blocks = blocks(self.shape[0], self.shape[1], cfg.block) if preconditioned else []
+        self.L = [np.zeros((p, p)) for (_, p, _, q) in self.blocks]
+        self.R = [np.zeros((q, q)) for (_, p, _, q) in self.blocks]
+        self.QL = [np.eye(p) for (_, p, _, q) in self.blocks]
+        self.QR = [np.eye(q) for (_, p, _, q) in self.blocks]
+        self.V = [np.zeros((p, q)) for (_, p, _, q) in self.blocks]
+
+
+def soap_apply(st: SoapTensorState, cfg: SoapConfig, w: np.ndarray, g: np.ndarray,
+               step: int) -> float:
+    """In place on w and the state; returns ||W_new - W_old||_F."""
+    g = np.asarray(g, dtype=np.float64).reshape(st.shape)
+    t = step + 1
+    bc1, bc2 = 1.0 - cfg.beta1 ** t, 1.0 - cfg.beta2 ** t
+    st.m = cfg.beta1 * st.m + (1.0 - cfg.beta1) * g
+    if not st.pre:
+        st.v = cfg.beta2 * st.v + (1.0 - cfg.beta2) * g * g
+        upd = cfg.lr * (st.m / bc1) / (np.sqrt(st.v / bc2) + cfg.eps)
+        w -= upd
+        return float(np.linalg.norm(upd))
+    upd = np.zeros(st.shape)
+    bs = cfg.shampoo_beta
+    for k, (r0, p, c0, q) in enumerate(st.blocks):
+        gb = g[r0:r0 + p, c0:c0 + q]
+        st.L[k] = bs * st.L[k] + (1.0 - bs) * (gb @ gb.T)
+        st.R[k] = bs * st.R[k] + (1.0 - bs) * (gb.T @ gb)
+        if step % cfg.precond_every == 0:
+            iters = cfg.init_iters if step == 0 else 1
+            st.QL[k], ol = refresh_basis(st.L[k], st.QL[k], cfg, iters)
+            st.QR[k], orr = refresh_basis(st.R[k], st.QR[k], cfg, iters)
+            st.V[k] = st.V[k][ol, :][:, orr]
+        ql, qr = st.QL[k], st.QR[k]
+        gp = ql.T @ gb @ qr
+        st.V[k] = cfg.beta2 * st.V[k] + (1.0 - cfg.beta2) * gp * gp
+        mp = ql.T @ st.m[r0:r0 + p, c0:c0 + q] @ qr
+        n_rot = (mp / bc1) / (np.sqrt(st.V[k] / bc2) + cfg.eps)
+        upd[r0:r0 + p, c0:c0 + q] = cfg.lr * (ql @ n_rot @ qr.T)
+    w -= upd
+    return float(np.linalg.norm(upd))
+
+
+def is_preconditioned(p) -> bool:
+    """SURVEY.md §8 A19 policy: 2-D, not vocabulary-space."""
+    return len(p.shape) == 2 and not p.vocab_space
+
+
+def run(params, cfg: SoapConfig, steps: int, seed: int, contributors: int = 1,
+        init=None, grad=None) -> Tuple[Dict[int, np.ndarray], List[np.ndarray]]:
+    """Replicated trajectory over `params` (planner ParamSpecs) with the
+    reference generator's inputs (oracle.init_weight / reduced_gradient)."""
+    from oracle import oracle as O
+    init = init or (lambda p: O.init_weight(p.shape, p.id, seed).reshape(_shape2(p)))
+    grad = grad or (lambda p, s: O.reduced_gradient(p.shape, p.id, seed, s, contributors)
+                    .reshape(_shape2(p)))
+    w = {p.id: init(p).astype(np.float64) for p in params}
+    st = {p.id: SoapTensorState(_shape2(p), cfg, is_preconditioned(p)) for p in params}
+    norms = []
+    for s in range(steps):
+        n = np.zeros(len(params))
+        for p in params:
+            n[p.id] = soap_apply(st[p.id], cfg, w[p.id], grad(p, s), s)
+        norms.append(n)
+    return w, norms
+
+
+def _shape2(p):
+    return tuple(p.shape) if len(p.shape) == 2 else (p.shape[0], 1)
