@@ -58,8 +58,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workspace-gb", type=float, default=0.0)
-    ap.add_argument("--optimizer", default="muon", choices=["muon", "shampoo"],
-                    help="muon = the headline metric; shampoo = builder-defined blocked Shampoo")
+    ap.add_argument("--optimizer", default="muon", choices=["muon", "shampoo", "soap"],
+                    help="muon = the headline metric; shampoo / soap = builder-defined blocked "
+                         "Shampoo / SOAP")
     ap.add_argument("--shampoo-block", type=int, default=1024)
     ap.add_argument("--precond-every", type=int, default=10)
     ap.add_argument("--strategy", default="sharded", choices=["sharded", "sc", "nv-layerwise"],
@@ -255,7 +256,7 @@ def run_ours(a, dist: Dist):
 
     from paper_2602_06079_b200 import planner as P
     from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,
-                                              ShampooConfig, nccl_unique_id)
+                                              ShampooConfig, SoapConfig, nccl_unique_id)
 
     N = dist.world
     T = a.tp
@@ -286,7 +287,9 @@ def run_ours(a, dist: Dist):
                           tp_uid=tp_uid, tp_capacity=a.tp_cmax if T > 1 else None,
                           collectives=a.collectives, optimizer=a.optimizer, strategy=a.strategy,
                           shampoo=(ShampooConfig(block=a.shampoo_block, precond_every=a.precond_every)
-                                   if a.optimizer == "shampoo" else None))
+                                   if a.optimizer == "shampoo" else
+                                   SoapConfig(block=a.shampoo_block, precond_every=a.precond_every)
+                                   if a.optimizer == "soap" else None))
     info = eng.info()
     coll_path = COLLECTIVE_NAMES[info["collectives"]]
     eng.fill_synthetic(42, "weights")
@@ -340,7 +343,7 @@ def run_ours(a, dist: Dist):
     last = eng.timing()
     clock = clocks.stop(torch.cuda.device_count()) if clocks else None
     refresh_ms, refresh_modes = None, None
-    if a.optimizer == "shampoo":
+    if a.optimizer in ("shampoo", "soap"):
         # the timed steps avoid the root refresh (step index % precond_every != 0
         # when warmup + steps < precond_every); time one refresh step on its own
         done = a.warmup + a.steps
@@ -401,7 +404,7 @@ def run_ours(a, dist: Dist):
            "ns_flops": (info["ns_flops_per_iter"] * 5 if a.optimizer == "muon"
                         else float(last["gemm_flops"])),
            "refresh_ms": refresh_ms,
-           "refresh_modes": refresh_modes if a.optimizer == "shampoo" else None}
+           "refresh_modes": refresh_modes if a.optimizer != "muon" else None}
     allrec = dist.gather(rec)
     eng.close()
     if dist.rank != 0:
@@ -423,7 +426,8 @@ def run_ours(a, dist: Dist):
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     alpha_src = " (auto: lowest planned NS-flop max/mean of {1,.75,.5,.25,0})" if a.alpha_auto else ""
     out = {
-        "metric": METRIC if a.optimizer == "muon" else METRIC_SHAMPOO,
+        "metric": (METRIC if a.optimizer == "muon" else METRIC_SHAMPOO if a.optimizer == "shampoo"
+                   else METRIC_SHAMPOO.replace("Shampoo", "SOAP")),
         "value": round(ms_max, 3),
         "unit": "ms",
         "n_gpus": N,
@@ -487,6 +491,14 @@ def run_ours(a, dist: Dist):
         out["e2e"] = {"value": round(e, 3), "unit": "ms",
                       "h2d_bytes_per_step": allrec[0]["e2e"]["h2d"],
                       "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"]}
+    if a.optimizer == "soap":
+        rms = max(r["refresh_ms"] for r in allrec)
+        out["soap"] = {"block": a.shampoo_block, "precond_every": a.precond_every,
+                       "refresh_step_ms": round(rms, 3),
+                       "refresh_by_mode_rank0": allrec[0]["refresh_modes"],
+                       "amortized_step_ms": round(ms_max + (rms - ms_max) / a.precond_every, 3),
+                       "note": "value = a step without the eigenbasis refresh; the refresh step "
+                               "(power iteration + CholeskyQR2) is timed separately"}
     if a.optimizer == "shampoo":
         rms = max(r["refresh_ms"] for r in allrec)
         out["shampoo"] = {"block": a.shampoo_block, "precond_every": a.precond_every,

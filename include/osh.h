@@ -252,7 +252,14 @@ osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode);
  *                    it: cost.hpp:47-48,68-75 — specification and fp64 oracle
  *                    in oracle/shampoo_oracle.py). osh_step's osh_muon_cfg
  *                    supplies lr and beta (= beta1, momentum); ns_* are unused.
- * Shampoo needs tp_size == 1. */
+ *   OSH_OPT_SOAP     builder-defined blocked SOAP (Adam in the eigenbasis of
+ *                    Shampoo's statistics, basis refreshed by shifted power
+ *                    iteration + CholeskyQR2; oracle/soap_oracle.py). The
+ *                    osh_shampoo_cfg fields read: beta2 (second moment and
+ *                    statistics decay, 0.95), eps (Adam epsilon, 1e-8), block,
+ *                    precond_every, newton_iters = power iterations of the
+ *                    first refresh (4). osh_muon_cfg supplies lr and beta1.
+ * Shampoo and SOAP need tp_size == 1. */
 typedef struct osh_shampoo_cfg {
   double beta2;           /* statistics decay (0.95) */
   double eps;             /* relative regularisation of the roots (1e-4) */
@@ -261,7 +268,7 @@ typedef struct osh_shampoo_cfg {
   int32_t newton_iters;   /* coupled-Newton iterations per root (16) */
   int32_t reserved;
 } osh_shampoo_cfg;
-enum { OSH_OPT_MUON = 0, OSH_OPT_SHAMPOO = 1 };
+enum { OSH_OPT_MUON = 0, OSH_OPT_SHAMPOO = 1, OSH_OPT_SOAP = 2 };
 
 /* Data-parallel optimizer strategy (simulate.hpp:33-39 made executable, the
  * paper's baselines measured on the GPU). Call before

@@ -11,32 +11,41 @@ refreshed every `precond_every` steps by one step of power iteration + QR).
 
 Per 2-D tensor that is not vocabulary-space (SURVEY.md §8 A19 policy), the
 tensor W is cut into blocks of at most `block` rows and columns (ragged last
-blocks). For each block with gradient G (p x q), at step s (t = s + 1):
+blocks). Step order follows the published implementation (Vyas et al.,
+github.com/nikhilvyas/SOAP, soap.py): the FIRST call only accumulates the
+statistics and computes the initial basis (no parameter, momentum or second
+moment update); every later call s = 1, 2, ... first takes the Adam step in
+the current basis and then updates the statistics, refreshing the basis
+every `precond_every` calls. For each block with gradient G (p x q):
 
-    L <- bs L + (1 - bs) G G^T        R <- bs R + (1 - bs) G^T G      (fp32 state)
-    if s % precond_every == 0:        for (S, Q) in ((L, Q_L), (R, Q_R)):
-        c = shift * ||S||_F           (c == 0: the basis is kept)
-        Y = S Q + c Q                 est_j = (Q^T Y)_jj
-        order = stable argsort of -est
-        Q <- qr(Y[:, order])          (R with a positive diagonal)
-        V <- V[order, :] (L side) / V[:, order] (R side)
-    G' = Q_L^T G Q_R
-    M  <- b1 M + (1 - b1) G                           (original space)
-    V  <- b2 V + (1 - b2) G'^2                        (eigenbasis)
-    N' = (Q_L^T M Q_R / (1 - b1^t)) / (sqrt(V / (1 - b2^t)) + eps)
-    W  <- W - lr * Q_L N' Q_R^T
+    s == 0:
+        L = (1 - bs) G G^T ;  R = (1 - bs) G^T G
+        Q_L, Q_R <- refresh(L, I), refresh(R, I)   (init_iters iterations)
+    s >= 1 (t = s):
+        G' = Q_L^T G Q_R
+        M  <- b1 M + (1 - b1) G                           (original space)
+        V  <- b2 V + (1 - b2) G'^2                        (eigenbasis)
+        N' = (Q_L^T M Q_R / (1 - b1^t)) / (sqrt(V / (1 - b2^t)) + eps)
+        W  <- W - lr * Q_L N' Q_R^T
+        L  <- bs L + (1 - bs) G G^T ;  R <- bs R + (1 - bs) G^T G   (fp32 state)
+        if s % precond_every == 0:   Q_L, Q_R <- refresh (one iteration),
+                                     V <- V[order_L, :][:, order_R]
 
-Q_L, Q_R start as the identity; the first refresh (s = 0) runs
-`init_iters` power-iteration steps instead of one (V is still 0 then, so the
-permutations are free). The shift keeps the power iteration well defined
-when S is rank deficient (non-square blocks, early steps): the columns of Q
-in S's null space stay the previous basis, orthogonalised against the range,
-instead of being whatever rounding noise a QR of a singular matrix returns —
-this is what makes the basis a deterministic function of the inputs on both
-the fp64 oracle and the fp32 GPU path.
+refresh(S, Q), `iters` times:
+    c = shift * ||S||_F           (c == 0: the basis is kept)
+    Y = S Q + c Q                 est_j = (Q^T Y)_jj
+    order = stable argsort of -est
+    Q <- qr(Y[:, order])          (R with a positive diagonal)
+
+The shift keeps the power iteration well defined when S is rank deficient
+(non-square blocks, early steps): the columns of Q in S's null space stay
+the previous basis, orthogonalised against the range, instead of whatever
+rounding noise a QR of a singular matrix returns — this is what makes the
+basis a deterministic function of the inputs on both the fp64 oracle and
+the fp32 GPU path.
 
 Vectors and vocabulary-space matrices: elementwise Adam with the same b1,
-b2, eps and bias correction.
+b2, eps and bias correction (also skipped on the first call).
 """
 from __future__ import annotations
 
@@ -107,11 +116,35 @@ class SoapTensorState:
         self.V = [np.zeros((p, q)) for (_, p, _, q) in self.blocks]
 
 
+def _bf16(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bfloat16 (ties to even), returned as float64."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
 def soap_apply(st: SoapTensorState, cfg: SoapConfig, w: np.ndarray, g: np.ndarray,
-               step: int) -> float:
-    """In place on w and the state; returns ||W_new - W_old||_F."""
+               step: int, emulate_bf16: bool = False) -> float:
+    """In place on w and the state; returns ||W_new - W_old||_F.
+
+    emulate_bf16: round where the GPU path stores plain bf16 — the
+    back-projection operands and intermediates (Q_L, Q_R, N', T3, N); the
+    statistics and the projections G', M' run in bf16x3 there (fp32-level,
+    treated as exact here). A precision model of the GPU, used to separate
+    implementation errors from the rounding the fp64 comparison measures."""
+    r = _bf16 if emulate_bf16 else (lambda x: x)
     g = np.asarray(g, dtype=np.float64).reshape(st.shape)
-    t = step + 1
+    bs = cfg.shampoo_beta
+    if step == 0:  # statistics and the initial basis only
+        for k, (r0, p, c0, q) in enumerate(st.blocks):
+            gs = g[r0:r0 + p, c0:c0 + q]
+            st.L[k] = (1.0 - bs) * (gs @ gs.T)
+            st.R[k] = (1.0 - bs) * (gs.T @ gs)
+            st.QL[k], _ = refresh_basis(st.L[k], st.QL[k], cfg, cfg.init_iters)
+            st.QR[k], _ = refresh_basis(st.R[k], st.QR[k], cfg, cfg.init_iters)
+        return 0.0
+    t = step
     bc1, bc2 = 1.0 - cfg.beta1 ** t, 1.0 - cfg.beta2 ** t
     st.m = cfg.beta1 * st.m + (1.0 - cfg.beta1) * g
     if not st.pre:
@@ -120,22 +153,20 @@ def soap_apply(st: SoapTensorState, cfg: SoapConfig, w: np.ndarray, g: np.ndarra
         w -= upd
         return float(np.linalg.norm(upd))
     upd = np.zeros(st.shape)
-    bs = cfg.shampoo_beta
     for k, (r0, p, c0, q) in enumerate(st.blocks):
-        gb = g[r0:r0 + p, c0:c0 + q]
-        st.L[k] = bs * st.L[k] + (1.0 - bs) * (gb @ gb.T)
-        st.R[k] = bs * st.R[k] + (1.0 - bs) * (gb.T @ gb)
-        if step % cfg.precond_every == 0:
-            iters = cfg.init_iters if step == 0 else 1
-            st.QL[k], ol = refresh_basis(st.L[k], st.QL[k], cfg, iters)
-            st.QR[k], orr = refresh_basis(st.R[k], st.QR[k], cfg, iters)
-            st.V[k] = st.V[k][ol, :][:, orr]
+        gs = g[r0:r0 + p, c0:c0 + q]
         ql, qr = st.QL[k], st.QR[k]
-        gp = ql.T @ gb @ qr
+        gp = ql.T @ gs @ qr
         st.V[k] = cfg.beta2 * st.V[k] + (1.0 - cfg.beta2) * gp * gp
         mp = ql.T @ st.m[r0:r0 + p, c0:c0 + q] @ qr
-        n_rot = (mp / bc1) / (np.sqrt(st.V[k] / bc2) + cfg.eps)
-        upd[r0:r0 + p, c0:c0 + q] = cfg.lr * (ql @ n_rot @ qr.T)
+        n_rot = r((mp / bc1) / (np.sqrt(st.V[k] / bc2) + cfg.eps))
+        upd[r0:r0 + p, c0:c0 + q] = cfg.lr * r(r(r(ql) @ n_rot) @ r(qr).T)
+        st.L[k] = bs * st.L[k] + (1.0 - bs) * (gs @ gs.T)
+        st.R[k] = bs * st.R[k] + (1.0 - bs) * (gs.T @ gs)
+        if step % cfg.precond_every == 0:
+            st.QL[k], ol = refresh_basis(st.L[k], st.QL[k], cfg, 1)
+            st.QR[k], orr = refresh_basis(st.R[k], st.QR[k], cfg, 1)
+            st.V[k] = st.V[k][ol, :][:, orr]
     w -= upd
     return float(np.linalg.norm(upd))
 

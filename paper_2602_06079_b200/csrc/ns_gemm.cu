@@ -137,6 +137,18 @@ __device__ __forceinline__ void store_row32(__nv_bfloat16* dst, int col0, int n,
 // All loads are issued before any store (no load-after-store chain).
 __device__ __forceinline__ void rmw_row32(float* dst, int col0, int n, float alpha,
                                           const float (&v)[32]) {
+  if (alpha == 0.f) {  // plain fp32 store (no read of the previous value)
+    if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < n) dst[j] = v[j];
+    }
+    return;
+  }
   if (col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     float4* d4 = reinterpret_cast<float4*>(dst);
     float4 o[8];

@@ -292,10 +292,10 @@ osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out) {
 
 osh_status osh_ctx_set_optimizer(osh_ctx* ctx, int32_t kind, const osh_shampoo_cfg* cfg) {
   if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
-  if (kind != OSH_OPT_MUON && kind != OSH_OPT_SHAMPOO)
+  if (kind != OSH_OPT_MUON && kind != OSH_OPT_SHAMPOO && kind != OSH_OPT_SOAP)
     return osh::fail(OSH_ERR_ARG, "unknown optimizer");
-  if (kind == OSH_OPT_SHAMPOO && ctx->tp_size > 1)
-    return osh::fail(OSH_ERR_UNSUPPORTED, "Shampoo runs with tp_size == 1");
+  if (kind != OSH_OPT_MUON && ctx->tp_size > 1)
+    return osh::fail(OSH_ERR_UNSUPPORTED, "Shampoo / SOAP run with tp_size == 1");
   ctx->optimizer = kind;
   if (cfg != nullptr) {
     if (cfg->block < 64 || cfg->block % 64 != 0 || cfg->precond_every < 1 ||
@@ -545,8 +545,17 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     cudaMemGetInfo(&free_b, &total_b);
     budget = std::min<size_t>(24ull << 30, free_b / 3);
   }
-  if (ctx->optimizer == OSH_OPT_SHAMPOO)
+  if (ctx->optimizer == OSH_OPT_SHAMPOO) {
     ctx->engine = std::make_unique<osh::ShampooEngine>(ctx->shampoo);
+  } else if (ctx->optimizer == OSH_OPT_SOAP) {
+    osh::SoapConfig sc;  // osh_shampoo_cfg fields: newton_iters = init_iters
+    sc.beta2 = ctx->shampoo.beta2;
+    sc.eps = ctx->shampoo.eps;
+    sc.block = ctx->shampoo.block;
+    sc.precond_every = ctx->shampoo.precond_every;
+    sc.init_iters = ctx->shampoo.newton_iters;
+    ctx->engine = std::make_unique<osh::SoapEngine>(sc);
+  }
   else
     ctx->engine = std::make_unique<osh::MuonEngine>();
   const char* ov = std::getenv("OSH_OVERLAP");

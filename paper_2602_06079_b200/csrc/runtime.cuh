@@ -31,6 +31,7 @@
 
 #include "ns_engine.cuh"
 #include "shampoo_engine.cuh"
+#include "soap_engine.cuh"
 #include "optishard/optishard.hpp"
 #include "osh.h"
 

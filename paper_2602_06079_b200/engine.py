@@ -54,7 +54,24 @@ class ShampooConfig:
                                 self.newton_iters, 0)
 
 
-OPTIMIZERS = {"muon": 0, "shampoo": 1}
+@dataclass
+class SoapConfig:
+    """Builder-defined blocked SOAP (osh.h OSH_OPT_SOAP; specification
+    oracle/soap_oracle.py). lr / beta1 come from OptimizerConfig; beta2 is
+    both the second-moment and the statistics decay; init_iters = power
+    iterations of the first basis refresh. Carried in osh_shampoo_cfg."""
+    beta2: float = 0.95
+    eps: float = 1e-8
+    block: int = 1024
+    precond_every: int = 10
+    init_iters: int = 4
+
+    def c(self) -> _lib.ShampooCfgC:
+        return _lib.ShampooCfgC(self.beta2, self.eps, self.block, self.precond_every,
+                                self.init_iters, 0)
+
+
+OPTIMIZERS = {"muon": 0, "shampoo": 1, "soap": 2}
 STRATEGIES = {"sharded": 0, "sc": 1, "nv-layerwise": 2}
 
 
@@ -115,7 +132,7 @@ class DistributedMuon:
             _lib.check(L.osh_ctx_set_tp_capacity(ctx, tp_capacity))
         _lib.check(L.osh_ctx_set_collectives(ctx, COLLECTIVES[collectives]))
         if optimizer != "muon" or shampoo is not None:
-            sc = (shampoo or ShampooConfig()).c()
+            sc = (shampoo or (SoapConfig() if optimizer == "soap" else ShampooConfig())).c()
             _lib.check(L.osh_ctx_set_optimizer(ctx, OPTIMIZERS[optimizer], ctypes.byref(sc)))
         self.optimizer = optimizer
         if strategy != "sharded":

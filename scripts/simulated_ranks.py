@@ -6,8 +6,8 @@ box has (the 8-GPU configs C2 / M0 of SURVEY.md §8 D2).
 
     python scripts/simulated_ranks.py CONFIG RANKS METHOD [ALPHA] [STEPS] [ROUNDS]
 prints one JSON line. ALPHA may be "auto" (planner.choose_alpha).
-OSH_SIMRANK_OPT=shampoo runs the builder-defined blocked Shampoo instead of
-Muon (config C4) and also times one preconditioner-refresh step per rank;
+OSH_SIMRANK_OPT=shampoo|soap runs the builder-defined blocked Shampoo / SOAP
+instead of Muon (config C4) and also times one preconditioner-refresh step per rank;
 OSH_SIMRANK_WS_GB caps the NS / Shampoo workspace (default: the runtime's).
 
 Every rank is measured ROUNDS times, the ranks interleaved (rank 0..R-1, then
@@ -27,9 +27,10 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_06079_b200 import planner as P  # noqa: E402
-from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, ShampooConfig  # noqa: E402
+from paper_2602_06079_b200.engine import (DistributedMuon, OptimizerConfig, ShampooConfig,  # noqa: E402
+                                          SoapConfig)
 
-OPT = os.environ.get("OSH_SIMRANK_OPT", "muon")
+OPT = os.environ.get("OSH_SIMRANK_OPT", "muon")  # muon | shampoo | soap
 WS = int(float(os.environ.get("OSH_SIMRANK_WS_GB", "0")) * (1 << 30))
 PRECOND_EVERY = 10
 
@@ -56,7 +57,8 @@ def timed(e, n):
 
 
 def measure_rank(params, cap, plan, r, steps, breakdown):
-    sh = ShampooConfig(precond_every=PRECOND_EVERY) if OPT == "shampoo" else None
+    sh = (ShampooConfig(precond_every=PRECOND_EVERY) if OPT == "shampoo" else
+          SoapConfig(precond_every=PRECOND_EVERY) if OPT == "soap" else None)
     with DistributedMuon(params, cap, plan, rank=r, comm="none", grad_dtype="bf16",
                          optimizer=OPT, shampoo=sh, workspace_bytes=WS) as e:
         e.fill_synthetic(42, "weights")
@@ -125,7 +127,7 @@ def main():
            "note": "ranks run one at a time on one B200 (comm none): the compute "
                    "half of an R-GPU step, no collectives; per-rank median over "
                    "interleaved rounds"}
-    if OPT == "shampoo":
+    if OPT in ("shampoo", "soap"):
         # Newton-Schulz flops do not apply; the per-step ratio is the measured one
         for k in ("per_rank_ns_tflop", "per_rank_alg_tflops", "plan_nsflops_max_mean"):
             out.pop(k)
