@@ -6,9 +6,6 @@
 #include <map>
 #include <string>
 
-#include <cublas_v2.h>
-#include <cusolverDn.h>
-
 #include "status.hpp"
 
 namespace osh {
@@ -55,11 +52,14 @@ std::vector<BlockGeom> blocks_of(int rows, int cols, int b) {
 size_t block_ws(int p, int q) {
   const size_t ldp = rup(p, 64), ldq = rup(q, 64);
   return rup(2 * p * 4 * ldq, 256) * 3 + rup(2 * q * 4 * ldp, 256) + 2 * rup(2 * 4 * ldp * ldq, 256) +
-         2 * rup(4 * p * ldq, 256) + 3 * rup(2 * p * ldq, 256) + 2 * rup(4 * p * ldp, 256) +
-         2 * rup(4 * q * ldq, 256);
+         2 * rup(4 * p * ldq, 256) + 3 * rup(2 * p * ldq, 256);
 }
 
-const char* blas_err(cublasStatus_t s) { return s == CUBLAS_STATUS_SUCCESS ? nullptr : "cuBLAS"; }
+// refresh workspace bytes of one n x n matrix (see SoapEngine::Side)
+size_t refresh_ws(int n, int ld) {
+  return 3 * rup(2ull * n * 4 * ld, 256) + rup(2ull * 4 * ld * ld, 256) + rup(4ull * n * ld, 256) +
+         2 * rup(4ull * ld * ld, 256);
+}
 
 }  // namespace
 
@@ -69,7 +69,8 @@ void SoapEngine::release() {
   for (void* p : {static_cast<void*>(d_ws_), static_cast<void*>(d_state_),
                   static_cast<void*>(d_partial_), static_cast<void*>(d_update_sq_),
                   static_cast<void*>(d_bscale_), static_cast<void*>(d_order_),
-                  static_cast<void*>(d_info_), static_cast<void*>(d_ptrs_),
+                  static_cast<void*>(d_rws_), static_cast<void*>(d_split_),
+                  static_cast<void*>(d_chol_),
                   static_cast<void*>(d_prep_), static_cast<void*>(d_rot_),
                   static_cast<void*>(d_apply_), static_cast<void*>(d_blockrefs_),
                   static_cast<void*>(d_adam_), static_cast<void*>(d_basis_),
@@ -80,8 +81,10 @@ void SoapEngine::release() {
   d_ws_ = d_state_ = nullptr;
   d_partial_ = d_update_sq_ = nullptr;
   d_bscale_ = nullptr;
-  d_order_ = d_info_ = nullptr;
-  d_ptrs_ = nullptr;
+  d_order_ = nullptr;
+  d_rws_ = nullptr;
+  d_split_ = nullptr;
+  d_chol_ = nullptr;
   d_prep_ = nullptr;
   d_rot_ = nullptr;
   d_apply_ = nullptr;
@@ -92,15 +95,12 @@ void SoapEngine::release() {
   d_qcast_ = nullptr;
   d_slot_begin_ = nullptr;
   d_slot_count_ = d_slot_target_ = nullptr;
-  if (blas_ != nullptr) cublasDestroy(static_cast<cublasHandle_t>(blas_));
-  if (solver_ != nullptr) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
-  blas_ = solver_ = nullptr;
   waves_.clear();
 }
 
 const char* SoapEngine::elementwise_name(int mode) const {
   static const char* kNames[] = {"soap_prep",  "soap_rot",   "soap_apply", "soap_adam",
-                                 "soap_basis", "soap_vperm", "soap_qcast", "soap_cholqr",
+                                 "soap_basis", "soap_vperm", "soap_qcast", "soap_split_chol",
                                  "partial_sums"};
   const int i = mode - kModeElementwise;
   return i >= 0 && i < 9 ? kNames[i] : "elementwise";
@@ -153,7 +153,9 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   };
   std::vector<std::vector<std::vector<TB>>> cls_blocks(members.size());  // [wave][cls] -> blocks
   size_t state_off = 0;
-  int n_orders = 0, n_ptrs = 0;
+  int n_orders = 0;
+  // refresh sub-batch budget: a quarter of the workspace budget, at most 2 GiB
+  const size_t rws_cap = std::min<size_t>(budget / 4, 2ull << 30);
   std::vector<size_t> vec_v(tensors.size(), 0);  // Adam second moment of non-preconditioned tensors
   for (size_t wi = 0; wi < members.size(); ++wi) {
     Wave w;
@@ -209,10 +211,21 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       k.Mp = off; off += pq4 * k.nb;
       k.l.n = k.p; k.l.ld = k.ldp;
       k.r.n = k.q; k.r.ld = k.ldq;
-      k.l.Y = off; off += pp4 * k.nb;
-      k.l.C = off; off += pp4 * k.nb;
-      k.r.Y = off; off += qq4 * k.nb;
-      k.r.C = off; off += qq4 * k.nb;
+      for (Side* sd : {&k.l, &k.r}) {  // refresh sub-batches
+        sd->rb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(
+                                      static_cast<size_t>(k.nb), rws_cap / refresh_ws(sd->n, sd->ld))));
+        const size_t rb = static_cast<size_t>(sd->rb);
+        const size_t n = static_cast<size_t>(sd->n), ld = static_cast<size_t>(sd->ld);
+        size_t o = 0;
+        sd->Ss = o; o += rb * rup(2 * n * 4 * ld, 256);
+        sd->Qc = o; o += rb * rup(2 * n * 4 * ld, 256);
+        sd->Lc = o; o += rb * rup(2 * n * 4 * ld, 256);
+        sd->Qr = o; o += rb * rup(2 * 4 * ld * ld, 256);
+        sd->Y = o; o += rb * rup(4 * n * ld, 256);
+        sd->C = o; o += rb * rup(4 * ld * ld, 256);
+        sd->Li = o; o += rb * rup(4 * ld * ld, 256);
+        rws_bytes_ = std::max(rws_bytes_, o);
+      }
       k.l.S = state_off; state_off += pp4 * k.nb;
       k.r.S = state_off; state_off += qq4 * k.nb;
       k.l.Q = state_off; state_off += pp4 * k.nb;
@@ -223,8 +236,6 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       k.V = state_off; state_off += pq4 * k.nb;
       k.l.order0 = n_orders; n_orders += k.p * k.nb;
       k.r.order0 = n_orders; n_orders += k.q * k.nb;
-      k.l.ptr0 = n_ptrs; n_ptrs += 2 * k.nb;
-      k.r.ptr0 = n_ptrs; n_ptrs += 2 * k.nb;
       w.cls.push_back(k);
     }
     ws_bytes_ = std::max(ws_bytes_, off);
@@ -235,6 +246,8 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_state_), std::max<size_t>(state_bytes_, 256)));
   OSH_CUDA_TRY(cudaMemset(d_ws_, 0, std::max<size_t>(ws_bytes_, 256)));
   OSH_CUDA_TRY(cudaMemset(d_state_, 0, std::max<size_t>(state_bytes_, 256)));
+  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_rws_), std::max<size_t>(rws_bytes_, 256)));
+  OSH_CUDA_TRY(cudaMemset(d_rws_, 0, std::max<size_t>(rws_bytes_, 256)));
   auto ws = [&](size_t o) { return d_ws_ + o; };
   auto st = [&](size_t o) { return d_state_ + o; };
 
@@ -249,7 +262,8 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   std::vector<SoapQcastTask> qcast;
   std::vector<long long> slot_begin;
   std::vector<int> slot_count, slot_target;
-  std::vector<float*> ptrs(static_cast<size_t>(std::max(n_ptrs, 1)), nullptr);
+  std::vector<SoapSplitTask> split;
+  std::vector<SoapCholTask> chol;
   long long max_partial = 1;
   const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   std::vector<size_t> apply_bref_first;  // per apply task: first ShBlockRef (patched below)
@@ -279,19 +293,80 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       rot.push_back(rt);
       for (Side* sd : {&k.l, &k.r}) {
         sd->basis0 = static_cast<int>(basis.size());
-        const long long nn = static_cast<long long>(sd->n) * sd->ld;
-        for (int i = 0; i < k.nb; ++i) {
-          SoapBasisTask bt{};
-          bt.s = reinterpret_cast<const float*>(st(sd->S)) + nn * i;
-          bt.lds = sd->ld;
-          bt.q = reinterpret_cast<float*>(st(sd->Q)) + nn * i;
-          bt.y = reinterpret_cast<float*>(ws(sd->Y)) + nn * i;
-          bt.ldq = sd->ld;
-          bt.order = nullptr;  // patched after d_order_ exists
-          bt.n = sd->n;
-          basis.push_back(bt);
-          ptrs[static_cast<size_t>(sd->ptr0 + i)] = bt.q;
-          ptrs[static_cast<size_t>(sd->ptr0 + k.nb + i)] = reinterpret_cast<float*>(ws(sd->C)) + nn * i;
+        const long long n = sd->n, ld = sd->ld, nn = n * ld;
+        uint8_t* R = d_rws_;
+        auto bf = [&](size_t off, long long j, long long per) {
+          return reinterpret_cast<__nv_bfloat16*>(R + off) + per * j;
+        };
+        auto f32 = [&](size_t off, long long j, long long per) {
+          return reinterpret_cast<float*>(R + off) + per * j;
+        };
+        const long long tiles = tiles_of(sd->n, sd->n);
+        for (int i0 = 0; i0 < k.nb; i0 += sd->rb) {
+          RChunk ch;
+          ch.i0 = i0;
+          ch.b = std::min(sd->rb, k.nb - i0);
+          ch.split_s = static_cast<int>(split.size());
+          for (int j = 0; j < ch.b; ++j) {  // S -> column split
+            SoapSplitTask t{};
+            t.src = reinterpret_cast<const float*>(st(sd->S)) + nn * (i0 + j);
+            t.lds = ld;
+            t.rows = t.cols = sd->n;
+            t.col = bf(sd->Ss, j, n * 4 * ld);
+            t.ldd = ld;
+            t.tiles_c = (sd->n + kTile - 1) / kTile;
+            t.tile_start = ch.tiles_s;
+            ch.tiles_s += tiles;
+            split.push_back(t);
+          }
+          ch.split_q = static_cast<int>(split.size());
+          for (int j = 0; j < ch.b; ++j) {  // Q storage -> column and row splits
+            SoapSplitTask t{};
+            t.src = reinterpret_cast<const float*>(st(sd->Q)) + nn * (i0 + j);
+            t.lds = ld;
+            t.rows = t.cols = sd->n;
+            t.col = bf(sd->Qc, j, n * 4 * ld);
+            t.row = bf(sd->Qr, j, 4 * ld * ld);
+            t.ldd = ld;
+            t.tiles_c = (sd->n + kTile - 1) / kTile;
+            t.tile_start = ch.tiles_q;
+            ch.tiles_q += tiles;
+            split.push_back(t);
+          }
+          ch.split_l = static_cast<int>(split.size());
+          for (int j = 0; j < ch.b; ++j) {  // L^-1 -> column split
+            SoapSplitTask t{};
+            t.src = f32(sd->Li, j, ld * ld);
+            t.lds = ld;
+            t.rows = t.cols = sd->n;
+            t.col = bf(sd->Lc, j, n * 4 * ld);
+            t.ldd = ld;
+            t.tiles_c = (sd->n + kTile - 1) / kTile;
+            t.tile_start = ch.tiles_l;
+            ch.tiles_l += tiles;
+            split.push_back(t);
+          }
+          ch.chol = static_cast<int>(chol.size());
+          for (int j = 0; j < ch.b; ++j) {
+            SoapCholTask t{};
+            t.c = f32(sd->C, j, ld * ld);
+            t.linv = f32(sd->Li, j, ld * ld);
+            t.ld = ld;
+            t.n = sd->n;
+            chol.push_back(t);
+          }
+          for (int j = 0; j < ch.b; ++j) {
+            SoapBasisTask bt{};
+            bt.s = reinterpret_cast<const float*>(st(sd->S)) + nn * (i0 + j);
+            bt.lds = ld;
+            bt.q = reinterpret_cast<float*>(st(sd->Q)) + nn * (i0 + j);
+            bt.y = f32(sd->Y, j, nn);
+            bt.ldq = ld;
+            bt.order = nullptr;  // patched after d_order_ exists
+            bt.n = sd->n;
+            basis.push_back(bt);
+          }
+          sd->chunks.push_back(ch);
         }
       }
       for (int i = 0; i < k.nb; ++i) {
@@ -444,7 +519,6 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_update_sq_), sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(cudaMemset(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_order_), sizeof(int) * static_cast<size_t>(std::max(n_orders, 1))));
-  OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_info_), sizeof(int) * static_cast<size_t>(max_nb_)));
   {
     const std::vector<float> bs(static_cast<size_t>(max_nb_), static_cast<float>(1.0 - cfg_.beta2));
     OSH_CUDA_TRY(upload(&d_bscale_, bs));
@@ -478,7 +552,8 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(upload(&d_basis_, basis));
   OSH_CUDA_TRY(upload(&d_vperm_, vperm));
   OSH_CUDA_TRY(upload(&d_qcast_, qcast));
-  OSH_CUDA_TRY(upload(&d_ptrs_, ptrs));
+  OSH_CUDA_TRY(upload(&d_split_, split));
+  OSH_CUDA_TRY(upload(&d_chol_, chol));
   OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
   OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
   OSH_CUDA_TRY(upload(&d_slot_target_, slot_target));
@@ -490,14 +565,6 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
                                      static_cast<long long>(sd->n) * sd->ld, sd->n, k.nb, nullptr));
     OSH_CUDA_TRY(launch_soap_qcast(d_qcast_ + w.qcast.first, w.qcast.count, w.qcast.tiles, nullptr));
   }
-  cublasHandle_t h = nullptr;
-  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return fail(OSH_ERR_CUDA, "cublasCreate failed");
-  blas_ = h;
-  cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);  // true fp32 (no TF32) for the basis refresh
-  cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
-  cusolverDnHandle_t sv = nullptr;
-  if (cusolverDnCreate(&sv) != CUSOLVER_STATUS_SUCCESS) return fail(OSH_ERR_CUDA, "cusolverDnCreate failed");
-  solver_ = sv;
   OSH_CUDA_TRY(cudaDeviceSynchronize());
   return OSH_OK;
 }
@@ -509,63 +576,69 @@ osh_status SoapEngine::begin_step(cudaStream_t s) {
   return OSH_OK;
 }
 
-// Q <- Q R^-1 with Q^T Q = R^T R (CholeskyQR), twice (CholeskyQR2)
-osh_status SoapEngine::cholesky_qr(const Side& sd, int nb, cudaStream_t s) {
-  cublasHandle_t h = static_cast<cublasHandle_t>(blas_);
-  cusolverDnHandle_t sv = static_cast<cusolverDnHandle_t>(solver_);
-  const float one = 1.f, zero = 0.f;
-  const long long nn = static_cast<long long>(sd.n) * sd.ld;
-  float* Q = reinterpret_cast<float*>(d_state_ + sd.Q);
-  float* C = reinterpret_cast<float*>(d_ws_ + sd.C);
-  float** qp = d_ptrs_ + sd.ptr0;
-  float** cp = d_ptrs_ + sd.ptr0 + nb;
-  for (int pass = 0; pass < 2; ++pass) {
-    if (blas_err(cublasSgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, sd.n, sd.n, sd.n, &one, Q,
-                                           sd.ld, nn, Q, sd.ld, nn, &zero, C, sd.ld, nn, nb)))
-      return fail(OSH_ERR_CUDA, "SOAP: cublasSgemmStridedBatched (Gram) failed");
-    if (cusolverDnSpotrfBatched(sv, CUBLAS_FILL_MODE_LOWER, sd.n, cp, sd.ld, d_info_, nb) !=
-        CUSOLVER_STATUS_SUCCESS)
-      return fail(OSH_ERR_CUDA, "SOAP: cusolverDnSpotrfBatched failed");
-    if (blas_err(cublasStrsmBatched(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                                    CUBLAS_DIAG_NON_UNIT, sd.n, sd.n, &one, cp, sd.ld, qp, sd.ld, nb)))
-      return fail(OSH_ERR_CUDA, "SOAP: cublasStrsmBatched failed");
-  }
-  (void)s;
+// One side's basis refresh, `iters` times, in sub-batches (soap_engine.cuh):
+// Y = S Q, soap_basis, then CholeskyQR2 on the result. All products are
+// tcgen05 STAT GEMMs (fp32 out) over bf16x3 splits; the Cholesky factor and
+// its inverse come from soap_chol_inv. Q (fp32) is stored column-major, i.e.
+// its storage rows are Q's columns: Y^T = Q^T S, Gram = Q^T Q and
+// Q' = Q (L^T)^-1  <=>  Q'^T = L^-1 Q^T are row-major products of the storage.
+osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
+  const long long n = sd.n, ld = sd.ld, nn = n * ld;
+  auto gemm1 = [&](NsProblemDesc& d) -> osh_status {
+    const cudaError_t e = timed_gemm(kEpiStat, &d, 1, 0.f, 0.f, s);
+    if (e != cudaSuccess)
+      return fail(OSH_ERR_CUDA, std::string("SoapEngine refresh: ns_gemm_launch: ") + cudaGetErrorString(e));
+    return OSH_OK;
+  };
+  for (int it = 0; it < iters; ++it)
+    for (const RChunk& ch : sd.chunks) {
+      const int b = ch.b;
+      float* Q = reinterpret_cast<float*>(d_state_ + sd.Q) + nn * ch.i0;
+      OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
+        cudaError_t e = launch_soap_split(d_split_ + ch.split_s, b, ch.tiles_s, s);
+        if (e == cudaSuccess) e = launch_soap_split(d_split_ + ch.split_q, b, ch.tiles_q, s);
+        return e;
+      }));
+      {  // Y^T (= Y column-major) = Q^T S: A = Q storage (hi,lo,hi), B = S (lo,hi,hi)
+        NsProblemDesc d{};
+        d.a = mref(d_rws_ + sd.Qc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        d.b = mref(d_rws_ + sd.Ss + 2 * ld, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        d.out = mref(d_rws_ + sd.Y, b, sd.n, sd.n, ld, nn);
+        if (osh_status st = gemm1(d); st != OSH_OK) return st;
+      }
+      OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 4, 0.0, 0.0, s, [&] {
+        return launch_soap_basis(d_basis_ + sd.basis0 + ch.i0, b, cfg_.shift, s);
+      }));
+      for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2
+        OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
+          return launch_soap_split(d_split_ + ch.split_q, b, ch.tiles_q, s);
+        }));
+        NsProblemDesc g{};  // Gram = Q^T Q (symmetric)
+        g.a = mref(d_rws_ + sd.Qc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        g.b = mref(d_rws_ + sd.Qc + 2 * ld, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        g.out = mref(d_rws_ + sd.C, b, sd.n, sd.n, ld, ld * ld);
+        g.symmetric = 1;
+        if (osh_status st = gemm1(g); st != OSH_OK) return st;
+        OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
+          cudaError_t e = launch_soap_chol_inv(d_chol_ + ch.chol, b, s);
+          if (e == cudaSuccess) e = launch_soap_split(d_split_ + ch.split_l, b, ch.tiles_l, s);
+          return e;
+        }));
+        NsProblemDesc u{};  // Q'^T = L^-1 Q^T: A = L^-1 (hi,lo,hi), B = Q storage row-split (lo,hi,hi)
+        u.a = mref(d_rws_ + sd.Lc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        u.b = mref(d_rws_ + sd.Qr + 2 * ld * ld, b, 3 * sd.ld, sd.n, ld, 4 * ld * ld);
+        u.b_mn_major = 1;
+        u.out = mref(Q, b, sd.n, sd.n, ld, nn);
+        if (osh_status st = gemm1(u); st != OSH_OK) return st;
+      }
+    }
   return OSH_OK;
 }
 
 osh_status SoapEngine::refresh(const Wave& w, int iters, bool permute_v, cudaStream_t s) {
-  cublasHandle_t h = static_cast<cublasHandle_t>(blas_);
-  cusolverDnHandle_t sv = static_cast<cusolverDnHandle_t>(solver_);
-  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS || cusolverDnSetStream(sv, s) != CUSOLVER_STATUS_SUCCESS)
-    return fail(OSH_ERR_CUDA, "SOAP: cuBLAS / cuSOLVER stream binding failed");
-  const float one = 1.f, zero = 0.f;
   for (const Cls& k : w.cls)
-    for (const Side* sd : {&k.l, &k.r}) {
-      const long long nn = static_cast<long long>(sd->n) * sd->ld;
-      const float* S = reinterpret_cast<const float*>(d_state_ + sd->S);
-      float* Q = reinterpret_cast<float*>(d_state_ + sd->Q);
-      float* Y = reinterpret_cast<float*>(d_ws_ + sd->Y);
-      for (int it = 0; it < iters; ++it) {
-        osh_status rc = OSH_OK;
-        OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
-          // Y = S Q (S symmetric: its row-major storage is its column-major one)
-          if (blas_err(cublasSgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, sd->n, sd->n, sd->n, &one,
-                                                 S, sd->ld, nn, Q, sd->ld, nn, &zero, Y, sd->ld, nn, k.nb)))
-            rc = fail(OSH_ERR_CUDA, "SOAP: cublasSgemmStridedBatched (S Q) failed");
-          return cudaGetLastError();
-        }));
-        if (rc != OSH_OK) return rc;
-        OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 4, 0.0, 0.0, s, [&] {
-          return launch_soap_basis(d_basis_ + sd->basis0, k.nb, cfg_.shift, s);
-        }));
-        OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
-          rc = cholesky_qr(*sd, k.nb, s);
-          return cudaGetLastError();
-        }));
-        if (rc != OSH_OK) return rc;
-      }
-    }
+    for (const Side* sd : {&k.l, &k.r})
+      if (osh_status st = refresh_side(*sd, iters, s); st != OSH_OK) return st;
   if (permute_v && w.vperm.count > 0) {
     OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 5, 0.0, 0.0, s, [&] {
       return launch_soap_vperm(d_vperm_ + w.vperm.first, w.vperm.count, w.vperm.tiles, s);

@@ -18,9 +18,12 @@
 // statistics) amplify operand rounding, so every product feeding them runs in
 // bf16x3 (measured: bf16 operands there move the update 25-45 % away from the
 // fp64 specification, bf16x3 ~1e-3); the back-projection N stays bf16.
-//   [refresh calls]      Y = S Q (cuBLAS SGEMM), soap_basis (shift, order,
-//                        unit columns), CholeskyQR2 (cuBLAS SGEMM + cuSOLVER
-//                        POTRF + cuBLAS TRSM), V reordered, bf16 Q / Q^T
+//   [refresh calls]      per side, in sub-batches: bf16x3 splits of S and Q,
+//                        Y = S Q (STAT, bf16x3), soap_basis (shift, order,
+//                        unit columns), CholeskyQR2 = 2 x {Gram Q^T Q (STAT,
+//                        bf16x3), soap_chol_inv (Cholesky + L^-1, one CTA per
+//                        matrix), Q <- L^-1-applied Q (STAT, bf16x3)},
+//                        V reordered, bf16 / bf16x3 copies of Q
 //   soap_adam            vectors and vocabulary matrices: elementwise Adam
 // Waves run back to back on one stream.
 #pragma once
@@ -61,13 +64,22 @@ class SoapEngine : public OptimizerEngine {
   void set_step_counter(long long s) override { step_ = s; }
 
  private:
+  struct RChunk {                  // refresh sub-batch: matrices [i0, i0 + b) of a side
+    int i0 = 0, b = 0;
+    int split_s = 0, split_q = 0, split_l = 0, chol = 0;  // first task of each kind
+    long long tiles_s = 0, tiles_q = 0, tiles_l = 0;
+  };
   struct Side {                    // one side (L or R) of a class: nb matrices of n x n
     int n = 0, ld = 0;
     size_t S = 0, Q = 0;           // state: statistics [n][ld] fp32, basis column-major fp32
-    size_t Y = 0, C = 0;           // workspace: S Q and the CholeskyQR Gram matrix
     int order0 = 0;                // first order entry (d_order_)
-    int ptr0 = 0;                  // first pointer slot (d_ptrs_): Q ptrs, then Gram ptrs
     int basis0 = 0;                // first soap_basis task
+    // refresh workspace (d_rws_), by kind for rb matrices: S, Q and L^-1
+    // column-splits [rb][n][4 ld], Q row-split [rb][4 ld][ld], Y [rb][n][ld],
+    // Gram and L^-1 [rb][ld][ld]
+    int rb = 1;
+    size_t Ss = 0, Qc = 0, Lc = 0, Qr = 0, Y = 0, C = 0, Li = 0;
+    std::vector<RChunk> chunks;
   };
   struct Cls {                     // blocks of one (p, q) inside one wave
     int p = 0, q = 0, ldp = 0, ldq = 0, nb = 0;
@@ -94,7 +106,7 @@ class SoapEngine : public OptimizerEngine {
   const char* elementwise_name(int mode) const override;
   void release();
   osh_status refresh(const Wave& w, int iters, bool permute_v, cudaStream_t s);
-  osh_status cholesky_qr(const Side& sd, int nb, cudaStream_t s);
+  osh_status refresh_side(const Side& sd, int iters, cudaStream_t s);
 
   SoapConfig cfg_;
   int n_tensors_ = 0, grad_dtype_ = 0;
@@ -107,8 +119,10 @@ class SoapEngine : public OptimizerEngine {
   double* d_update_sq_ = nullptr;
   float* d_bscale_ = nullptr;     // (1 - beta2) per batch entry (statistics scale)
   int* d_order_ = nullptr;        // basis orders of every statistics matrix
-  int* d_info_ = nullptr;         // cuSOLVER potrf info per matrix
-  float** d_ptrs_ = nullptr;      // batched cuBLAS / cuSOLVER pointer arrays
+  uint8_t* d_rws_ = nullptr;      // basis-refresh workspace (one sub-batch)
+  size_t rws_bytes_ = 0;
+  SoapSplitTask* d_split_ = nullptr;
+  SoapCholTask* d_chol_ = nullptr;
   SoapPrepTask* d_prep_ = nullptr;
   SoapRotTask* d_rot_ = nullptr;
   ShApplyTask* d_apply_ = nullptr;
@@ -120,8 +134,6 @@ class SoapEngine : public OptimizerEngine {
   long long* d_slot_begin_ = nullptr;
   int* d_slot_count_ = nullptr;
   int* d_slot_target_ = nullptr;
-  void* blas_ = nullptr;          // cublasHandle_t
-  void* solver_ = nullptr;        // cusolverDnHandle_t
   int max_nb_ = 1;
 };
 

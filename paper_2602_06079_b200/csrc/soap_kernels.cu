@@ -422,6 +422,177 @@ __global__ void soap_eye_kernel(float* q, long long ldq, long long bstride, int 
   for (long long i = threadIdx.x; i < ldq; i += blockDim.x) c[i] = i == j ? 1.f : 0.f;
 }
 
+// ---------------------------------------------------------------- refresh factorizations
+__global__ void __launch_bounds__(256) soap_split_kernel(const SoapSplitTask* tasks, int n) {
+  const long long t = blockIdx.x;
+  const SoapSplitTask T = tasks[find_task(tasks, n, t)];
+  const long long local = t - T.tile_start;
+  const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
+  const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = 0; i < kTile / 8; ++i) {
+    const int r = r0 + ty + 8 * i;
+    for (int j = 0; j < kTile / 32; ++j) {
+      const int c = c0 + tx + 32 * j;
+      const float v = (r < T.rows && c < T.cols) ? T.src[static_cast<size_t>(r) * T.lds + c] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+      if (T.col != nullptr && r < T.rows) {
+        __nv_bfloat16* d = T.col + static_cast<size_t>(r) * 4 * T.ldd + c;
+        d[0] = hi;
+        d[T.ldd] = lo;
+        d[2 * T.ldd] = hi;
+        d[3 * T.ldd] = hi;
+      }
+      if (T.row != nullptr) {
+        const size_t seg = static_cast<size_t>(T.ldd) * T.ldd;
+        __nv_bfloat16* d = T.row + static_cast<size_t>(r) * T.ldd + c;
+        d[0] = hi;
+        d[seg] = lo;
+        d[2 * seg] = hi;
+        d[3 * seg] = hi;
+      }
+    }
+  }
+}
+
+constexpr int kCholThreads = 1024;
+constexpr int kCholLrs = kSoapCholMaxN + 1;  // row stride of the phase-2 row block in smem
+constexpr size_t kCholSmem =
+    sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 > 32ull * kCholLrs
+                         ? static_cast<size_t>(kSoapCholMaxN) * 33
+                         : 32ull * kCholLrs) +
+    sizeof(float) * 32 * 33;
+
+__global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const SoapCholTask* tasks) {
+  extern __shared__ float sm[];
+  float* P = sm;                                   // phase 1: panel [m][33]; phase 2: row block [32][kCholLrs]
+  float* D = sm + (kCholSmem / sizeof(float) - 32 * 33);  // diagonal block [32][33]
+  const SoapCholTask T = tasks[blockIdx.x];
+  const int n = T.n;
+  const int np = (n + 31) / 32 * 32;
+  const long long ld = T.ld;
+  float* C = T.c;
+  float* X = T.linv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the pad [n, np) becomes the identity; L^-1 starts at 0
+  for (long long e = threadIdx.x; e < static_cast<long long>(np) * np; e += kCholThreads) {
+    const int i = static_cast<int>(e / np), j = static_cast<int>(e % np);
+    if (i >= n || j >= n) C[i * ld + j] = i == j ? 1.f : 0.f;
+    X[i * ld + j] = 0.f;
+  }
+  __syncthreads();
+  // ---- phase 1: right-looking blocked Cholesky, C = L L^T (lower, in place)
+  for (int k0 = 0; k0 < np; k0 += 32) {
+    if (warp == 0) {
+      for (int r = 0; r < 32; ++r) D[r * 33 + lane] = lane <= r ? C[(k0 + r) * ld + k0 + lane] : 0.f;
+      __syncwarp();
+      for (int j = 0; j < 32; ++j) {
+        if (lane == j) D[j * 33 + j] = sqrtf(fmaxf(D[j * 33 + j], 1e-30f));
+        __syncwarp();
+        if (lane > j) D[lane * 33 + j] /= D[j * 33 + j];
+        __syncwarp();
+        if (lane > j) {
+          const float lij = D[lane * 33 + j];
+          for (int l = j + 1; l <= lane; ++l) D[lane * 33 + l] -= lij * D[l * 33 + j];
+        }
+        __syncwarp();
+      }
+      for (int r = 0; r < 32; ++r)
+        if (lane <= r) C[(k0 + r) * ld + k0 + lane] = D[r * 33 + lane];
+    }
+    __syncthreads();
+    const int m = np - k0 - 32;  // rows below the diagonal block
+    for (int t = threadIdx.x; t < m; t += kCholThreads) {
+      const long long i = k0 + 32 + t;
+      float x[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = C[i * ld + k0 + j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float v = x[j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) v -= x[q] * D[j * 33 + q];
+        x[j] = v / D[j * 33 + j];
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        P[t * 33 + j] = x[j];
+        C[i * ld + k0 + j] = x[j];
+      }
+    }
+    __syncthreads();
+    const int mt = m / 4;  // m is a multiple of 32
+    const int ntile = mt * (mt + 1) / 2;
+    for (int id = threadIdx.x; id < ntile; id += kCholThreads) {
+      int ti = static_cast<int>((sqrtf(8.f * id + 1.f) - 1.f) * 0.5f);
+      while ((ti + 1) * (ti + 2) / 2 <= id) ++ti;
+      while (ti * (ti + 1) / 2 > id) --ti;
+      const int tj = id - ti * (ti + 1) / 2;
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) {
+        float av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = P[(ti * 4 + a) * 33 + q];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bv[b] = P[(tj * 4 + b) * 33 + q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const long long i = k0 + 32 + ti * 4 + a, j = k0 + 32 + tj * 4 + b;
+          if (i >= j) C[i * ld + j] -= acc[a][b];
+        }
+    }
+    __syncthreads();
+  }
+  // ---- phase 2: X = L^-1 by row blocks: X[k..k+32) = Ldiag^-1 (E - L[k.., 0:k) X[0:k))
+  float* Lr = P;
+  for (int k = 0; k < np; k += 32) {
+    const int w = k + 32;
+    for (int e = threadIdx.x; e < 32 * w; e += kCholThreads) {
+      const int r = e / w, mm = e % w;
+      Lr[r * kCholLrs + mm] = mm <= k + r ? C[(k + r) * ld + mm] : 0.f;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < w; c += kCholThreads) {
+      float x[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) x[r] = 0.f;
+      if (c < k) {
+        for (int mm = 0; mm < k; ++mm) {
+          const float xv = X[static_cast<long long>(mm) * ld + c];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) x[r] -= Lr[r * kCholLrs + mm] * xv;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (c - k == r) x[r] += 1.f;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        float v = x[r];
+#pragma unroll
+        for (int q = 0; q < r; ++q) v -= Lr[r * kCholLrs + k + q] * x[q];
+        x[r] = v / Lr[r * kCholLrs + k + r];
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) X[static_cast<long long>(k + r) * ld + c] = x[r];
+    }
+    __syncthreads();
+  }
+}
+
 bool bad_grid(long long tiles) { return tiles <= 0 || tiles > 0x7fffffffll; }
 
 }  // namespace
@@ -493,6 +664,25 @@ cudaError_t launch_soap_qcast(const SoapQcastTask* d, int n, long long tiles, cu
   if (n == 0) return cudaSuccess;
   if (bad_grid(tiles)) return cudaErrorInvalidValue;
   soap_qcast_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(d, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_soap_split(const SoapSplitTask* d, int n, long long tiles, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (bad_grid(tiles)) return cudaErrorInvalidValue;
+  soap_split_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(d, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_soap_chol_inv(const SoapCholTask* d, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(soap_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kCholSmem));
+    attr = true;
+  }
+  soap_chol_inv_kernel<<<n, kCholThreads, kCholSmem, s>>>(d);
   return cudaGetLastError();
 }
 

@@ -1,10 +1,10 @@
 // Elementwise and per-matrix kernels of the blocked SOAP step (DESIGN.md
 // "SOAP"; specification: oracle/soap_oracle.py). The projections into and
-// out of the eigenbasis and the statistics run on the tcgen05 GEMM
-// (ns_gemm.cu: GRAM / STAT epilogues); the basis refresh's power-iteration
-// product and CholeskyQR2 use cuBLAS SGEMM / TRSM and cuSOLVER POTRF
-// (plain dense library factorizations, soap_engine.cu). Everything here is
-// HBM-bound (or, for the refresh helpers, one CTA per matrix).
+// out of the eigenbasis, the statistics and the refresh's products (S Q,
+// Q^T Q, L^-1 Q^T) run on the tcgen05 GEMM (ns_gemm.cu: SPLIT / STAT / GRAM
+// epilogues, bf16x3 operands where precision matters); the Cholesky factor
+// and its inverse come from soap_chol_inv (one CTA per matrix, fp32 CUDA
+// cores). Everything else here is HBM-bound elementwise work.
 //
 //   soap_prep      g (tensor layout, bf16/fp32, optionally the NVLS multicast
 //                  sum), M (fp32 tensor layout) -> M = b1 M + (1-b1) g and,
@@ -21,6 +21,9 @@
 //   soap_qcast     fp32 column-major Q -> bf16 Q^T column-split, Q row-major,
 //                  Q row-split
 //   soap_eye       Q = I (column-major fp32, zero padding)
+//   soap_split     fp32 matrix -> bf16x3 column / row splits (refresh operands)
+//   soap_chol_inv  C = L L^T and L^-1 (blocked right-looking Cholesky, then a
+//                  row-block forward substitution), one CTA per matrix
 #pragma once
 
 #include <cstdint>
@@ -111,6 +114,31 @@ struct SoapQcastTask {    // fp32 column-major Q (n x n) -> bf16 copies (each nu
   int tiles_c, pad2_;
 };
 
+struct SoapSplitTask {    // fp32 [rows][lds] -> bf16x3 copies (each nullable), pads 0
+  const float* src;
+  long long lds;
+  int rows, cols;         // logical size; tiles cover [rup(rows,64)] x [rup(cols,64)]
+  __nv_bfloat16* col;     // column-split [rows][4 ldd]
+  __nv_bfloat16* row;     // row-split    [4 ldd][ldd] (rows up to ldd, pads 0)
+  long long ldd;
+  long long tile_start;
+  int tiles_c, pad_;
+};
+
+// Batched Cholesky + triangular inverse, one CTA per matrix (n <= 1024):
+// C (SPD, fp32 [ld][ld], only [n][n] meaningful; the pad is made the identity)
+// is factored in place as C = L L^T (lower) and L^-1 is written to linv
+// ([ld][ld], upper part 0). Non-positive pivots are clamped to a tiny value.
+struct SoapCholTask {
+  float* c;
+  float* linv;
+  long long ld;
+  int n, pad_;
+};
+constexpr int kSoapCholMaxN = 1024;
+
+cudaError_t launch_soap_split(const SoapSplitTask* d, int n, long long tiles, cudaStream_t s);
+cudaError_t launch_soap_chol_inv(const SoapCholTask* d, int n, cudaStream_t s);
 cudaError_t launch_soap_prep(const SoapPrepTask* d, int n, long long tiles, int grad_dtype,
                              float beta1, cudaStream_t s);
 cudaError_t launch_soap_rot(const SoapRotTask* d, int n, long long chunks, float beta2,
