@@ -254,7 +254,8 @@ osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode);
  *                    supplies lr and beta (= beta1, momentum); ns_* are unused.
  *   OSH_OPT_SOAP     builder-defined blocked SOAP (Adam in the eigenbasis of
  *                    Shampoo's statistics, basis refreshed by shifted power
- *                    iteration + CholeskyQR2; oracle/soap_oracle.py). The
+ *                    iteration + CholeskyQR2, all on this library's own
+ *                    kernels; oracle/soap_oracle.py). The
  *                    osh_shampoo_cfg fields read: beta2 (second moment and
  *                    statistics decay, 0.95), eps (Adam epsilon, 1e-8), block,
  *                    precond_every, newton_iters = power iterations of the

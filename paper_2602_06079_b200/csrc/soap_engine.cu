@@ -57,8 +57,7 @@ size_t block_ws(int p, int q) {
 
 // refresh workspace bytes of one n x n matrix (see SoapEngine::Side)
 size_t refresh_ws(int n, int ld) {
-  return 3 * rup(2ull * n * 4 * ld, 256) + rup(2ull * 4 * ld * ld, 256) + rup(4ull * n * ld, 256) +
-         2 * rup(4ull * ld * ld, 256);
+  return 2 * rup(2ull * n * 4 * ld, 256) + rup(2ull * 4 * ld * ld, 256) + 2 * rup(4ull * ld * ld, 256);
 }
 
 }  // namespace
@@ -154,8 +153,9 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   std::vector<std::vector<std::vector<TB>>> cls_blocks(members.size());  // [wave][cls] -> blocks
   size_t state_off = 0;
   int n_orders = 0;
-  // refresh sub-batch budget: a quarter of the workspace budget, at most 2 GiB
-  const size_t rws_cap = std::min<size_t>(budget / 4, 2ull << 30);
+  // refresh sub-batch budget: enough for 2 x 148 matrices (two CTA waves of
+  // the one-CTA-per-matrix kernels) where the workspace budget allows
+  const size_t rws_cap = std::min<size_t>(budget / 2, 12ull << 30);
   std::vector<size_t> vec_v(tensors.size(), 0);  // Adam second moment of non-preconditioned tensors
   for (size_t wi = 0; wi < members.size(); ++wi) {
     Wave w;
@@ -216,13 +216,13 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
                                       static_cast<size_t>(k.nb), rws_cap / refresh_ws(sd->n, sd->ld))));
         const size_t rb = static_cast<size_t>(sd->rb);
         const size_t n = static_cast<size_t>(sd->n), ld = static_cast<size_t>(sd->ld);
+        // S's split is dead once Y = S Q is formed, Y once soap_basis ran:
+        // the L^-1 split aliases S's, the Gram matrix aliases Y
         size_t o = 0;
-        sd->Ss = o; o += rb * rup(2 * n * 4 * ld, 256);
+        sd->Ss = sd->Lc = o; o += rb * rup(2 * n * 4 * ld, 256);
         sd->Qc = o; o += rb * rup(2 * n * 4 * ld, 256);
-        sd->Lc = o; o += rb * rup(2 * n * 4 * ld, 256);
         sd->Qr = o; o += rb * rup(2 * 4 * ld * ld, 256);
-        sd->Y = o; o += rb * rup(4 * n * ld, 256);
-        sd->C = o; o += rb * rup(4 * ld * ld, 256);
+        sd->Y = sd->C = o; o += rb * rup(4 * ld * ld, 256);
         sd->Li = o; o += rb * rup(4 * ld * ld, 256);
         rws_bytes_ = std::max(rws_bytes_, o);
       }
@@ -699,10 +699,14 @@ osh_status SoapEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
         if (k.q % 64 != 0)
           OSH_CUDA_TRY(cudaMemsetAsync(d_ws_ + k.T1s, 0, 2 * 2ull * cpq * k.nb, s));  // T1s, T2s
         for (size_t src : {k.Grs, k.Mrs}) {
+          // bf16 gradients are exact in hi (lo = 0): T1 needs only the
+          // (lo, hi) x (hi, hi) segment pairs, K = 2 ldp
+          const int segs = (src == k.Grs && grad_dtype_ == kGradBF16) ? 2 : 3;
+          const int a0 = 3 - segs;  // first A segment: 0 (hi) or 1 (lo)
           NsProblemDesc d{};
-          d.a = mref(d_state_ + k.QLts, k.nb, k.p, 3 * k.ldp, 4ll * k.ldp,
+          d.a = mref(d_state_ + k.QLts + 2ull * a0 * k.ldp, k.nb, k.p, segs * k.ldp, 4ll * k.ldp,
                      static_cast<long long>(k.p) * 4 * k.ldp);
-          d.b = mref(d_ws_ + src + 2ull * k.ldp * k.ldq, k.nb, 3 * k.ldp, k.q, k.ldq,
+          d.b = mref(d_ws_ + src + 2ull * (1 + a0) * k.ldp * k.ldq, k.nb, segs * k.ldp, k.q, k.ldq,
                      4ll * k.ldp * k.ldq);
           d.b_mn_major = 1;
           d.out = mref(d_ws_ + (src == k.Grs ? k.T1s : k.T2s), k.nb, k.p, k.q, 4ll * k.ldq, cpq);
@@ -761,17 +765,21 @@ osh_status SoapEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
     pd.clear();
     for (const Cls& k : w.cls) {
       // bf16x3: A view (hi, lo, hi) at segment 0, B view (lo, hi, hi) at segment 1
+      // (bf16 gradients: G is exact in hi, one segment hi x hi suffices)
+      const bool exact = grad_dtype_ == kGradBF16;
+      const int ks = exact ? 1 : 3;
+      const size_t b_off = exact ? 0 : 1;
       NsProblemDesc L{};
       const long long cpq = static_cast<long long>(k.p) * 4 * k.ldq;
-      L.a = mref(d_ws_ + k.Gs, k.nb, k.p, 3 * k.ldq, 4ll * k.ldq, cpq);
-      L.b = mref(d_ws_ + k.Gs + 2ull * k.ldq, k.nb, k.p, 3 * k.ldq, 4ll * k.ldq, cpq);
+      L.a = mref(d_ws_ + k.Gs, k.nb, k.p, ks * k.ldq, 4ll * k.ldq, cpq);
+      L.b = mref(d_ws_ + k.Gs + 2ull * b_off * k.ldq, k.nb, k.p, ks * k.ldq, 4ll * k.ldq, cpq);
       L.out = S16(k.l.S, k.nb, k.p, k.p, k.ldp);
       L.scale = d_bscale_;
       L.symmetric = 1;
       NsProblemDesc R{};
       const long long cqp = static_cast<long long>(k.q) * 4 * k.ldp;
-      R.a = mref(d_ws_ + k.Gts, k.nb, k.q, 3 * k.ldp, 4ll * k.ldp, cqp);
-      R.b = mref(d_ws_ + k.Gts + 2ull * k.ldp, k.nb, k.q, 3 * k.ldp, 4ll * k.ldp, cqp);
+      R.a = mref(d_ws_ + k.Gts, k.nb, k.q, ks * k.ldp, 4ll * k.ldp, cqp);
+      R.b = mref(d_ws_ + k.Gts + 2ull * b_off * k.ldp, k.nb, k.q, ks * k.ldp, 4ll * k.ldp, cqp);
       R.out = S16(k.r.S, k.nb, k.q, k.q, k.ldq);
       R.scale = d_bscale_;
       R.symmetric = 1;

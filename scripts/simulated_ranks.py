@@ -74,6 +74,19 @@ def measure_rank(params, cap, plan, r, steps, breakdown):
                 e.step(OptimizerConfig())
             e.sync()
             refresh = timed(e, 1)
+        refresh_modes = None
+        if sh is not None and breakdown:  # one more refresh step, profiled
+            for _ in range(PRECOND_EVERY - 1):
+                e.step(OptimizerConfig())
+            e.sync()
+            e.profile_gemm(True)
+            e.step(OptimizerConfig())
+            e.sync()
+            e.profile_gemm(False)
+            refresh_modes = {}
+            for mode, lms, _fl, _ex, _what in e.gemm_profile_launches():
+                refresh_modes[mode] = round(refresh_modes.get(mode, 0.0) + lms, 3)
+            e.gemm_profile(reset=True)
         modes = None
         if breakdown:
             e.profile_gemm(True)
@@ -84,6 +97,8 @@ def measure_rank(params, cap, plan, r, steps, breakdown):
             for mode, lms, _fl, _ex, _what in e.gemm_profile_launches():
                 modes[mode] = round(modes.get(mode, 0.0) + lms, 3)
             e.gemm_profile(reset=True)
+            if refresh_modes is not None:
+                modes = {"step": modes, "refresh_step": refresh_modes}
         return ms, modes, refresh
 
 
