@@ -456,17 +456,13 @@ __global__ void __launch_bounds__(256) soap_split_kernel(const SoapSplitTask* ta
   }
 }
 
-constexpr int kCholThreads = 1024;
-constexpr int kCholLrs = kSoapCholMaxN + 1;  // row stride of the phase-2 row block in smem
-constexpr size_t kCholSmem =
-    sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 > 32ull * kCholLrs
-                         ? static_cast<size_t>(kSoapCholMaxN) * 33
-                         : 32ull * kCholLrs) +
-    sizeof(float) * 32 * 33;
+constexpr int kCholThreads = 512;
+// panel [n][33] (phase 1) / transposed row block [n][32] (phase 2), diagonal block [32][33]
+constexpr size_t kCholSmem = sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 + 32 * 33);
 
 __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const SoapCholTask* tasks) {
   extern __shared__ float sm[];
-  float* P = sm;                                   // phase 1: panel [m][33]; phase 2: row block [32][kCholLrs]
+  float* P = sm;  // phase 1: panel [m][33]; phase 2: transposed row block [w][32]
   float* D = sm + (kCholSmem / sizeof(float) - 32 * 33);  // diagonal block [32][33]
   const SoapCholTask T = tasks[blockIdx.x];
   const int n = T.n;
@@ -557,12 +553,14 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
     __syncthreads();
   }
   // ---- phase 2: X = L^-1 by row blocks: X[k..k+32) = Ldiag^-1 (E - L[k.., 0:k) X[0:k))
-  float* Lr = P;
+  // The row block is staged transposed, Lt[mm][r], so a thread's 32 row
+  // coefficients of one mm are 8 broadcast 128-bit shared loads.
+  float* Lt = P;
   for (int k = 0; k < np; k += 32) {
     const int w = k + 32;
     for (int e = threadIdx.x; e < 32 * w; e += kCholThreads) {
-      const int r = e / w, mm = e % w;
-      Lr[r * kCholLrs + mm] = mm <= k + r ? C[(k + r) * ld + mm] : 0.f;
+      const int mm = e / 32, r = e % 32;
+      Lt[mm * 32 + r] = mm <= k + r ? C[(k + r) * ld + mm] : 0.f;
     }
     __syncthreads();
     for (int c = threadIdx.x; c < w; c += kCholThreads) {
@@ -572,8 +570,15 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       if (c < k) {
         for (int mm = 0; mm < k; ++mm) {
           const float xv = X[static_cast<long long>(mm) * ld + c];
+          const float4* l4 = reinterpret_cast<const float4*>(Lt + mm * 32);
 #pragma unroll
-          for (int r = 0; r < 32; ++r) x[r] -= Lr[r * kCholLrs + mm] * xv;
+          for (int q = 0; q < 8; ++q) {
+            const float4 l = l4[q];
+            x[4 * q + 0] -= l.x * xv;
+            x[4 * q + 1] -= l.y * xv;
+            x[4 * q + 2] -= l.z * xv;
+            x[4 * q + 3] -= l.w * xv;
+          }
         }
       }
 #pragma unroll
@@ -583,8 +588,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       for (int r = 0; r < 32; ++r) {
         float v = x[r];
 #pragma unroll
-        for (int q = 0; q < r; ++q) v -= Lr[r * kCholLrs + k + q] * x[q];
-        x[r] = v / Lr[r * kCholLrs + k + r];
+        for (int q = 0; q < r; ++q) v -= Lt[(k + q) * 32 + r] * x[q];
+        x[r] = v / Lt[(k + r) * 32 + r];
       }
 #pragma unroll
       for (int r = 0; r < 32; ++r) X[static_cast<long long>(k + r) * ld + c] = x[r];

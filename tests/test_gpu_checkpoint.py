@@ -1,7 +1,8 @@
 """Sharded optimizer-state checkpoint keyed by the plan (osh_ctx_save_state /
 osh_ctx_load_state): resuming from a checkpoint continues
-the trajectory BIT FOR BIT (master, momentum, replica; Muon and Shampoo,
-including the Shampoo statistics, roots and refresh counter), and a
+the trajectory BIT FOR BIT (master, momentum, replica; Muon, Shampoo and
+SOAP, including the Shampoo statistics, roots and refresh counter and the
+SOAP statistics, bases, second moments and step counter), and a
 checkpoint refuses to load under a different plan or rank.
 """
 import numpy as np
@@ -12,7 +13,8 @@ pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from paper_2602_06079_b200 import _lib  # noqa: E402
 from paper_2602_06079_b200 import planner as P  # noqa: E402
-from paper_2602_06079_b200.engine import DistributedMuon, OptimizerConfig, ShampooConfig  # noqa: E402
+from paper_2602_06079_b200.engine import (DistributedMuon, OptimizerConfig, ShampooConfig,  # noqa: E402
+                                          SoapConfig)
 
 pytestmark = pytest.mark.gpu
 SEED = 42
@@ -27,7 +29,9 @@ def params():
 
 def make(ps, ranks, opt, method="alpha-balanced"):
     plan = P.plan_dp(ps, 600_000, ranks, method, "numel", 1.0)
-    kw = dict(optimizer=opt, shampoo=ShampooConfig(block=256, precond_every=2)) if opt == "shampoo" else {}
+    kw = (dict(optimizer=opt, shampoo=ShampooConfig(block=256, precond_every=2)) if opt == "shampoo"
+          else dict(optimizer=opt, shampoo=SoapConfig(block=256, precond_every=2)) if opt == "soap"
+          else {})
     return [DistributedMuon(ps, 600_000, plan, rank=r, comm="none", grad_dtype="f32", **kw)
             for r in range(ranks)]
 
@@ -55,7 +59,7 @@ def snapshot(ctxs, ps):
     return out
 
 
-@pytest.mark.parametrize("opt", ["muon", "shampoo"])
+@pytest.mark.parametrize("opt", ["muon", "shampoo", "soap"])
 @pytest.mark.parametrize("ranks", [1, 2])
 def test_resume_is_bit_exact(tmp_path, opt, ranks):
     ps = params()
