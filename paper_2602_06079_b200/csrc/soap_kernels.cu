@@ -281,9 +281,12 @@ __global__ void __launch_bounds__(kBasisThreads) soap_basis_kernel(const SoapBas
   int* order = reinterpret_cast<int*>(sm + 2 * n);
   // (a) c = shift * ||S||_F (fixed-order fp64 block reduction)
   double ss = 0.0;
-  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += kBasisThreads) {
-    const double x = T.s[(e / n) * T.lds + e % n];
-    ss += x * x;
+  const int warp0 = threadIdx.x >> 5, lane0 = threadIdx.x & 31;
+  for (int r = warp0; r < n; r += kBasisThreads / 32) {  // warp per row, coalesced
+    const float* row = T.s + static_cast<long long>(r) * T.lds;
+    float acc = 0.f;
+    for (int c = lane0; c < n; c += 32) acc += row[c] * row[c];
+    ss += acc;
   }
   const double tot = block_sum(ss, red);
   if (threadIdx.x == 0) s_c = static_cast<float>(static_cast<double>(shift) * sqrt(tot));
@@ -456,13 +459,18 @@ __global__ void __launch_bounds__(256) soap_split_kernel(const SoapSplitTask* ta
   }
 }
 
-constexpr int kCholThreads = 512;
-// panel [n][33] (phase 1) / transposed row block [n][32] (phase 2), diagonal block [32][33]
-constexpr size_t kCholSmem = sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 + 32 * 33);
+constexpr int kCholThreads = 1024;
+constexpr int kCholLrs = kSoapCholMaxN + 1;  // row stride of the phase-2 row block in smem
+// panel [n][33] (phase 1) / row block [32][kCholLrs] (phase 2), diagonal block [32][33]
+constexpr size_t kCholSmem =
+    sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 > 32ull * kCholLrs
+                         ? static_cast<size_t>(kSoapCholMaxN) * 33
+                         : 32ull * kCholLrs) +
+    sizeof(float) * 32 * 33;
 
 __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const SoapCholTask* tasks) {
   extern __shared__ float sm[];
-  float* P = sm;  // phase 1: panel [m][33]; phase 2: transposed row block [w][32]
+  float* P = sm;  // phase 1: panel [m][33]; phase 2: row block [32][kCholLrs]
   float* D = sm + (kCholSmem / sizeof(float) - 32 * 33);  // diagonal block [32][33]
   const SoapCholTask T = tasks[blockIdx.x];
   const int n = T.n;
@@ -472,11 +480,11 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
   float* X = T.linv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the pad [n, np) becomes the identity; L^-1 starts at 0
-  for (long long e = threadIdx.x; e < static_cast<long long>(np) * np; e += kCholThreads) {
-    const int i = static_cast<int>(e / np), j = static_cast<int>(e % np);
-    if (i >= n || j >= n) C[i * ld + j] = i == j ? 1.f : 0.f;
-    X[i * ld + j] = 0.f;
-  }
+  for (int i = warp; i < np; i += kCholThreads / 32)  // warp per row, coalesced
+    for (int j = lane; j < np; j += 32) {
+      if (i >= n || j >= n) C[i * ld + j] = i == j ? 1.f : 0.f;
+      X[i * ld + j] = 0.f;
+    }
   __syncthreads();
   // ---- phase 1: right-looking blocked Cholesky, C = L L^T (lower, in place)
   for (int k0 = 0; k0 < np; k0 += 32) {
@@ -553,14 +561,12 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
     __syncthreads();
   }
   // ---- phase 2: X = L^-1 by row blocks: X[k..k+32) = Ldiag^-1 (E - L[k.., 0:k) X[0:k))
-  // The row block is staged transposed, Lt[mm][r], so a thread's 32 row
-  // coefficients of one mm are 8 broadcast 128-bit shared loads.
-  float* Lt = P;
+  float* Lr = P;
   for (int k = 0; k < np; k += 32) {
     const int w = k + 32;
     for (int e = threadIdx.x; e < 32 * w; e += kCholThreads) {
-      const int mm = e / 32, r = e % 32;
-      Lt[mm * 32 + r] = mm <= k + r ? C[(k + r) * ld + mm] : 0.f;
+      const int r = e / w, mm = e % w;
+      Lr[r * kCholLrs + mm] = mm <= k + r ? C[(k + r) * ld + mm] : 0.f;
     }
     __syncthreads();
     for (int c = threadIdx.x; c < w; c += kCholThreads) {
@@ -570,15 +576,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       if (c < k) {
         for (int mm = 0; mm < k; ++mm) {
           const float xv = X[static_cast<long long>(mm) * ld + c];
-          const float4* l4 = reinterpret_cast<const float4*>(Lt + mm * 32);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 l = l4[q];
-            x[4 * q + 0] -= l.x * xv;
-            x[4 * q + 1] -= l.y * xv;
-            x[4 * q + 2] -= l.z * xv;
-            x[4 * q + 3] -= l.w * xv;
-          }
+          for (int r = 0; r < 32; ++r) x[r] -= Lr[r * kCholLrs + mm] * xv;
         }
       }
 #pragma unroll
@@ -588,8 +587,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       for (int r = 0; r < 32; ++r) {
         float v = x[r];
 #pragma unroll
-        for (int q = 0; q < r; ++q) v -= Lt[(k + q) * 32 + r] * x[q];
-        x[r] = v / Lt[(k + r) * 32 + r];
+        for (int q = 0; q < r; ++q) v -= Lr[r * kCholLrs + k + q] * x[q];
+        x[r] = v / Lr[r * kCholLrs + k + r];
       }
 #pragma unroll
       for (int r = 0; r < 32; ++r) X[static_cast<long long>(k + r) * ld + c] = x[r];
