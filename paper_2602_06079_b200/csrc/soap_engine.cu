@@ -131,8 +131,13 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     return fail(OSH_ERR_OOM, "SoapEngine: one tensor needs " + std::to_string(largest) +
                                  " workspace bytes, budget is " + std::to_string(budget) +
                                  " (lower the block size)");
+  // Waves run back to back here (no overlap to feed), so they are as large
+  // as the budget allows: larger batches fill the GEMMs and give the
+  // one-CTA-per-matrix refresh kernels enough matrices for every SM.
+  // min_waves only matters for bucket-pipelined collectives (NCCL path).
   size_t cap = budget;
-  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total + min_waves - 1) / min_waves));
+  if (min_waves > 1 && min_waves <= 4)
+    cap = std::min(cap, std::max(largest, (total + min_waves - 1) / min_waves));
   std::vector<std::vector<int>> members(1);
   size_t used = 0;
   for (int i = 0; i < n_tensors_; ++i) {
