@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(256) soap_split_kernel(const SoapSplitTask* ta
 }
 
 constexpr int kCholThreads = 1024;
-constexpr int kCholLrs = kSoapCholMaxN + 1;  // row stride of the phase-2 row block in smem
+constexpr int kCholLrs = kSoapCholMaxN + 4;  // row stride of the phase-2 row block (16 B aligned)
 // panel [n][33] (phase 1) / row block [32][kCholLrs] (phase 2), diagonal block [32][33]
 constexpr size_t kCholSmem =
     sizeof(float) * (static_cast<size_t>(kSoapCholMaxN) * 33 > 32ull * kCholLrs
@@ -573,11 +573,18 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       float x[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) x[r] = 0.f;
-      if (c < k) {
-        for (int mm = 0; mm < k; ++mm) {
-          const float xv = X[static_cast<long long>(mm) * ld + c];
+      if (c < k) {  // k is a multiple of 32: four X loads in flight per step,
+                    // the row-block coefficients as broadcast 128-bit loads
+        for (int mm = 0; mm < k; mm += 4) {
+          const float x0 = X[static_cast<long long>(mm) * ld + c];
+          const float x1 = X[static_cast<long long>(mm + 1) * ld + c];
+          const float x2 = X[static_cast<long long>(mm + 2) * ld + c];
+          const float x3 = X[static_cast<long long>(mm + 3) * ld + c];
 #pragma unroll
-          for (int r = 0; r < 32; ++r) x[r] -= Lr[r * kCholLrs + mm] * xv;
+          for (int r = 0; r < 32; ++r) {
+            const float4 l = *reinterpret_cast<const float4*>(Lr + r * kCholLrs + mm);
+            x[r] -= l.x * x0 + l.y * x1 + l.z * x2 + l.w * x3;
+          }
         }
       }
 #pragma unroll
