@@ -127,8 +127,12 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
     return fail(OSH_ERR_OOM, "ShampooEngine: one tensor needs " + std::to_string(largest) +
                                  " workspace bytes, budget is " + std::to_string(budget) +
                                  " (lower the block size)");
+  // Waves run back to back (no overlap to feed): as large as the budget
+  // allows, so the batched GEMMs and Newton iterations see full batches;
+  // min_waves only matters for bucket-pipelined collectives (NCCL path).
   size_t cap = budget;
-  if (min_waves > 1) cap = std::min(cap, std::max(largest, (total + min_waves - 1) / min_waves));
+  if (min_waves > 1 && min_waves <= 4)
+    cap = std::min(cap, std::max(largest, (total + min_waves - 1) / min_waves));
   std::vector<std::vector<int>> members(1);
   size_t used = 0;
   for (int i = 0; i < n_tensors_; ++i) {
