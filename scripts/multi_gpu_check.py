@@ -1,6 +1,6 @@
 """N-GPU correctness of the real NCCL path (RS-v -> owner Muon -> AG-v).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps] [auto|nccl|nvls] [muon|shampoo]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/multi_gpu_check.py [steps] [auto|nccl|nvls] [muon|shampoo|soap]
 
 The optional second argument selects the DP collective path (engine.py
 ``collectives``); the JSON line reports the path the runtime actually took.
@@ -27,11 +27,13 @@ sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 from paper_2602_06079_b200 import planner as P  # noqa: E402
 from oracle import shampoo_oracle as S  # noqa: E402
+from oracle import soap_oracle as SO  # noqa: E402
 from paper_2602_06079_b200.engine import (COLLECTIVE_NAMES, DistributedMuon, OptimizerConfig,  # noqa: E402
-                                          ShampooConfig, nccl_unique_id)
+                                          ShampooConfig, SoapConfig, nccl_unique_id)
 
 SEED = 42
 SCFG = ShampooConfig(block=512, precond_every=2)
+SOCFG = SoapConfig(block=512, precond_every=2)
 
 
 def main():
@@ -56,7 +58,8 @@ def main():
     td.broadcast_object_list(uid, src=0)
     eng = DistributedMuon(params, cap, plan, rank=rank, device=local, comm="nccl", nccl_uid=uid[0],
                           grad_dtype=gdt, collectives=coll, optimizer=opt,
-                          shampoo=SCFG if opt == "shampoo" else None, strategy=strategy)
+                          shampoo=(SCFG if opt == "shampoo" else SOCFG if opt == "soap" else None),
+                          strategy=strategy)
     path = COLLECTIVE_NAMES[eng.info()["collectives"]]
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
@@ -116,22 +119,33 @@ def main():
                                block=SCFG.block, precond_every=SCFG.precond_every,
                                newton_iters=SCFG.newton_iters)
         st = {p.id: S.ShampooTensorState(w[p.id].shape, scfg, S.is_preconditioned(p)) for p in params}
+    if opt == "soap":
+        socfg = SO.SoapConfig(lr=cfg.lr, beta1=cfg.beta, beta2=SOCFG.beta2, shampoo_beta=SOCFG.beta2,
+                              eps=SOCFG.eps, block=SOCFG.block, precond_every=SOCFG.precond_every,
+                              init_iters=SOCFG.init_iters)
+        st = {p.id: SO.SoapTensorState(w[p.id].shape, socfg, SO.is_preconditioned(p)) for p in params}
     for s in range(steps):
         for p in params:
             g = O.reduced_gradient(p.shape, p.id, SEED, s, world)
             if opt == "shampoo":
                 rnorms[s, p.id] = S.shampoo_apply(st[p.id], scfg, w[p.id], g.reshape(w[p.id].shape), s)
+            elif opt == "soap":
+                rnorms[s, p.id] = SO.soap_apply(st[p.id], socfg, w[p.id], g.reshape(w[p.id].shape), s)
             else:
                 rnorms[s, p.id] = O.muon_apply(p.is_matrix, cfg, w[p.id], mom[p.id], g)
     report, ok = {}, True
     for p in params:
         got, ref = weights[p.id].reshape(-1), w[p.id].reshape(-1)
         e_w = float(np.abs(got - ref).max() / np.abs(ref).max())
-        e_n = float(np.max(np.abs(gnorms[:, p.id] - rnorms[:, p.id]) / rnorms[:, p.id]))
+        live = rnorms[:, p.id] > 0  # (SOAP's first call only builds its statistics)
+        e_n = float(np.max(np.abs(gnorms[live, p.id] - rnorms[live, p.id]) / rnorms[live, p.id]))
         tol_w = 2.5e-3 if p.is_matrix else (1e-5 if gdt == "f32" else 1e-3)
         tol_n = (3e-2 if min(p.shape) >= 64 else 1e-1) if p.is_matrix else (1e-5 if gdt == "f32" else 1e-2)
         if opt == "shampoo" and p.is_matrix:
             tol_n = 5e-2
+        if opt == "soap" and p.is_matrix:  # Adam-type steps (tests/test_gpu_soap.py tolerances)
+            tol_n = 5e-2
+            tol_w = cfg.lr / float(np.abs(ref).max())
         rep_ok = all(np.array_equal(g[2][p.id].reshape(-1),
                                     torch.tensor(weights[p.id].reshape(-1)).float().bfloat16().float().numpy())
                      for g in gathered)

@@ -94,6 +94,12 @@ def test_dp2_shampoo_matches_spec():
     assert res["optimizer"] == "shampoo"
 
 
+def test_dp2_soap_matches_spec():
+    for coll in ("auto", "nccl"):  # NVLS-fused prep / apply, and the NCCL RS-v / AG-v path
+        res = _run(2, "multi_gpu_check.py", 4, coll, "soap")
+        assert res["optimizer"] == "soap"
+
+
 def test_dp4_nccl_matches_oracle():
     _run(4, "multi_gpu_check.py", 3, "nccl")
 
