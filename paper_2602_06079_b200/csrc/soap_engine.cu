@@ -57,7 +57,9 @@ size_t block_ws(int p, int q) {
 
 // refresh workspace bytes of one n x n matrix (see SoapEngine::Side)
 size_t refresh_ws(int n, int ld) {
-  return 2 * rup(2ull * n * 4 * ld, 256) + rup(2ull * 4 * ld * ld, 256) + 2 * rup(4ull * ld * ld, 256);
+  const size_t seg = kSoapSplitSegs;
+  return 3 * rup(2ull * n * seg * ld, 256) + rup(2ull * seg * ld * ld, 256) +
+         2 * rup(4ull * ld * ld, 256);
 }
 
 }  // namespace
@@ -223,10 +225,12 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         const size_t n = static_cast<size_t>(sd->n), ld = static_cast<size_t>(sd->ld);
         // S's split is dead once Y = S Q is formed, Y once soap_basis ran:
         // the L^-1 split aliases S's, the Gram matrix aliases Y
+        const size_t sg = kSoapSplitSegs;
         size_t o = 0;
-        sd->Ss = sd->Lc = o; o += rb * rup(2 * n * 4 * ld, 256);
-        sd->Qc = o; o += rb * rup(2 * n * 4 * ld, 256);
-        sd->Qr = o; o += rb * rup(2 * 4 * ld * ld, 256);
+        sd->Sb = sd->La = o; o += rb * rup(2 * n * sg * ld, 256);
+        sd->Qa = o; o += rb * rup(2 * n * sg * ld, 256);
+        sd->Qb = o; o += rb * rup(2 * n * sg * ld, 256);
+        sd->Qrb = o; o += rb * rup(2 * sg * ld * ld, 256);
         sd->Y = sd->C = o; o += rb * rup(4 * ld * ld, 256);
         sd->Li = o; o += rb * rup(4 * ld * ld, 256);
         rws_bytes_ = std::max(rws_bytes_, o);
@@ -317,7 +321,7 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
             t.src = reinterpret_cast<const float*>(st(sd->S)) + nn * (i0 + j);
             t.lds = ld;
             t.rows = t.cols = sd->n;
-            t.col = bf(sd->Ss, j, n * 4 * ld);
+            t.col_b = bf(sd->Sb, j, n * kSoapSplitSegs * ld);
             t.ldd = ld;
             t.tiles_c = (sd->n + kTile - 1) / kTile;
             t.tile_start = ch.tiles_s;
@@ -330,8 +334,9 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
             t.src = reinterpret_cast<const float*>(st(sd->Q)) + nn * (i0 + j);
             t.lds = ld;
             t.rows = t.cols = sd->n;
-            t.col = bf(sd->Qc, j, n * 4 * ld);
-            t.row = bf(sd->Qr, j, 4 * ld * ld);
+            t.col_a = bf(sd->Qa, j, n * kSoapSplitSegs * ld);
+            t.col_b = bf(sd->Qb, j, n * kSoapSplitSegs * ld);
+            t.row_b = bf(sd->Qrb, j, kSoapSplitSegs * ld * ld);
             t.ldd = ld;
             t.tiles_c = (sd->n + kTile - 1) / kTile;
             t.tile_start = ch.tiles_q;
@@ -344,7 +349,7 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
             t.src = f32(sd->Li, j, ld * ld);
             t.lds = ld;
             t.rows = t.cols = sd->n;
-            t.col = bf(sd->Lc, j, n * 4 * ld);
+            t.col_a = bf(sd->La, j, n * kSoapSplitSegs * ld);
             t.ldd = ld;
             t.tiles_c = (sd->n + kTile - 1) / kTile;
             t.tile_start = ch.tiles_l;
@@ -583,7 +588,7 @@ osh_status SoapEngine::begin_step(cudaStream_t s) {
 
 // One side's basis refresh, `iters` times, in sub-batches (soap_engine.cuh):
 // Y = S Q, soap_basis, then CholeskyQR2 on the result. All products are
-// tcgen05 STAT GEMMs (fp32 out) over bf16x3 splits; the Cholesky factor and
+// tcgen05 STAT GEMMs (fp32 out) over bf16x6 splits; the Cholesky factor and
 // its inverse come from soap_chol_inv. Q (fp32) is stored column-major, i.e.
 // its storage rows are Q's columns: Y^T = Q^T S, Gram = Q^T Q and
 // Q' = Q (L^T)^-1  <=>  Q'^T = L^-1 Q^T are row-major products of the storage.
@@ -604,10 +609,11 @@ osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
         if (e == cudaSuccess) e = launch_soap_split(d_split_ + ch.split_q, b, ch.tiles_q, s);
         return e;
       }));
-      {  // Y^T (= Y column-major) = Q^T S: A = Q storage (hi,lo,hi), B = S (lo,hi,hi)
+      const long long sg = kSoapSplitSegs;
+      {  // Y^T (= Y column-major) = Q^T S over the bf16x6 layouts (A: Q storage, B: S)
         NsProblemDesc d{};
-        d.a = mref(d_rws_ + sd.Qc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
-        d.b = mref(d_rws_ + sd.Ss + 2 * ld, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        d.a = mref(d_rws_ + sd.Qa, b, sd.n, sg * sd.ld, sg * ld, n * sg * ld);
+        d.b = mref(d_rws_ + sd.Sb, b, sd.n, sg * sd.ld, sg * ld, n * sg * ld);
         d.out = mref(d_rws_ + sd.Y, b, sd.n, sd.n, ld, nn);
         if (osh_status st = gemm1(d); st != OSH_OK) return st;
       }
@@ -619,8 +625,8 @@ osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
           return launch_soap_split(d_split_ + ch.split_q, b, ch.tiles_q, s);
         }));
         NsProblemDesc g{};  // Gram = Q^T Q (symmetric)
-        g.a = mref(d_rws_ + sd.Qc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
-        g.b = mref(d_rws_ + sd.Qc + 2 * ld, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
+        g.a = mref(d_rws_ + sd.Qa, b, sd.n, sg * sd.ld, sg * ld, n * sg * ld);
+        g.b = mref(d_rws_ + sd.Qb, b, sd.n, sg * sd.ld, sg * ld, n * sg * ld);
         g.out = mref(d_rws_ + sd.C, b, sd.n, sd.n, ld, ld * ld);
         g.symmetric = 1;
         if (osh_status st = gemm1(g); st != OSH_OK) return st;
@@ -629,9 +635,9 @@ osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
           if (e == cudaSuccess) e = launch_soap_split(d_split_ + ch.split_l, b, ch.tiles_l, s);
           return e;
         }));
-        NsProblemDesc u{};  // Q'^T = L^-1 Q^T: A = L^-1 (hi,lo,hi), B = Q storage row-split (lo,hi,hi)
-        u.a = mref(d_rws_ + sd.Lc, b, sd.n, 3 * sd.ld, 4 * ld, n * 4 * ld);
-        u.b = mref(d_rws_ + sd.Qr + 2 * ld * ld, b, 3 * sd.ld, sd.n, ld, 4 * ld * ld);
+        NsProblemDesc u{};  // Q'^T = L^-1 Q^T: A = L^-1 (A layout), B = Q storage rows (B layout)
+        u.a = mref(d_rws_ + sd.La, b, sd.n, sg * sd.ld, sg * ld, n * sg * ld);
+        u.b = mref(d_rws_ + sd.Qrb, b, sg * sd.ld, sd.n, ld, sg * ld * ld);
         u.b_mn_major = 1;
         u.out = mref(Q, b, sd.n, sd.n, ld, nn);
         if (osh_status st = gemm1(u); st != OSH_OK) return st;

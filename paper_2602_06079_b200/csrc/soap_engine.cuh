@@ -18,11 +18,11 @@
 // statistics) amplify operand rounding, so every product feeding them runs in
 // bf16x3 (measured: bf16 operands there move the update 25-45 % away from the
 // fp64 specification, bf16x3 ~1e-3); the back-projection N stays bf16.
-//   [refresh calls]      per side, in sub-batches: bf16x3 splits of S and Q,
-//                        Y = S Q (STAT, bf16x3), soap_basis (shift, order,
+//   [refresh calls]      per side, in sub-batches: bf16x6 splits of S and Q,
+//                        Y = S Q (STAT, bf16x6), soap_basis (shift, order,
 //                        unit columns), CholeskyQR2 = 2 x {Gram Q^T Q (STAT,
-//                        bf16x3), soap_chol_inv (Cholesky + L^-1, one CTA per
-//                        matrix), Q <- L^-1-applied Q (STAT, bf16x3)},
+//                        bf16x6), soap_chol_inv (Cholesky + L^-1, one CTA per
+//                        matrix), Q <- L^-1-applied Q (STAT, bf16x6)},
 //                        V reordered, bf16 / bf16x3 copies of Q
 //   soap_adam            vectors and vocabulary matrices: elementwise Adam
 // Waves run back to back on one stream.
@@ -74,11 +74,12 @@ class SoapEngine : public OptimizerEngine {
     size_t S = 0, Q = 0;           // state: statistics [n][ld] fp32, basis column-major fp32
     int order0 = 0;                // first order entry (d_order_)
     int basis0 = 0;                // first soap_basis task
-    // refresh workspace (d_rws_), by kind for rb matrices: S, Q and L^-1
-    // column-splits [rb][n][4 ld], Q row-split [rb][4 ld][ld], Y [rb][n][ld],
-    // Gram and L^-1 [rb][ld][ld]
+    // refresh workspace (d_rws_), by kind for rb matrices (bf16x6 layouts,
+    // soap_kernels.cuh): S (B), Q (A and B) and L^-1 (A) column layouts
+    // [rb][n][6 ld], Q row B layout [rb][6 ld][ld], Y / Gram and L^-1 fp32
+    // [rb][ld][ld]
     int rb = 1;
-    size_t Ss = 0, Qc = 0, Lc = 0, Qr = 0, Y = 0, C = 0, Li = 0;
+    size_t Sb = 0, Qa = 0, Qb = 0, La = 0, Qrb = 0, Y = 0, C = 0, Li = 0;
     std::vector<RChunk> chunks;
   };
   struct Cls {                     // blocks of one (p, q) inside one wave

@@ -438,22 +438,29 @@ __global__ void __launch_bounds__(256) soap_split_kernel(const SoapSplitTask* ta
     for (int j = 0; j < kTile / 32; ++j) {
       const int c = c0 + tx + 32 * j;
       const float v = (r < T.rows && c < T.cols) ? T.src[static_cast<size_t>(r) * T.lds + c] : 0.f;
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-      if (T.col != nullptr && r < T.rows) {
-        __nv_bfloat16* d = T.col + static_cast<size_t>(r) * 4 * T.ldd + c;
-        d[0] = hi;
-        d[T.ldd] = lo;
-        d[2 * T.ldd] = hi;
-        d[3 * T.ldd] = hi;
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      const float r1 = v - __bfloat162float(h);
+      const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 l = __float2bfloat16_rn(r1 - __bfloat162float(m));
+      const __nv_bfloat16 sa[6] = {h, m, h, l, m, h};
+      const __nv_bfloat16 sb[6] = {h, h, m, h, m, l};
+      if (r < T.rows) {
+        if (T.col_a != nullptr) {
+          __nv_bfloat16* d = T.col_a + static_cast<size_t>(r) * 6 * T.ldd + c;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) d[q * T.ldd] = sa[q];
+        }
+        if (T.col_b != nullptr) {
+          __nv_bfloat16* d = T.col_b + static_cast<size_t>(r) * 6 * T.ldd + c;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) d[q * T.ldd] = sb[q];
+        }
       }
-      if (T.row != nullptr) {
+      if (T.row_b != nullptr) {
         const size_t seg = static_cast<size_t>(T.ldd) * T.ldd;
-        __nv_bfloat16* d = T.row + static_cast<size_t>(r) * T.ldd + c;
-        d[0] = hi;
-        d[seg] = lo;
-        d[2 * seg] = hi;
-        d[3 * seg] = hi;
+        __nv_bfloat16* d = T.row_b + static_cast<size_t>(r) * T.ldd + c;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) d[q * seg] = sb[q];
       }
     }
   }

@@ -21,7 +21,7 @@
 //   soap_qcast     fp32 column-major Q -> bf16 Q^T column-split, Q row-major,
 //                  Q row-split
 //   soap_eye       Q = I (column-major fp32, zero padding)
-//   soap_split     fp32 matrix -> bf16x3 column / row splits (refresh operands)
+//   soap_split     fp32 matrix -> bf16x6 column / row splits (refresh operands)
 //   soap_chol_inv  C = L L^T and L^-1 (blocked right-looking Cholesky, then a
 //                  row-block forward substitution), one CTA per matrix
 #pragma once
@@ -114,16 +114,22 @@ struct SoapQcastTask {    // fp32 column-major Q (n x n) -> bf16 copies (each nu
   int tiles_c, pad2_;
 };
 
-struct SoapSplitTask {    // fp32 [rows][lds] -> bf16x3 copies (each nullable), pads 0
+// bf16x6 (~24-bit) split for the basis refresh, whose power iteration
+// amplifies operand rounding: x = h + m + l (three bf16 terms); the A layout
+// stores segments (h, m, h, l, m, h) and the B layout (h, h, m, h, m, l), so
+// one contraction over K = 6 seg sums h*h + m*h + h*m + l*h + m*m + h*l.
+struct SoapSplitTask {    // fp32 [rows][lds] -> bf16x6 copies (each nullable), pads 0
   const float* src;
   long long lds;
   int rows, cols;         // logical size; tiles cover [rup(rows,64)] x [rup(cols,64)]
-  __nv_bfloat16* col;     // column-split [rows][4 ldd]
-  __nv_bfloat16* row;     // row-split    [4 ldd][ldd] (rows up to ldd, pads 0)
+  __nv_bfloat16* col_a;   // column A layout [rows][6 ldd]
+  __nv_bfloat16* col_b;   // column B layout [rows][6 ldd]
+  __nv_bfloat16* row_b;   // row B layout    [6 ldd][ldd] (rows up to ldd, pads 0)
   long long ldd;
   long long tile_start;
   int tiles_c, pad_;
 };
+constexpr int kSoapSplitSegs = 6;
 
 // Batched Cholesky + triangular inverse, one CTA per matrix (n <= 1024):
 // C (SPD, fp32 [ld][ld], only [n][n] meaningful; the pad is made the identity)

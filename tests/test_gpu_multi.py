@@ -95,8 +95,9 @@ def test_dp2_shampoo_matches_spec():
 
 
 def test_dp2_soap_matches_spec():
-    for coll in ("auto", "nccl"):  # NVLS-fused prep / apply, and the NCCL RS-v / AG-v path
-        res = _run(2, "multi_gpu_check.py", 4, coll, "soap")
+    # NVLS-fused prep / apply and the NCCL RS-v / AG-v path; f32 and bf16 gradients
+    for coll, gdt in (("auto", "f32"), ("nccl", "f32"), ("auto", "bf16")):
+        res = _run(2, "multi_gpu_check.py", 4, coll, "soap", "-", "sharded", gdt)
         assert res["optimizer"] == "soap"
 
 
