@@ -118,6 +118,10 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   n_tensors_ = static_cast<int>(tensors.size());
   grad_dtype_ = grad_dtype;
   step_ = -1;
+  // bf16 gradients are exact in the hi segment, unless NVLS sums the ranks'
+  // bf16 gradients in fp32 on the way in (multimem.ld_reduce)
+  exact_grad_ = grad_dtype == kGradBF16;
+  for (const MuonTensorDesc& t : tensors) exact_grad_ = exact_grad_ && !t.g_mc;
   auto pre = [&](const MuonTensorDesc& t) { return t.is_matrix && !t.vocab_space; };
 
   // ---- waves: consecutive tensors (declaration order) within the budget
@@ -712,7 +716,7 @@ osh_status SoapEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
         for (size_t src : {k.Grs, k.Mrs}) {
           // bf16 gradients are exact in hi (lo = 0): T1 needs only the
           // (lo, hi) x (hi, hi) segment pairs, K = 2 ldp
-          const int segs = (src == k.Grs && grad_dtype_ == kGradBF16) ? 2 : 3;
+          const int segs = (src == k.Grs && exact_grad_) ? 2 : 3;
           const int a0 = 3 - segs;  // first A segment: 0 (hi) or 1 (lo)
           NsProblemDesc d{};
           d.a = mref(d_state_ + k.QLts + 2ull * a0 * k.ldp, k.nb, k.p, segs * k.ldp, 4ll * k.ldp,
@@ -777,7 +781,7 @@ osh_status SoapEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
     for (const Cls& k : w.cls) {
       // bf16x3: A view (hi, lo, hi) at segment 0, B view (lo, hi, hi) at segment 1
       // (bf16 gradients: G is exact in hi, one segment hi x hi suffices)
-      const bool exact = grad_dtype_ == kGradBF16;
+      const bool exact = exact_grad_;
       const int ks = exact ? 1 : 3;
       const size_t b_off = exact ? 0 : 1;
       NsProblemDesc L{};

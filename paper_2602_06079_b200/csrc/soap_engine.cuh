@@ -136,6 +136,7 @@ class SoapEngine : public OptimizerEngine {
   int* d_slot_count_ = nullptr;
   int* d_slot_target_ = nullptr;
   int max_nb_ = 1;
+  bool exact_grad_ = false;       // gradients exact in bf16 (statistics / T1 fast path)
 };
 
 }  // namespace osh
