@@ -118,10 +118,9 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   n_tensors_ = static_cast<int>(tensors.size());
   grad_dtype_ = grad_dtype;
   step_ = -1;
-  // bf16 gradients are exact in the hi segment, unless NVLS sums the ranks'
-  // bf16 gradients in fp32 on the way in (multimem.ld_reduce)
+  // bf16 gradients are exact in the hi segment (NVLS too: multimem.ld_reduce
+  // accumulates in fp32 but returns the sum as bf16x2)
   exact_grad_ = grad_dtype == kGradBF16;
-  for (const MuonTensorDesc& t : tensors) exact_grad_ = exact_grad_ && !t.g_mc;
   auto pre = [&](const MuonTensorDesc& t) { return t.is_matrix && !t.vocab_space; };
 
   // ---- waves: consecutive tensors (declaration order) within the budget

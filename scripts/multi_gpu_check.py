@@ -128,9 +128,12 @@ def main():
         for p in params:
             if opt == "soap" and gdt == "bf16":
                 # SOAP's basis is ill-conditioned in its statistics (DESIGN.md
-                # 3c): the spec gets the same bf16-rounded rank gradients
-                g = sum(torch.from_numpy(O.synth_gradient(p.shape, p.id, SEED, s, r))
-                        .bfloat16().double().numpy() for r in range(world))
+                # 3c): the spec gets the GPU's input, the bf16 rank gradients
+                # summed in fp32 and rounded to bf16 (multimem.ld_reduce
+                # .acc::f32 .bf16x2 and NCCL's bf16 reduction alike)
+                acc = sum(torch.from_numpy(O.synth_gradient(p.shape, p.id, SEED, s, r))
+                          .bfloat16().float() for r in range(world))
+                g = acc.bfloat16().double().numpy()
             else:
                 g = O.reduced_gradient(p.shape, p.id, SEED, s, world)
             if opt == "shampoo":
