@@ -592,6 +592,12 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
       if (!queued[static_cast<size_t>(b)]) ctx->h2d_bucket_order.push_back(b);
     if (!reorder || distributed(ctx))  // NCCL RS-v waits per bucket in bucket order
       for (int b = 0; b < nbk; ++b) ctx->h2d_bucket_order[static_cast<size_t>(b)] = b;
+    ctx->wave_done_buckets.assign(static_cast<size_t>(nw), {});
+    for (int b = 0; b < nbk; ++b)  // (buckets no wave touches go with the last wave)
+      ctx->wave_done_buckets[static_cast<size_t>(done_at[static_cast<size_t>(b)] >= 0
+                                                     ? done_at[static_cast<size_t>(b)]
+                                                     : nw - 1)]
+          .push_back(b);
     ctx->wave_final_upto.assign(static_cast<size_t>(nw), -1);
     for (int w = 0; w < nw; ++w) {
       int upto = -1;
@@ -818,9 +824,23 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
         OSH_CUDA_TRY(cudaStreamWaitEvent(cs, (*ev)[b], 0));
     return OSH_OK;
   };
-  // after wave w every bucket before the next wave's first one is final
+  // after wave w: the buckets it completes leave at once (one rank / no
+  // cross-rank barrier needed); NVLS copies bucket prefixes behind per-bucket
+  // barriers issued in the same order on every rank
   auto wave_done = [&](int w) -> osh_status {
     OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    if (io.replica_out != nullptr && !io.nvls_out) {
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->wave_end[w], 0));
+      for (const int b : ctx->wave_done_buckets[static_cast<size_t>(w)]) {
+        const int64_t b0 = ctx->bucket_base[b];
+        const int64_t b1 = b + 1 < nb ? ctx->bucket_base[b + 1] : ctx->total_numel;
+        OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<__nv_bfloat16*>(io.replica_out) + b0,
+                                     ctx->replica + b0, 2 * static_cast<size_t>(b1 - b0),
+                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
+      }
+      if (w + 1 == nw) io.d2h_next = nb;  // every bucket is out
+      return OSH_OK;
+    }
     return d2h_buckets(ctx, io, w + 1 < nw ? ctx->wave_final_upto[static_cast<size_t>(w)] : nb - 1,
                        ctx->wave_end[w]);
   };

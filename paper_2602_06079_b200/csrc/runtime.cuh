@@ -83,6 +83,7 @@ struct osh_ctx {
   // bucket <= B is final once the wave is done; and the order in which a
   // single rank's pipelined H2D copies the buckets (first need first)
   std::vector<int> wave_final_upto;
+  std::vector<std::vector<int>> wave_done_buckets;  // per wave: buckets it completes
   std::vector<int> h2d_bucket_order;
   // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
   // the update kernels reduce / broadcast through their multicast addresses
