@@ -257,9 +257,10 @@ osh_status osh_ctx_set_collectives(osh_ctx* ctx, int32_t mode);
  *                    iteration + CholeskyQR2, all on this library's own
  *                    kernels; oracle/soap_oracle.py). The
  *                    osh_shampoo_cfg fields read: beta2 (second moment and
- *                    statistics decay, 0.95), eps (Adam epsilon, 1e-8), block,
- *                    precond_every, newton_iters = power iterations of the
- *                    first refresh (4). osh_muon_cfg supplies lr and beta1.
+ *                    statistics decay, 0.95), eps (Adam epsilon, 1e-8), block
+ *                    (multiple of 64, <= 1024), precond_every, newton_iters =
+ *                    power iterations of the first refresh (4). osh_muon_cfg
+ *                    supplies lr and beta1.
  * Shampoo and SOAP need tp_size == 1. */
 typedef struct osh_shampoo_cfg {
   double beta2;           /* statistics decay (0.95) */

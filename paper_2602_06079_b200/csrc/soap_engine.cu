@@ -111,8 +111,8 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
                              size_t budget, int min_waves, bool /*double_buffer*/) {
   release();
   const int B = cfg_.block;
-  if (B < 64 || B % 64 != 0 || B > 4096)
-    return fail(OSH_ERR_CONFIG, "SOAP block size must be a multiple of 64 in [64, 4096]");
+  if (B < 64 || B % 64 != 0 || B > kSoapCholMaxN)  // (one CTA factors one block's statistics)
+    return fail(OSH_ERR_CONFIG, "SOAP block size must be a multiple of 64 in [64, 1024]");
   if (cfg_.precond_every < 1 || cfg_.init_iters < 1)
     return fail(OSH_ERR_CONFIG, "SOAP precond_every and init_iters must be >= 1");
   n_tensors_ = static_cast<int>(tensors.size());

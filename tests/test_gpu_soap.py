@@ -123,6 +123,7 @@ def test_soap_sharded_equals_replicated_bitwise():
 def test_soap_rejects_bad_config():
     ps = params()
     plan = P.plan_dp(ps, 10 ** 9, 1, "alpha-balanced", "numel", 1.0)
-    with pytest.raises(Exception):
-        DistributedMuon(ps, 10 ** 9, plan, comm="none", optimizer="soap",
-                        shampoo=SoapConfig(block=100))
+    for block in (100, 2048):  # not a multiple of 64 / above the 1024 factorization limit
+        with pytest.raises(Exception):
+            DistributedMuon(ps, 10 ** 9, plan, comm="none", optimizer="soap",
+                            shampoo=SoapConfig(block=block))
