@@ -407,6 +407,7 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         pt.ldq = k.ldq;
         pt.ldp = k.ldp;
         pt.vec = (t.cols % 8 == 0 && g.c0 % 8 == 0 && g.q % 8 == 0 && a16(t.g) && a16(t.m)) ? 1 : 0;
+        pt.exact = exact_grad_ ? 1 : 0;
         if (t.g_mc && !pt.vec) return fail(OSH_ERR_UNSUPPORTED, "NVLS path needs the 128-bit layout");
         pt.tiles_c = (g.q + kTile - 1) / kTile;
         pt.tile_start = w.prep.tiles;

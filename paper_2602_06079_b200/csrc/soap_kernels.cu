@@ -88,9 +88,10 @@ __global__ void __launch_bounds__(256) soap_prep_kernel(const SoapPrepTask* task
     const uint4 seg_m[4] = {mhi, mlo, mhi, mhi};
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      if (r < T.p)  // (the column split has p rows; the row splits ldp)
+      if (r < T.p && (!T.exact || s == 0))  // (the column split has p rows; the row splits ldp)
         *reinterpret_cast<uint4*>(T.gs + static_cast<size_t>(r) * 4 * T.ldq + s * T.ldq + c) = seg_g[s];
-      *reinterpret_cast<uint4*>(T.grs + (static_cast<size_t>(s) * T.ldp + r) * T.ldq + c) = seg_g[s];
+      if (!T.exact || s >= 2)
+        *reinterpret_cast<uint4*>(T.grs + (static_cast<size_t>(s) * T.ldp + r) * T.ldq + c) = seg_g[s];
       *reinterpret_cast<uint4*>(T.mrs + (static_cast<size_t>(s) * T.ldp + r) * T.ldq + c) = seg_m[s];
     }
 #pragma unroll
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(256) soap_prep_kernel(const SoapPrepTask* task
       const __nv_bfloat16 hi = __float2bfloat16_rn(th[lr][lc]);
       const __nv_bfloat16 lo = __float2bfloat16_rn(tl[lr][lc]);
       row[r] = hi;
+      if (T.exact) continue;
       row[T.ldp + r] = lo;
       row[2 * T.ldp + r] = hi;
       row[3 * T.ldp + r] = hi;

@@ -54,7 +54,9 @@ struct SoapPrepTask {
   __nv_bfloat16* mrs;     // M   row-split    [4 ldp][ldq]
   long long ldq, ldp;
   long long tile_start;   // prefix over 64x64 tiles of ldp x ldq (pads written 0)
-  int tiles_c, pad_;
+  int tiles_c;
+  int exact;              // gradients exact in bf16: only the segments the fast
+                          // path reads are written (G / G^T hi, G rows 2-3)
 };
 
 struct SoapRotTask {      // one class: nb blocks of [p][ldq] (elements = nb * p * ldq)
