@@ -375,11 +375,24 @@ def run_ours(a, dist: Dist):
 
     # e2e through the C ABI with host buffers (pinned)
     e2e = None
+    e2e_skip = None
     if not a.no_e2e and a.e2e_steps > 0:
         total = info["total_numel"]
         gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
-        hg = torch.empty(total, dtype=gdt, pin_memory=True)
-        hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
+        # every rank pins a full gradient and replica (N x 29 GB at 8B bf16):
+        # all ranks take the e2e leg together or none does
+        try:
+            hg = torch.empty(total, dtype=gdt, pin_memory=True)
+            hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
+            pinned = True
+        except RuntimeError as exc:  # pinned host memory exhausted
+            hg = hr = None
+            pinned = str(exc).splitlines()[0][:200]
+        flags = dist.gather(pinned)
+        if any(f is not True for f in flags):
+            e2e_skip = next(f for f in flags if f is not True)
+            del hg, hr
+    if not a.no_e2e and a.e2e_steps > 0 and e2e_skip is None:
         # host gradients: synthetic bf16/f32 values staged through the device in
         # 256M-element chunks (outside the timed region)
         chunk = 1 << 28
@@ -400,6 +413,7 @@ def run_ours(a, dist: Dist):
         del hg, hr
 
     rec = {"ms": ms, "prof": prof, "by_mode": by_mode, "last": last, "info": info, "e2e": e2e,
+           "e2e_skip": e2e_skip,
            "owned_numel": info["owned_numel"],
            "ns_flops": (info["ns_flops_per_iter"] * 5 if a.optimizer == "muon"
                         else float(last["gemm_flops"])),
@@ -486,6 +500,9 @@ def run_ours(a, dist: Dist):
     }
     if clock:
         out["clocks"] = clock
+    if allrec[0]["e2e_skip"] is not None:
+        out["e2e"] = {"value": None, "unit": "ms", "skipped": "pinned host buffers unavailable: "
+                      + str(allrec[0]["e2e_skip"])}
     if allrec[0]["e2e"]:
         e = max(r["e2e"]["e2e_ms"] for r in allrec)
         out["e2e"] = {"value": round(e, 3), "unit": "ms",
