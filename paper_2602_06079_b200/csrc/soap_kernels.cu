@@ -542,6 +542,12 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       while ((ti + 1) * (ti + 2) / 2 <= id) ++ti;
       while (ti * (ti + 1) / 2 > id) --ti;
       const int tj = id - ti * (ti + 1) / 2;
+      // the tile's current values are loaded first, so their (L2 / HBM)
+      // latency overlaps the 512 FMAs below
+      float4 cur[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        cur[a] = *reinterpret_cast<const float4*>(C + (k0 + 32 + ti * 4 + a) * ld + k0 + 32 + tj * 4);
       float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -558,12 +564,13 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
           for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a) {
+        const long long i = k0 + 32 + ti * 4 + a, j0 = k0 + 32 + tj * 4;
+        const float cv[4] = {cur[a].x, cur[a].y, cur[a].z, cur[a].w};
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const long long i = k0 + 32 + ti * 4 + a, j = k0 + 32 + tj * 4 + b;
-          if (i >= j) C[i * ld + j] -= acc[a][b];
-        }
+        for (int b = 0; b < 4; ++b)
+          if (i >= j0 + b) C[i * ld + j0 + b] = cv[b] - acc[a][b];
+      }
     }
     __syncthreads();
   }
