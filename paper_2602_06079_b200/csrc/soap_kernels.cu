@@ -589,11 +589,17 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       for (int r = 0; r < 32; ++r) x[r] = 0.f;
       if (c < k) {  // k is a multiple of 32: four X loads in flight per step,
                     // the row-block coefficients as broadcast 128-bit loads
+        // software pipeline: the next four X values load while this step's
+        // 128 FMAs run
+        float n0 = X[c], n1 = X[ld + c], n2 = X[2 * ld + c], n3 = X[3 * ld + c];
         for (int mm = 0; mm < k; mm += 4) {
-          const float x0 = X[static_cast<long long>(mm) * ld + c];
-          const float x1 = X[static_cast<long long>(mm + 1) * ld + c];
-          const float x2 = X[static_cast<long long>(mm + 2) * ld + c];
-          const float x3 = X[static_cast<long long>(mm + 3) * ld + c];
+          const float x0 = n0, x1 = n1, x2 = n2, x3 = n3;
+          if (mm + 4 < k) {
+            n0 = X[static_cast<long long>(mm + 4) * ld + c];
+            n1 = X[static_cast<long long>(mm + 5) * ld + c];
+            n2 = X[static_cast<long long>(mm + 6) * ld + c];
+            n3 = X[static_cast<long long>(mm + 7) * ld + c];
+          }
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
             const float4 l = *reinterpret_cast<const float4*>(Lr + r * kCholLrs + mm);
