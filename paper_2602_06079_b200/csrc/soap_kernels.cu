@@ -590,9 +590,12 @@ __global__ void __launch_bounds__(kCholThreads, 1) soap_chol_inv_kernel(const So
       if (c < k) {  // k is a multiple of 32: four X loads in flight per step,
                     // the row-block coefficients as broadcast 128-bit loads
         // software pipeline: the next four X values load while this step's
-        // 128 FMAs run
-        float n0 = X[c], n1 = X[ld + c], n2 = X[2 * ld + c], n3 = X[3 * ld + c];
-        for (int mm = 0; mm < k; mm += 4) {
+        // 128 FMAs run. X is lower triangular (X[mm][c] = 0 for mm < c), so
+        // the contraction starts at row c (exactly: the skipped terms are 0)
+        const int m0 = c & ~3;
+        float n0 = X[static_cast<long long>(m0) * ld + c], n1 = X[static_cast<long long>(m0 + 1) * ld + c];
+        float n2 = X[static_cast<long long>(m0 + 2) * ld + c], n3 = X[static_cast<long long>(m0 + 3) * ld + c];
+        for (int mm = m0; mm < k; mm += 4) {
           const float x0 = n0, x1 = n1, x2 = n2, x3 = n3;
           if (mm + 4 < k) {
             n0 = X[static_cast<long long>(mm + 4) * ld + c];
