@@ -47,7 +47,8 @@ def parse_args():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--alpha", default="auto",
                     help="alpha of the alpha-balanced plan, or 'auto': the alpha of {1, .75, .5, "
-                         ".25, 0} with the lowest planned per-rank NS-flop max/mean (ties keep 1)")
+                         ".25, 0} with the lowest planned per-rank NS-flop max/mean, kept at 1 "
+                         "unless another plans > 1.5 %% better (planner.choose_alpha)")
     ap.add_argument("--method", default="alpha-balanced",
                     choices=["alpha-balanced", "atomic-ownership"],
                     help="executable (atomic) partition; equal-chunk splits tensors, see "
@@ -438,7 +439,8 @@ def run_ours(a, dist: Dist):
     achieved = p0["flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
     achieved_exec = p0["exec_flops"] / (p0["ms"] * 1e-3) / 1e12 if p0["ms"] > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
-    alpha_src = " (auto: lowest planned NS-flop max/mean of {1,.75,.5,.25,0})" if a.alpha_auto else ""
+    alpha_src = (" (auto: planner.choose_alpha over {1,.75,.5,.25,0} by planned NS-flop max/mean)"
+                 if a.alpha_auto else "")
     out = {
         "metric": (METRIC if a.optimizer == "muon" else METRIC_SHAMPOO if a.optimizer == "shampoo"
                    else METRIC_SHAMPOO.replace("Shampoo", "SOAP")),
