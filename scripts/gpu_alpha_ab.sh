@@ -1,5 +1,5 @@
 # Same-box A/B of the plan's alpha at N=4 (NVLS): alpha = 1 (paper default)
-# against the planner-chosen alpha (0.25 at R=4), interleaved.
+# against alpha = 0.25 (the best planned NS-flop balance at R=4), interleaved.
 mkdir -p gpurun_out
 : > gpurun_out/alpha_ab.jsonl
 for al in 1 auto 1 auto; do

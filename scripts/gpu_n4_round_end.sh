@@ -1,4 +1,4 @@
-# 4-GPU round-end evidence: default bench (alpha auto -> 0.25 at R=4), the
+# 4-GPU round-end evidence: default bench (alpha auto), the
 # SOAP step at DP4 (NVLS), and the 4-rank multi-GPU checks.
 mkdir -p gpurun_out
 run() { timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 "$@"; }
