@@ -2,7 +2,7 @@
 # against alpha = 0.25 (the best planned NS-flop balance at R=4), interleaved.
 mkdir -p gpurun_out
 : > gpurun_out/alpha_ab.jsonl
-for al in 1 auto 1 auto; do
+for al in 1 0.25 1 0.25; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29523 bench.py --gpus 4 --no-cpu-baseline --no-e2e --steps 10 --warmup 3 --alpha $al 2>/dev/null | grep '^{' >> gpurun_out/alpha_ab.jsonl
 done
 python -c "
