@@ -119,3 +119,14 @@ def test_ragged_blocks_cover_the_tensor():
     for s in range(4):
         S.soap_apply(st, cfg, w, rng.standard_normal((130, 70)), s)
     assert np.all(np.isfinite(w)) and np.all(w != 0.0)
+
+
+def test_bf16_rounding_matches_torch():
+    """The precision model's bf16 rounding (oracle.soap_oracle._bf16) is
+    round-to-nearest-even, as the GPU's __float2bfloat16_rn."""
+    torch = __import__("pytest").importorskip("torch")
+    rng = np.random.default_rng(6)
+    x = np.concatenate([rng.standard_normal(10000) * 10.0 ** rng.integers(-8, 8, 10000),
+                        [0.0, -0.0, 1.0, 1.00390625, 1.01171875, -3.5]])
+    ref = torch.from_numpy(x.astype(np.float32)).bfloat16().double().numpy()
+    np.testing.assert_array_equal(S._bf16(x), ref)
