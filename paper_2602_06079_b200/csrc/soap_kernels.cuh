@@ -87,7 +87,7 @@ struct SoapBasisTask {    // one statistics matrix S (n x n) and its basis Q
   const float* s;         // [n][lds] fp32 (symmetric)
   long long lds;
   float* q;               // column-major [n][ldq]: column j at q + j * ldq
-  float* y;               // S Q (column-major, same ld), from cuBLAS
+  float* y;               // S Q (column-major, same ld), from this library's tcgen05 STAT GEMM
   long long ldq;
   int* order;             // [n] out: new column k = old column order[k]
   int n, pad_;

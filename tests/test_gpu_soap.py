@@ -15,7 +15,7 @@ cuSOLVER CholeskyQR2):
   vectors / vocabulary matrices (elementwise Adam in fp32)              <= 1e-4
 The products that feed the rotated Adam ratio and the basis (statistics,
 G', M') run in bf16x3 on the GPU; with plain bf16 there the update moved
-25-45 % away from this specification (scripts/debug_soap.py).
+25-45 % away from this specification (a numpy sensitivity study, in the round-1 history).
 Runs 5 calls with a basis refresh every 2 (the first call only builds the
 statistics and the initial 4-iteration basis; two one-iteration refreshes
 with the V reordering follow), block 256 so tensors split into full and
