@@ -292,6 +292,41 @@ enum { OSH_STRAT_SHARDED = 0, OSH_STRAT_SC = 1, OSH_STRAT_NV_LAYERWISE = 2 };
 osh_status osh_ctx_set_strategy(osh_ctx* ctx, int32_t strategy, const int32_t* layer_of,
                                 int32_t n, const osh_cost_model* cost);
 osh_status osh_shampoo_cfg_default(osh_shampoo_cfg* out);
+
+/* The data-parallel collective schedule of one step (csrc/comm_schedule.hpp):
+ * every NCCL operation the runtime issues, in issue order, identical on every
+ * rank (NCCL requires it). Replaces the reference's analytic RS-v / AG-v
+ * (collective.hpp:49-76, simulate.hpp:199-253) with the executed exchange.
+ *   kind   OSH_OP_REDUCE     root receives the sum of [offset, offset+count) of
+ *                            every rank's flat gradient buffer at element
+ *                            dst_offset of its reduced-slice buffer (RS-v leg)
+ *          OSH_OP_BROADCAST  root's [offset, offset+count) of the bf16 replica
+ *                            is copied in place to every rank (AG-v leg)
+ *          OSH_OP_ALLREDUCE  in-place sum of a whole gradient bucket (SC /
+ *                            NV-layerwise baselines; root = -1)
+ *   phase  OSH_PHASE_RS (before the update) / OSH_PHASE_AG (after)
+ *   group  operations sharing a group id are issued inside one
+ *          ncclGroupStart / ncclGroupEnd
+ * With the NVLS path the same reduce / broadcast pairs run inside the update
+ * kernels (multimem.ld_reduce / multimem.st) instead of as NCCL calls. */
+enum { OSH_OP_REDUCE = 0, OSH_OP_BROADCAST = 1, OSH_OP_ALLREDUCE = 2 };
+enum { OSH_PHASE_RS = 0, OSH_PHASE_AG = 1 };
+typedef struct osh_coll_op {
+  int32_t kind, phase, bucket, root, group, reserved_;
+  int64_t offset, count, dst_offset;
+} osh_coll_op;
+/* Pure function of the model, bucket capacity and plan (no GPU needed):
+ * the schedule a ctx with this layout and strategy issues. layer_of / cost
+ * are read for OSH_STRAT_NV_LAYERWISE only. With out == NULL only *n_out is
+ * written; otherwise cap must cover the schedule. */
+osh_status osh_comm_schedule(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                             int32_t ranks, const int64_t* cuts, int32_t n_buckets,
+                             int32_t strategy, const int32_t* layer_of,
+                             const osh_cost_model* cost, osh_coll_op* out, int32_t cap,
+                             int32_t* n_out);
+/* The schedule this ctx issues (empty for a single rank / OSH_COMM_NONE). */
+osh_status osh_ctx_comm_schedule(osh_ctx* ctx, osh_coll_op* out, int32_t cap, int32_t* n_out);
+
 osh_status osh_ctx_set_optimizer(osh_ctx* ctx, int32_t kind, const osh_shampoo_cfg* cfg);
 
 /* Installs the parameter list (ids dense 0..n-1, declaration order), the

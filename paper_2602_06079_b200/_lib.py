@@ -94,6 +94,12 @@ class GemmProblem(ctypes.Structure):
                 ("out_seg", c_int32)]
 
 
+class CollOp(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("phase", c_int32), ("bucket", c_int32), ("root", c_int32),
+                ("group", c_int32), ("reserved_", c_int32), ("offset", c_int64),
+                ("count", c_int64), ("dst_offset", c_int64)]
+
+
 _lib = None
 
 
@@ -174,6 +180,14 @@ def _declare(L: ctypes.CDLL) -> None:
         ("osh_ctx_profile_gemm", c_int32, c_void_p, c_int32),
         ("osh_gemm_profile_read", c_int32, c_void_p, POINTER(GemmProfile), c_int32),
         ("osh_gemm_profile_dump", c_int32, c_void_p, ctypes.c_char_p, c_size_t, POINTER(c_size_t)),
+        ("osh_comm_schedule", c_int32, POINTER(ParamDesc), c_int32, c_int64, c_int32,
+         POINTER(c_int64), c_int32, c_int32, c_void_p, c_void_p, POINTER(CollOp), c_int32,
+         POINTER(c_int32)),
+        ("osh_ctx_comm_schedule", c_int32, c_void_p, POINTER(CollOp), c_int32, POINTER(c_int32)),
+        ("osh_write_state", c_int32, c_void_p, c_int32, c_int32, POINTER(c_float)),
+        ("osh_muon_apply_host", c_int32, c_int32, POINTER(ParamDesc), POINTER(MuonCfgC),
+         POINTER(c_double), POINTER(c_double), POINTER(c_double), POINTER(c_double)),
+        ("osh_newton_schulz_host", c_int32, c_int32, POINTER(c_double), c_int64, c_int64, c_int32),
     ]
     for name, restype, *args in optional:
         if hasattr(L, name):

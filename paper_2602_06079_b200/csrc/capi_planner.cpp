@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "optishard/optishard.hpp"
+#include "comm_schedule.hpp"
 #include "osh.h"
 #include "status.hpp"
 
@@ -224,6 +225,49 @@ osh_status osh_plan_tp_serialize(const int32_t* item_ids, const uint64_t* item_c
     copy_text(serialize_tp_plan(build_micro_groups(std::move(items), ranks, c_max,
                                                    static_cast<CostKind>(cost_kind))),
               buf, cap, len);
+  });
+}
+
+osh_status osh_comm_schedule(const osh_param_desc* params, int32_t n, int64_t bucket_capacity,
+                             int32_t ranks, const int64_t* cuts, int32_t n_buckets,
+                             int32_t strategy, const int32_t* layer_of,
+                             const osh_cost_model* cost, osh_coll_op* out, int32_t cap,
+                             int32_t* n_out) {
+  return guarded("osh_comm_schedule", [&] {
+    const std::vector<ParamSpec> specs = to_specs(params, n);
+    const BufferLayout layout = build_buffer_layout(specs, bucket_capacity);
+    if (ranks < 1) throw PlanError("ranks must be >= 1");
+    if (cuts == nullptr || n_buckets != static_cast<int32_t>(layout.buckets.size()))
+      throw PlanError("cut vectors must cover every bucket of the layout");
+    if (strategy < OSH_STRAT_SHARDED || strategy > OSH_STRAT_NV_LAYERWISE)
+      throw ConfigError("unknown strategy");
+    std::vector<std::vector<int64_t>> cv;
+    std::vector<int64_t> bucket_base, flat_off(specs.size()), numel(specs.size());
+    int64_t base = 0;
+    for (const Bucket& b : layout.buckets) {
+      cv.emplace_back(cuts + static_cast<std::size_t>(b.index) * (ranks + 1),
+                      cuts + static_cast<std::size_t>(b.index + 1) * (ranks + 1));
+      if (cv.back().front() != 0 || cv.back().back() != b.numel)
+        throw PlanError("bucket " + std::to_string(b.index) + ": cuts must span [0, numel]");
+      bucket_base.push_back(base);
+      for (std::size_t j = 0; j < b.param_ids.size(); ++j)
+        flat_off[static_cast<std::size_t>(b.param_ids[j])] = base + b.param_offsets[j];
+      base += b.numel;
+    }
+    for (const ParamSpec& p : specs) numel[static_cast<std::size_t>(p.id)] = p.numel;
+    std::vector<int> owner(specs.size(), 0);
+    if (strategy == OSH_STRAT_NV_LAYERWISE) {
+      if (layer_of == nullptr) throw PlanError("NV-layerwise needs the layer group of every parameter");
+      owner = osh::layerwise_owners(specs, std::vector<int32_t>(layer_of, layer_of + n), ranks,
+                                    to_model(cost));
+    }
+    const std::vector<osh_coll_op> ops =
+        ranks > 1 ? osh::build_comm_schedule(strategy, cv, bucket_base, flat_off, numel, owner)
+                  : std::vector<osh_coll_op>{};
+    if (n_out != nullptr) *n_out = static_cast<int32_t>(ops.size());
+    if (out == nullptr) return;
+    if (cap < static_cast<int32_t>(ops.size())) throw UnsupportedError("output array too small");
+    std::copy(ops.begin(), ops.end(), out);
   });
 }
 

@@ -124,9 +124,42 @@ void free_layout(osh_ctx* ctx) {
 
 namespace osh {
 
+// Issues ops [begin, end) of the ctx's collective schedule on `st`; ops of
+// one group id go inside one ncclGroupStart / ncclGroupEnd.
+osh_status issue_ops(osh_ctx* ctx, int begin, int end, cudaStream_t st) {
+  const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
+  const size_t es = grad_esize(ctx->grad_dtype);
+  int open_group = -1;
+  for (int i = begin; i < end; ++i) {
+    const osh_coll_op& o = ctx->sched[static_cast<size_t>(i)];
+    if (o.group != open_group) {
+      if (open_group >= 0) OSH_NCCL_TRY(ncclGroupEnd());
+      OSH_NCCL_TRY(ncclGroupStart());
+      open_group = o.group;
+    }
+    const size_t cnt = static_cast<size_t>(o.count);
+    if (o.kind == OSH_OP_REDUCE) {
+      const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) + es * static_cast<size_t>(o.offset);
+      uint8_t* dst = o.root == ctx->rank
+                         ? static_cast<uint8_t*>(ctx->grad_owned) + es * static_cast<size_t>(o.dst_offset)
+                         : nullptr;
+      OSH_NCCL_TRY(ncclReduce(src, dst, cnt, gtype, ncclSum, o.root, ctx->comm, st));
+    } else if (o.kind == OSH_OP_BROADCAST) {
+      __nv_bfloat16* ptr = ctx->replica + o.offset;
+      OSH_NCCL_TRY(ncclBroadcast(ptr, ptr, cnt, ncclBfloat16, o.root, ctx->comm, st));
+    } else {
+      uint8_t* base = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(o.offset);
+      OSH_NCCL_TRY(ncclAllReduce(base, base, cnt, gtype, ncclSum, ctx->comm, st));
+    }
+  }
+  if (open_group >= 0) OSH_NCCL_TRY(ncclGroupEnd());
+  return OSH_OK;
+}
+
 // The bf16 replica from the owners' fp32 masters: every rank casts the
-// tensors it owns into its replica slots, then each bucket slice is
-// broadcast from its owner (tp_size == 1; with TP the next step refreshes it).
+// tensors it owns into its replica slots, then the AG-v leg of the schedule
+// broadcasts each slice from its owner (the plan's cut owners, or the layer
+// owners under NV-layerwise; tp_size == 1 — with TP the next step refreshes it).
 osh_status refresh_replica(osh_ctx* ctx) {
   cudaStream_t cs = ctx->compute;
   for (size_t p = 0; p < ctx->params.size(); ++p) {
@@ -136,17 +169,9 @@ osh_status refresh_replica(osh_ctx* ctx) {
                                                      ctx->replica + ctx->flat_off[p], n);
   }
   OSH_CUDA_TRY(cudaGetLastError());
-  if (distributed(ctx) && ctx->tp_size == 1) {
-    for (size_t b = 0; b < ctx->cuts.size(); ++b) {
-      OSH_NCCL_TRY(ncclGroupStart());
-      for (int r = 0; r < ctx->size; ++r) {
-        const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
-        if (cnt == 0) continue;
-        __nv_bfloat16* ptr = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
-        OSH_NCCL_TRY(ncclBroadcast(ptr, ptr, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, cs));
-      }
-      OSH_NCCL_TRY(ncclGroupEnd());
-    }
+  if (distributed(ctx) && ctx->tp_size == 1 && !ctx->sched_ag.empty()) {
+    const int b0 = ctx->sched_ag.front().first, b1 = ctx->sched_ag.back().second;
+    if (osh_status st = issue_ops(ctx, b0, b1, cs); st != OSH_OK) return st;
   }
   OSH_CUDA_TRY(cudaStreamSynchronize(cs));
   return OSH_OK;
@@ -155,20 +180,8 @@ osh_status refresh_replica(osh_ctx* ctx) {
 // RS-v of bucket b on the comm stream: the owner of each slice receives the
 // sum of all ranks' slices in its grad_owned region (local grads intact).
 osh_status issue_rs(osh_ctx* ctx, int b) {
-  const ncclDataType_t gtype = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
-  const size_t es = grad_esize(ctx->grad_dtype);
-  OSH_NCCL_TRY(ncclGroupStart());
-  for (int r = 0; r < ctx->size; ++r) {
-    const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
-    if (cnt == 0) continue;
-    const uint8_t* src = static_cast<const uint8_t*>(ctx->grad) +
-                         es * static_cast<size_t>(ctx->bucket_base[b] + ctx->cuts[b][r]);
-    uint8_t* dst = static_cast<uint8_t*>(ctx->grad_owned) +
-                   es * static_cast<size_t>(ctx->owned_slice_off[b]);
-    OSH_NCCL_TRY(ncclReduce(src, r == ctx->rank ? dst : nullptr, static_cast<size_t>(cnt), gtype,
-                            ncclSum, r, ctx->comm, ctx->comm_stream));
-  }
-  OSH_NCCL_TRY(ncclGroupEnd());
+  const auto [b0, b1] = ctx->sched_rs[static_cast<size_t>(b)];
+  if (osh_status st = issue_ops(ctx, b0, b1, ctx->comm_stream); st != OSH_OK) return st;
   OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ctx->comm_stream));
   return OSH_OK;
 }
@@ -422,27 +435,14 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     int64_t alloc = 0;
     // strategy baselines: SC replicates every tensor; NV-layerwise assigns whole
     // layers by LPT (min_heap_balance over the layer costs, simulate.hpp:140-157)
-    std::vector<int> layer_owner;
-    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE) {
-      if (ctx->layer_of.size() != np) throw PlanError("layer_of must cover every parameter");
-      std::vector<Cost> layer_cost;
-      for (size_t p = 0; p < np; ++p) {
-        const size_t l = static_cast<size_t>(ctx->layer_of[p]);
-        if (layer_cost.size() <= l) layer_cost.resize(l + 1, 0);
-        layer_cost[l] += param_cost(ctx->params[p], ctx->strategy_cost);
-      }
-      std::vector<TpItem> items;
-      for (size_t l = 0; l < layer_cost.size(); ++l) items.push_back({static_cast<int>(l), layer_cost[l]});
-      const HeapAssignment a = min_heap_balance(items, ctx->size);
-      layer_owner.assign(layer_cost.size(), 0);
-      for (size_t rr = 0; rr < a.rank_params.size(); ++rr)
-        for (const int l : a.rank_params[rr]) layer_owner[static_cast<size_t>(l)] = static_cast<int>(rr);
-    }
+    std::vector<int> layer_owner;  // per parameter (NV-layerwise)
+    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE)
+      layer_owner = osh::layerwise_owners(ctx->params, ctx->layer_of, ctx->size, ctx->strategy_cost);
     for (size_t p = 0; p < np; ++p) {
       if (ctx->strategy == OSH_STRAT_SC)
         ctx->owner[p] = ctx->rank;
       else if (ctx->strategy == OSH_STRAT_NV_LAYERWISE)
-        ctx->owner[p] = layer_owner[static_cast<size_t>(ctx->layer_of[p])];
+        ctx->owner[p] = layer_owner[p];
       else
         ctx->owner[p] = param_owner(plan, ctx->layout, static_cast<int>(p));
       if (ctx->owner[p] == ctx->rank && !is_tp_item(ctx, p)) {
@@ -452,6 +452,30 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
       }
     }
     ctx->owned_alloc = alloc;
+    // the collective schedule every rank issues (identical on all ranks)
+    ctx->sched.clear();
+    ctx->sched_rs.assign(static_cast<size_t>(n_buckets), {0, 0});
+    ctx->sched_ag.assign(static_cast<size_t>(n_buckets), {0, 0});
+    if (ctx->comm_mode == OSH_COMM_NCCL && R > 1) {
+      std::vector<int64_t> numel(np);
+      for (size_t p = 0; p < np; ++p) numel[p] = ctx->params[p].numel;
+      ctx->sched = osh::build_comm_schedule(ctx->strategy, ctx->cuts, ctx->bucket_base,
+                                            ctx->flat_off, numel, ctx->owner);
+      for (int32_t b = 0; b < n_buckets; ++b) {  // op ranges per bucket and leg
+        auto& rs = ctx->sched_rs[static_cast<size_t>(b)];
+        auto& ag = ctx->sched_ag[static_cast<size_t>(b)];
+        rs = ag = {-1, -1};
+        for (int i = 0; i < static_cast<int>(ctx->sched.size()); ++i) {
+          const osh_coll_op& o = ctx->sched[static_cast<size_t>(i)];
+          if (o.bucket != b) continue;
+          auto& r = o.phase == OSH_PHASE_RS ? rs : ag;
+          if (r.first < 0) r.first = i;
+          r.second = i + 1;
+        }
+        if (rs.first < 0) rs = {0, 0};
+        if (ag.first < 0) ag = {0, 0};
+      }
+    }
   } catch (const PlanError& e) {
     return osh::fail(OSH_ERR_PLAN, std::string("osh_ctx_set_layout: ") + e.what());
   } catch (const ShardError& e) {
@@ -922,7 +946,6 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   }
   if (host_replica_out != nullptr && pipelined) io.replica_out = host_replica_out;
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
-  const size_t es = grad_esize(ctx->grad_dtype);
   const int nb = static_cast<int>(ctx->cuts.size());
   osh::OptimizerEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
@@ -993,13 +1016,11 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     // waves (each waits for its buckets), then NV-layerwise broadcasts every
     // tensor from its layer owner. Reduction per bucket overlaps the waves.
     if (marked) return osh::fail(OSH_ERR_UNSUPPORTED, "osh_bucket_ready with SC / NV-layerwise");
-    const ncclDataType_t gt = ctx->grad_dtype == OSH_GRAD_BF16 ? ncclBfloat16 : ncclFloat32;
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[0], 0));
     for (int b = 0; b < nb; ++b) {
       if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->h2d_ev[b], 0));
-      uint8_t* base = static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(ctx->bucket_base[b]);
-      OSH_NCCL_TRY(ncclAllReduce(base, base, static_cast<size_t>(ctx->layout.buckets[b].numel), gt,
-                                 ncclSum, ctx->comm, ns));
+      const auto [o0, o1] = ctx->sched_rs[static_cast<size_t>(b)];  // the bucket's AllReduce
+      if (osh_status st = osh::issue_ops(ctx, o0, o1, ns); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev[b], ns));
     }
     HostIo bio;
@@ -1012,14 +1033,9 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     if (osh_status st = run_waves_local(ctx, *cfg, cs, bio); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
-    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE) {
-      OSH_NCCL_TRY(ncclGroupStart());
-      for (size_t p = 0; p < ctx->params.size(); ++p) {
-        __nv_bfloat16* ptr = ctx->replica + ctx->flat_off[p];
-        OSH_NCCL_TRY(ncclBroadcast(ptr, ptr, static_cast<size_t>(ctx->params[p].numel), ncclBfloat16,
-                                   ctx->owner[p], ctx->comm, ns));
-      }
-      OSH_NCCL_TRY(ncclGroupEnd());
+    if (ctx->strategy == OSH_STRAT_NV_LAYERWISE) {  // every tensor from its layer owner
+      const int o0 = ctx->sched_ag.front().first, o1 = ctx->sched_ag.back().second;
+      if (osh_status st = osh::issue_ops(ctx, o0, o1, ns); st != OSH_OK) return st;
     }
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
     OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
@@ -1053,14 +1069,8 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   }
   auto all_gather = [&](int b) -> osh_status {
     // AG-v of bucket b: every owner broadcasts its updated bf16 slice.
-    OSH_NCCL_TRY(ncclGroupStart());
-    for (int r = 0; r < ctx->size; ++r) {
-      const int64_t cnt = ctx->cuts[b][r + 1] - ctx->cuts[b][r];
-      if (cnt == 0) continue;
-      __nv_bfloat16* p = ctx->replica + ctx->bucket_base[b] + ctx->cuts[b][r];
-      OSH_NCCL_TRY(ncclBroadcast(p, p, static_cast<size_t>(cnt), ncclBfloat16, r, ctx->comm, ns));
-    }
-    OSH_NCCL_TRY(ncclGroupEnd());
+    const auto [o0, o1] = ctx->sched_ag[static_cast<size_t>(b)];
+    if (osh_status st = osh::issue_ops(ctx, o0, o1, ns); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ag_ev[b], ns));
     return d2h_buckets(ctx, io, b, ctx->ag_ev[b]);
   };
@@ -1159,6 +1169,16 @@ osh_status osh_ctx_sync(osh_ctx* ctx) {
       return osh::fail(OSH_ERR_NCCL, std::string("NCCL async error: ") +
                                          ncclGetErrorString(async_err));
   }
+  return OSH_OK;
+}
+
+osh_status osh_ctx_comm_schedule(osh_ctx* ctx, osh_coll_op* out, int32_t cap, int32_t* n_out) {
+  if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
+  const int32_t n = static_cast<int32_t>(ctx->sched.size());
+  if (n_out != nullptr) *n_out = n;
+  if (out == nullptr) return OSH_OK;
+  if (cap < n) return osh::fail(OSH_ERR_ARG, "osh_ctx_comm_schedule: output array too small");
+  std::copy(ctx->sched.begin(), ctx->sched.end(), out);
   return OSH_OK;
 }
 

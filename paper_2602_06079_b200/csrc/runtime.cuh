@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include "comm_schedule.hpp"
 #include "ns_engine.cuh"
 #include "shampoo_engine.cuh"
 #include "soap_engine.cuh"
@@ -99,6 +100,10 @@ struct osh_ctx {
   __nv_bfloat16* mc_replica = nullptr;  // multicast address of replica
   std::string nvls_why;                 // why NVLS is off (diagnostics)
   float* bar = nullptr;                 // 1-element buffer of the step barriers
+  // DP collective schedule (comm_schedule.hpp): what the NCCL path issues;
+  // per bucket, the [begin, end) op ranges of its RS-v and AG-v legs
+  std::vector<osh_coll_op> sched;
+  std::vector<std::pair<int, int>> sched_rs, sched_ag;
   bool layout_ready = false;
   osh_step_timing last_timing{};
 

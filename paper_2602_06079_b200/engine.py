@@ -273,6 +273,17 @@ class DistributedMuon:
         code 7 = OSH_ERR_FORMAT); rewrites and all-gathers the replica."""
         _lib.check(_lib.lib().osh_ctx_load_state(self._ctx, path.encode()))
 
+    def comm_schedule(self) -> list:
+        """The collective schedule this ctx issues (osh_ctx_comm_schedule; see
+        planner.comm_schedule for the record fields)."""
+        from .planner import _ops_to_records
+        L = _lib.lib()
+        n = ctypes.c_int32(0)
+        _lib.check(L.osh_ctx_comm_schedule(self._ctx, None, 0, ctypes.byref(n)))
+        arr = (_lib.CollOp * max(n.value, 1))()
+        _lib.check(L.osh_ctx_comm_schedule(self._ctx, arr, n.value, ctypes.byref(n)))
+        return _ops_to_records(arr, n.value)
+
     def update_norms(self) -> np.ndarray:
         out = np.zeros(len(self.params))
         _lib.check(_lib.lib().osh_update_norms(

@@ -61,6 +61,11 @@ def main():
                           shampoo=(SCFG if opt == "shampoo" else SOCFG if opt == "soap" else None),
                           strategy=strategy)
     path = COLLECTIVE_NAMES[eng.info()["collectives"]]
+    # the ctx issues exactly the schedule the pure planner function exports
+    # (the one tests/test_multi_rank_cpu.py executes over gloo)
+    from paper_2602_06079_b200.engine import layer_groups
+    sched_ok = eng.comm_schedule() == P.comm_schedule(
+        params, cap, plan, strategy, layer_groups(params) if strategy == "nv-layerwise" else None)
     for p in params:
         eng.load_param(p.id, O.init_weight(p.shape, p.id, SEED))
     norms = []
@@ -142,7 +147,7 @@ def main():
                 rnorms[s, p.id] = SO.soap_apply(st[p.id], socfg, w[p.id], g.reshape(w[p.id].shape), s)
             else:
                 rnorms[s, p.id] = O.muon_apply(p.is_matrix, cfg, w[p.id], mom[p.id], g)
-    report, ok = {}, True
+    report, ok = {}, sched_ok
     for p in params:
         got, ref = weights[p.id].reshape(-1), w[p.id].reshape(-1)
         e_w = float(np.abs(got - ref).max() / np.abs(ref).max())
@@ -173,7 +178,7 @@ def main():
                           "replica_bitexact": rep_ok, "ok": good}
     print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt,
                       "bucket_ready": announce, "host_buffers": host, "strategy": strategy,
-                      "grad_dtype": gdt, "ok": ok,
+                      "grad_dtype": gdt, "schedule_matches": sched_ok, "ok": ok,
                       "params": report}))
     return 0 if ok else 1
 
