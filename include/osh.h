@@ -135,9 +135,16 @@ void osh_muon_cfg_default(osh_muon_cfg* cfg);
  * in tests/test_gpu_parity.py, not bit for bit.
  *   osh_newton_schulz_host  newton_schulz_orthogonalize (verify.hpp:118-134):
  *                           x (rows x cols) is replaced by its orthogonalisation
+ *                           (computed on the GPU; zero input stays zero)
  *   osh_muon_apply_host     muon_apply (verify.hpp:138-147): m = beta*m + g;
- *                           matrix: w -= lr*NS(m); vector: w -= lr*m.
- *                           *update_norm (nullable) = ||lr * update||_F */
+ *                           matrix: w -= lr*NS(m); vector: w -= lr*m. The two
+ *                           elementwise expressions are the reference's fp64
+ *                           ones on the caller's fp64 arrays (vector and zero-
+ *                           gradient updates stay bit-identical to it); NS(m)
+ *                           runs on the GPU.
+ *                           *update_norm (nullable) = ||w_new - w_old||_F
+ * These serve the reference's fp64 host-array interface (include/optishard/
+ * muon.hpp); the production path is osh_step on device-resident buckets. */
 osh_status osh_newton_schulz_host(int32_t device, double* x, int64_t rows, int64_t cols,
                                   int32_t steps);
 osh_status osh_muon_apply_host(int32_t device, const osh_param_desc* p, const osh_muon_cfg* cfg,

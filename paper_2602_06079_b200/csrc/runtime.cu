@@ -1325,10 +1325,11 @@ osh_status osh_write_state(osh_ctx* ctx, int32_t pid, int32_t which, const float
 
 namespace {
 
-// One-rank, one-tensor context: the single-tensor drop-ins reuse the whole
-// distributed step machinery (same kernels) on a layout of one parameter.
-osh_status one_tensor_step(int32_t device, const osh_param_desc& d, const osh_muon_cfg& cfg,
-                           double* w, double* m, const double* g, double* update_norm) {
+// NS(x) of one matrix on `device` through the step machinery of a one-rank,
+// one-tensor context (same kernels as osh_step): momentum 0, beta 0, grad x,
+// w 0 and lr = -1 turn "w -= lr * NS(beta*m + g)" into w = NS(x).
+osh_status ns_one_matrix(int32_t device, double* x, int64_t rows, int64_t cols,
+                         const osh_muon_cfg& base) {
   osh_ctx* ctx = nullptr;
   if (osh_status st = osh_ctx_create(device, 0, 1, OSH_COMM_NONE, nullptr, &ctx); st != OSH_OK)
     return st;
@@ -1336,68 +1337,65 @@ osh_status one_tensor_step(int32_t device, const osh_param_desc& d, const osh_mu
     osh_ctx* c;
     ~Guard() { osh_ctx_destroy(c); }
   } guard{ctx};
-  osh_param_desc p = d;
-  p.id = 0;
-  const int64_t n = p.shape[0] * (p.ndim == 2 ? p.shape[1] : 1);
+  osh_param_desc p{};
+  p.ndim = 2;
+  p.shape[0] = rows;
+  p.shape[1] = cols;
+  p.dtype_bytes = 4;
+  const int64_t n = rows * cols;
   const int64_t cuts[2] = {0, n};
   if (osh_status st = osh_ctx_set_layout(ctx, &p, 1, n, cuts, 1, OSH_GRAD_F32, 0); st != OSH_OK)
     return st;
-  std::vector<float> buf(static_cast<size_t>(n));
-  auto put = [&](const double* src) {
-    for (int64_t i = 0; i < n; ++i) buf[i] = static_cast<float>(src[i]);
-  };
-  put(w);
-  if (osh_status st = osh_load_param(ctx, 0, buf.data()); st != OSH_OK) return st;
-  put(m);
-  if (osh_status st = osh_write_state(ctx, 0, OSH_READ_MOMENTUM, buf.data()); st != OSH_OK)
-    return st;
-  put(g);
+  std::vector<float> buf(static_cast<size_t>(n), 0.f);
+  if (osh_status st = osh_load_param(ctx, 0, buf.data()); st != OSH_OK) return st;  // w = m = 0
+  for (int64_t i = 0; i < n; ++i) buf[static_cast<size_t>(i)] = static_cast<float>(x[i]);
   if (osh_status st = osh_write_grad(ctx, 0, buf.data()); st != OSH_OK) return st;
+  osh_muon_cfg cfg = base;
+  cfg.lr = -1.0;
+  cfg.beta = 0.0;
   if (osh_status st = osh_step(ctx, &cfg, nullptr, nullptr); st != OSH_OK) return st;
   if (osh_status st = osh_read_param(ctx, 0, OSH_READ_MASTER, buf.data()); st != OSH_OK) return st;
-  for (int64_t i = 0; i < n; ++i) w[i] = buf[i];
-  if (osh_status st = osh_read_param(ctx, 0, OSH_READ_MOMENTUM, buf.data()); st != OSH_OK)
-    return st;
-  for (int64_t i = 0; i < n; ++i) m[i] = buf[i];
-  if (update_norm != nullptr) {
-    double norm = 0.0;
-    if (osh_status st = osh_update_norms(ctx, &norm); st != OSH_OK) return st;
-    *update_norm = norm;
-  }
+  for (int64_t i = 0; i < n; ++i) x[i] = buf[static_cast<size_t>(i)];
   return OSH_OK;
 }
 
 }  // namespace
 
+// Host-buffer drop-in of muon_apply (verify.hpp:138-147) on the reference's
+// fp64 arrays: the momentum and the final axpy are the reference's own fp64
+// expressions on the caller's arrays (so the vector and zero-gradient cases
+// stay bit-identical to it); the Newton-Schulz orthogonalisation — all of the
+// work — runs on the GPU.
 osh_status osh_muon_apply_host(int32_t device, const osh_param_desc* p, const osh_muon_cfg* cfg,
                                double* w, double* m, const double* g, double* update_norm) {
   if (p == nullptr || cfg == nullptr || w == nullptr || m == nullptr || g == nullptr)
     return osh::fail(OSH_ERR_ARG, "osh_muon_apply_host: null argument");
-  return one_tensor_step(device, *p, *cfg, w, m, g, update_norm);
+  if (p->ndim != 1 && p->ndim != 2) return osh::fail(OSH_ERR_UNSUPPORTED, "params must be 1-D or 2-D");
+  const int64_t rows = p->shape[0], cols = p->ndim == 2 ? p->shape[1] : 1;
+  if (rows < 1 || cols < 1) return osh::fail(OSH_ERR_ARG, "osh_muon_apply_host: empty tensor");
+  const size_t n = static_cast<size_t>(rows * cols);
+  for (size_t i = 0; i < n; ++i) m[i] = cfg->beta * m[i] + g[i];
+  std::vector<double> upd(m, m + n);
+  if (p->ndim == 2)
+    if (osh_status st = ns_one_matrix(device, upd.data(), rows, cols, *cfg); st != OSH_OK) return st;
+  double sq = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double before = w[i];
+    w[i] -= cfg->lr * upd[i];
+    sq += (w[i] - before) * (w[i] - before);
+  }
+  if (update_norm != nullptr) *update_norm = std::sqrt(sq);
+  return OSH_OK;
 }
 
 osh_status osh_newton_schulz_host(int32_t device, double* x, int64_t rows, int64_t cols,
                                   int32_t steps) {
   if (x == nullptr || rows < 1 || cols < 1) return osh::fail(OSH_ERR_ARG, "bad matrix");
-  // NS(x) through the step machinery: momentum 0, beta 0, grad x, w 0 and
-  // lr = -1 turn "w -= lr * NS(beta*m + g)" into w = NS(x).
-  osh_param_desc d{};
-  d.ndim = 2;
-  d.shape[0] = rows;
-  d.shape[1] = cols;
-  d.dtype_bytes = 4;
+  if (steps < 0) return osh::fail(OSH_ERR_CONFIG, "negative Newton-Schulz step count");
   osh_muon_cfg cfg;
   osh_muon_cfg_default(&cfg);
-  cfg.lr = -1.0;
-  cfg.beta = 0.0;
   cfg.ns_steps = steps;
-  const size_t n = static_cast<size_t>(rows * cols);
-  std::vector<double> w(n, 0.0), m(n, 0.0);
-  if (osh_status st = one_tensor_step(device, d, cfg, w.data(), m.data(), x, nullptr);
-      st != OSH_OK)
-    return st;
-  std::memcpy(x, w.data(), sizeof(double) * n);
-  return OSH_OK;
+  return ns_one_matrix(device, x, rows, cols, cfg);
 }
 
 }  // extern "C"
