@@ -73,10 +73,10 @@ void orc_reduced_gradient(int64_t rows, int64_t cols, int param_id, uint64_t see
 #pragma omp parallel for schedule(dynamic)
   for (r = 1; r < contributors; ++r)
     orc_synth_gradient(rows, cols, param_id, seed, step, r, tmp + (size_t)(r - 1) * (size_t)n);
-  for (r = 1; r < contributors; ++r) {
-    const double* g = tmp + (size_t)(r - 1) * (size_t)n;
-    for (int64_t k = 0; k < n; ++k) out[k] += g[k];
-  }
+  int64_t k;
+#pragma omp parallel for schedule(static)
+  for (k = 0; k < n; ++k) /* per element, ranks ascending: the reference's order */
+    for (int q = 1; q < contributors; ++q) out[k] += tmp[(size_t)(q - 1) * (size_t)n + (size_t)k];
   free(tmp);
 }
 
@@ -225,15 +225,20 @@ void orc_muon_apply(int64_t rows, int64_t cols, int is_matrix, double lr, double
     before = (double*)malloc(sizeof(double) * (size_t)n);
     memcpy(before, w, sizeof(double) * (size_t)n);
   }
-  for (int64_t k = 0; k < n; ++k) m[k] = beta * m[k] + g[k];
+  /* elementwise loops are independent per element: threaded, same values */
+  int64_t k;
+#pragma omp parallel for schedule(static)
+  for (k = 0; k < n; ++k) m[k] = beta * m[k] + g[k];
   if (is_matrix) {
     double* u = (double*)malloc(sizeof(double) * (size_t)n);
     memcpy(u, m, sizeof(double) * (size_t)n);
     orc_newton_schulz(u, rows, cols, ns_steps);
-    for (int64_t k = 0; k < n; ++k) w[k] -= lr * u[k];
+#pragma omp parallel for schedule(static)
+    for (k = 0; k < n; ++k) w[k] -= lr * u[k];
     free(u);
   } else {
-    for (int64_t k = 0; k < n; ++k) w[k] -= lr * m[k];
+#pragma omp parallel for schedule(static)
+    for (k = 0; k < n; ++k) w[k] -= lr * m[k];
   }
   if (update_norm != NULL) {
     for (int64_t k = 0; k < n; ++k) before[k] = w[k] - before[k];

@@ -182,17 +182,50 @@ void dump_fuzz(std::uint64_t seed, int count) {
   }
 }
 
+// One plan of one config: the parameter list, the serialized plan and the
+// owner table (bench.py's reference arm plans with the reference's own
+// planner through this mode; oracle/cpu_step.py parses it).
+void dump_one(const std::string& path, int R, const std::string& method, const std::string& kind,
+              double alpha) {
+  const RunFileConfig cfg = load_config_file(path);
+  const auto params = generate_transformer_params(cfg.model);
+  const BufferLayout layout = build_buffer_layout(params, cfg.model.bucket_capacity);
+  const CostModel model = model_of(kind);
+  const PlanMethod m = parse_plan_method(method);
+  const DpPartitionPlan plan = m == PlanMethod::kAlphaBalanced
+                                   ? alpha_balanced_partition(layout, params, R, model, alpha)
+                               : m == PlanMethod::kAtomicOwnership
+                                   ? atomic_ownership_partition(layout, params, R, model)
+                                   : equal_chunk_partition(layout, params, R, model);
+  for (const ParamSpec& p : params) {
+    std::cout << "param " << p.id << " " << p.name;
+    for (const auto e : p.shape) std::cout << " " << e;
+    std::cout << "\n";
+  }
+  std::cout << serialize_dp_plan(plan);
+  if (plan.atomic) {
+    std::cout << "owners";
+    for (const ParamSpec& p : params) std::cout << " " << param_owner(plan, layout, p.id);
+    std::cout << "\n";
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: %s config <file.cfg> | fuzz <seed> <count>\n", argv[0]);
+    std::fprintf(stderr,
+                 "usage: %s config <file.cfg> | fuzz <seed> <count> | "
+                 "plan <file.cfg> <ranks> <method> <cost> <alpha>\n",
+                 argv[0]);
     return 2;
   }
   const std::string mode = argv[1];
   try {
     if (mode == "config" && argc == 3) {
       dump_config(argv[2]);
+    } else if (mode == "plan" && argc == 7) {
+      dump_one(argv[2], std::stoi(argv[3]), argv[4], argv[5], std::stod(argv[6]));
     } else if (mode == "fuzz" && argc == 4) {
       dump_fuzz(std::stoull(argv[2]), std::stoi(argv[3]));
     } else {
