@@ -159,10 +159,13 @@ typedef struct osh_matrix_ref {
   int64_t ld, bstride;
 } osh_matrix_ref;
 
+/* OSH_EPI_FINAL targets: a HOST array of `batch` entries per problem. W and
+ * the replica move by TMA: both 16-byte aligned, W's row pitch a multiple of
+ * 16 bytes and the replica's too (cols % 4 / % 8 of the stored orientation). */
 typedef struct osh_final_target {
-  float* w;           /* fp32 master weight, original [rows][cols] */
-  void* replica;      /* bf16 replica of the same tensor, nullable */
-  double* sq_norm;    /* += ||lr*update||^2, nullable */
+  float* w;           /* fp32 master weight, original [rows][cols] (device) */
+  void* replica;      /* bf16 replica of the same tensor, nullable (device) */
+  double* sq_norm;    /* device; += ||lr*update||^2 (fixed-order sum), nullable */
   int32_t transposed; /* tensor is X^T of the Newton-Schulz iterate */
   int32_t reserved_;
 } osh_final_target;

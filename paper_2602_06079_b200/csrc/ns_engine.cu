@@ -68,8 +68,15 @@ void MuonEngine::release() {
                   static_cast<void*>(d_slot_tensor_), static_cast<void*>(d_scale_update_),
                   static_cast<void*>(d_scale_gram_), static_cast<void*>(d_update_sq_),
                   static_cast<void*>(d_mtasks_), static_cast<void*>(d_atasks_),
-                  static_cast<void*>(d_vtasks_)})
+                  static_cast<void*>(d_vtasks_), static_cast<void*>(d_ftargets_),
+                  static_cast<void*>(d_fpartial_), static_cast<void*>(d_fslot_begin_),
+                  static_cast<void*>(d_fslot_count_), static_cast<void*>(d_fslot_tensor_)})
     cudaFree(p);
+  d_ftargets_ = nullptr;
+  d_fpartial_ = nullptr;
+  fpartial_count_ = 0;
+  d_fslot_begin_ = nullptr;
+  d_fslot_count_ = d_fslot_tensor_ = nullptr;
   d_ws_ = nullptr;
   d_partial_ = d_update_sq_ = nullptr;
   d_slot_begin_ = nullptr;
@@ -109,6 +116,24 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   // owns few others) forms a wave of its own; the rest keep the target size
   if (min_waves > 1) cap = std::min(cap, (total_ws + min_waves - 1) / min_waves);
 
+  // FINAL fusion is a property of the TENSOR (TMA/vector-addressable W and a
+  // local replica), never of the wave it lands in, so results do not depend
+  // on how the plan groups tensors (sharded == replicated bit for bit).
+  const char* ff = std::getenv("OSH_FUSE_FINAL");
+  fuse_final_ = !(ff != nullptr && std::strcmp(ff, "0") == 0);
+  std::vector<char> fused_t(tensors.size(), 0);
+  for (size_t i = 0; i < tensors.size(); ++i) {
+    const MuonTensorDesc& t = tensors[i];
+    if (!t.is_matrix || !fuse_final_ || t.rep_mc) continue;
+    const Shape s = shape_of(t.rows, t.cols);
+    fused_t[i] = final_target_ok(t.w, t.replica, s.m, s.n, t.rows > t.cols ? 1 : 0) ? 1 : 0;
+  }
+  // chunk key: (m, n), n negated for fused tensors (a class splits by fusion)
+  const auto key_of = [&](int i) {
+    const Shape s = shape_of(tensors[i].rows, tensors[i].cols);
+    return std::pair<int, int>{s.m, fused_t[i] ? -s.n : s.n};
+  };
+
   std::vector<std::vector<int>> wave_members(1);
   std::vector<std::vector<std::pair<int, int>>> wave_classes(1);
   size_t used = 0, half = 0;
@@ -117,7 +142,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     if (t.is_matrix) {
       const Shape s = shape_of(t.rows, t.cols);
       const size_t need = 2 * s.xb + 2 * s.ab;
-      const std::pair<int, int> cls{s.m, s.n};
+      const std::pair<int, int> cls = key_of(i);
       auto& classes = wave_classes.back();
       const bool new_class = std::find(classes.begin(), classes.end(), cls) == classes.end();
       const bool has_matrix = used > 0;
@@ -156,6 +181,15 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     wave_members.swap(ordered);
   }
 
+  // fused FINAL targets: (tensor, m, n, partial offset) per fused matrix slot
+  struct FTarget {
+    int ti, m, n;
+    size_t poff;
+  };
+  std::vector<FTarget> ftargets;
+  std::vector<long long> fslot_begin;
+  std::vector<int> fslot_count, fslot_tensor;
+
   // ---- chunks (one per class per wave), slots, tables
   std::vector<MomentumMatrixTask> mtasks;
   std::vector<ApplyTask> atasks;
@@ -192,13 +226,18 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         vtasks.push_back(v);
         continue;
       }
-      const Shape s = shape_of(t.rows, t.cols);
-      const std::pair<int, int> cls{s.m, s.n};
+      const std::pair<int, int> cls = key_of(ti);
       if (!by_class.count(cls)) order.push_back(cls);
       by_class[cls].push_back(ti);
     }
+    // unfused chunks first: their momentum / apply tasks, tiles and slots form
+    // a prefix of the wave's tables (the apply pass runs over that prefix)
+    std::stable_partition(order.begin(), order.end(), [](const std::pair<int, int>& k) { return k.second > 0; });
     size_t off = double_buffer_ && (wi & 1) ? half : 0;
+    w.fslot0 = static_cast<int>(fslot_begin.size());
     for (const auto& cls : order) {
+      const bool cfused = cls.second < 0;
+      if (!cfused) ++w.nf_chunks;
       const std::vector<int>& members = by_class[cls];
       const MuonTensorDesc& t0 = tensors[members.front()];
       const Shape s = shape_of(t0.rows, t0.cols);
@@ -217,9 +256,29 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       off += s.ab * c.batch;
       c.b = off;
       off += s.ab * c.batch;
+      if (cfused) c.ftarget0 = static_cast<int>(ftargets.size());
       for (int b = 0; b < c.batch; ++b) {
         const int ti = members[b];
         const MuonTensorDesc& t = tensors[ti];
+        if (!cfused) {  // the unfused prefix of the wave's tables
+          ++w.nf_tasks;
+          ++w.nf_slots;
+        }
+        if (cfused) {
+          // partial slots of both CTA-group variants (the larger count)
+          const int cg0 = ns_gemm_cta_group();
+          ns_gemm_set_cta_group(1);
+          const int p1 = final_partials(s.m, s.n);
+          ns_gemm_set_cta_group(2);
+          const int p2 = final_partials(s.m, s.n);
+          ns_gemm_set_cta_group(cg0);
+          const int cnt = std::max(p1, p2);
+          ftargets.push_back({ti, s.m, s.n, fpartial_count_});
+          fslot_begin.push_back(static_cast<long long>(fpartial_count_));
+          fslot_count.push_back(cnt);
+          fslot_tensor.push_back(ti);
+          fpartial_count_ += static_cast<size_t>(cnt);
+        }
         const int tiles_c = (t.cols + kTile - 1) / kTile;
         const long long ntiles = static_cast<long long>((t.rows + kTile - 1) / kTile) * tiles_c;
         MomentumMatrixTask mt{};
@@ -258,6 +317,10 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
         slot_count.push_back(static_cast<int>(ntiles));
         slot_tensor.push_back(ti);
         w.tiles += ntiles;
+        if (!cfused) {
+          w.nf_tiles = w.tiles;
+          w.nf_elems += static_cast<double>(t.rows) * t.cols;
+        }
         w.elems_matrix += static_cast<double>(t.rows) * t.cols;
         ++slot;
       }
@@ -301,6 +364,21 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
   OSH_CUDA_TRY(upload(&d_slot_count_, slot_count));
   OSH_CUDA_TRY(upload(&d_slot_tensor_, slot_tensor));
+  if (!ftargets.empty()) {
+    OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_fpartial_), sizeof(double) * fpartial_count_));
+    OSH_CUDA_TRY(cudaMemset(d_fpartial_, 0, sizeof(double) * fpartial_count_));
+    std::vector<NsFinalTarget> ft(ftargets.size());
+    for (size_t i = 0; i < ftargets.size(); ++i) {
+      const MuonTensorDesc& t = tensors[ftargets[i].ti];
+      if (!make_final_target(&ft[i], t.w, t.replica, ftargets[i].m, ftargets[i].n,
+                             t.rows > t.cols ? 1 : 0, d_fpartial_ + ftargets[i].poff))
+        return fail(OSH_ERR_CUDA, "MuonEngine: cannot encode the FINAL TMA maps");
+    }
+    OSH_CUDA_TRY(upload(&d_ftargets_, ft));
+    OSH_CUDA_TRY(upload(&d_fslot_begin_, fslot_begin));
+    OSH_CUDA_TRY(upload(&d_fslot_count_, fslot_count));
+    OSH_CUDA_TRY(upload(&d_fslot_tensor_, fslot_tensor));
+  }
   // cost-balanced (LPT) tile schedules of the three GEMMs of every wave
   const char* aux = std::getenv("OSH_NS_AUX");
   fold_a_ = !(aux != nullptr && std::strcmp(aux, "1") == 0);
@@ -329,6 +407,33 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       sc.units = units;
       sc.total_tiles = total;
     }
+    // last iteration: UPDATE over the unfused prefix, FINAL over the fused rest
+    const int nc = static_cast<int>(w.chunks.size());
+    if (w.nf_chunks == nc) continue;  // nothing fused
+    if (w.nf_chunks == 0) {
+      w.sched[kEpiFinal] = w.sched[kEpiUpdate];  // the same tiles
+      continue;
+    }
+    const std::pair<int, int> parts[2] = {{0, w.nf_chunks}, {w.nf_chunks, nc}};
+    for (int part = 0; part < 2; ++part) {
+      std::vector<int> tl, off;
+      int total = 0;
+      const int mode = part == 0 ? kEpiUpdate : kEpiFinal;
+      const int units = ns_gemm_schedule(mode, pd[2] + parts[part].first,
+                                         parts[part].second - parts[part].first, &tl, &off, &total);
+      if (units == 0) continue;
+      int* d_tl = nullptr;
+      int* d_off = nullptr;
+      OSH_CUDA_TRY(upload(&d_tl, tl));
+      OSH_CUDA_TRY(upload(&d_off, off));
+      sched_mem_.push_back(d_tl);
+      sched_mem_.push_back(d_off);
+      NsSchedule& sc = part == 0 ? w.sched_last_update : w.sched[kEpiFinal];
+      sc.tiles = d_tl;
+      sc.off = d_off;
+      sc.units = units;
+      sc.total_tiles = total;
+    }
   }
   OSH_CUDA_TRY(cudaDeviceSynchronize());
   return OSH_OK;
@@ -337,6 +442,8 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
 osh_status MuonEngine::begin_step(cudaStream_t s) {
   stats_ = NsLaunchStats{};
   OSH_CUDA_TRY(cudaMemsetAsync(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1), s));
+  if (d_fpartial_ != nullptr)  // slots a CTA-group variant leaves unwritten stay zero
+    OSH_CUDA_TRY(cudaMemsetAsync(d_fpartial_, 0, sizeof(double) * fpartial_count_, s));
   return OSH_OK;
 }
 
@@ -415,8 +522,23 @@ osh_status MuonEngine::run_ns(int wi, const osh_muon_cfg& cfg, cudaStream_t s) {
     if (e == cudaSuccess)
       e = timed_launch(kEpiPoly, poly, static_cast<float>(cfg.ns_b), static_cast<float>(cfg.ns_c),
                        fold_a_ ? static_cast<float>(cfg.ns_a) : 0.f);
-    if (e == cudaSuccess)
+    const int nf = w.nf_chunks;
+    if (e == cudaSuccess && nf < np && it + 1 == cfg.ns_steps) {
+      // last iteration: fused chunks apply W -= lr * X' in the FINAL epilogue
+      // (no X' store, no apply pass); unfused ones (a prefix) UPDATE as usual
+      const float alpha = fold_a_ ? 0.f : static_cast<float>(cfg.ns_a);
+      for (int q = nf; q < np; ++q) upd[q].final_targets = d_ftargets_ + chunks_[w.chunks[q]].ftarget0;
+      if (nf > 0) {
+        const NsSchedule* sc = lpt_ && sched_symmetric_ == symmetric_ ? &w.sched_last_update : nullptr;
+        e = timed_gemm(kEpiUpdate, upd, nf, alpha, 0.f, s, sc, 0.f);
+      }
+      if (e == cudaSuccess) {
+        const NsSchedule* sc = lpt_ && sched_symmetric_ == symmetric_ ? &w.sched[kEpiFinal] : nullptr;
+        e = timed_gemm(kEpiFinal, upd + nf, np - nf, alpha, 0.f, s, sc, static_cast<float>(cfg.lr));
+      }
+    } else if (e == cudaSuccess) {
       e = timed_launch(kEpiUpdate, upd, fold_a_ ? 0.f : static_cast<float>(cfg.ns_a), 0.f, 0.f);
+    }
     if (e != cudaSuccess)
       return fail(OSH_ERR_CUDA, std::string("MuonEngine: ns_gemm_launch: ") + cudaGetErrorString(e));
   }
@@ -431,14 +553,22 @@ osh_status MuonEngine::run_post(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
   const auto timed = [&](int mode, double bytes, auto&& launch) {
     return timed_elementwise(mode, bytes, elems, s, launch);
   };
-  // after k iterations the iterate sits in X0 (k even) or X1 (k odd);
-  // X read, w read + write, bf16 replica write
-  OSH_CUDA_TRY(timed(kModeElementwise + 3, w.elems_matrix * 12.0, [&] {
-    return launch_apply_update(d_atasks_ + w.task0, w.n_tasks, w.tiles, lr, cfg.ns_steps & 1, s);
+  // fused tensors: W and the replica were written by FINAL; their norms are
+  // the FINAL epilogue partials
+  if (w.nf_slots < w.n_slots)
+    OSH_CUDA_TRY(timed(kModeElementwise + 4, 0.0, [&] {
+      return launch_partial_sums(d_fpartial_, d_fslot_begin_ + w.fslot0, d_fslot_count_ + w.fslot0,
+                                 d_fslot_tensor_ + w.fslot0, d_update_sq_, w.n_slots - w.nf_slots, s);
+    }));
+  if (w.nf_tasks == 0) return OSH_OK;
+  // unfused prefix: after k iterations the iterate sits in X0 (k even) or X1
+  // (k odd); X read, w read + write, bf16 replica write
+  OSH_CUDA_TRY(timed(kModeElementwise + 3, w.nf_elems * 12.0, [&] {
+    return launch_apply_update(d_atasks_ + w.task0, w.nf_tasks, w.nf_tiles, lr, cfg.ns_steps & 1, s);
   }));
   OSH_CUDA_TRY(timed(kModeElementwise + 4, 0.0, [&] {
     return launch_partial_sums(d_partial_, d_slot_begin_ + w.slot0, d_slot_count_ + w.slot0,
-                               d_slot_tensor_ + w.slot0, d_update_sq_, w.n_slots, s);
+                               d_slot_tensor_ + w.slot0, d_update_sq_, w.nf_slots, s);
   }));
   return OSH_OK;
 }

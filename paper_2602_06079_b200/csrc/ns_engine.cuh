@@ -9,9 +9,13 @@
 // last bucket has landed and all-gather a bucket as soon as the wave that
 // finishes it is done (runtime.cu). One wave of a step is:
 //   momentum_vector (1-D tensors) ; momentum_matrix (m = beta*m + g, tile
-//   sums of m^2, X0 = bf16 m) -> ns_scales -> k x {GRAM, POLY, UPDATE}
-//   -> apply_update (W -= lr*X_k, bf16 replica, tile sums of |dW|^2)
+//   sums of m^2, X0 = bf16 m) -> ns_scales -> (k-1) x {GRAM, POLY, UPDATE}
+//   -> GRAM, POLY, FINAL (W -= lr*X_k straight from the accumulator: W and
+//   the bf16 replica move by TMA in the GEMM epilogue, per-tile |dW|^2)
 //   -> partial_sums (||dW||^2 per tensor, fixed order)
+// A wave whose tensors TMA cannot address (row pitch not a multiple of 16
+// bytes, NVLS multicast replica) ends with UPDATE -> apply_update instead
+// (OSH_FUSE_FINAL=0 forces that path everywhere).
 // All task tables live in device memory and are reused every step.
 #pragma once
 
@@ -71,6 +75,7 @@ class MuonEngine : public OptimizerEngine {
     int m = 0, n = 0, ldm = 0, ldn = 0, batch = 0;
     int slot0 = 0;                        // first matrix slot (chunk-contiguous)
     size_t x0 = 0, x1 = 0, a = 0, b = 0;  // byte offsets in the workspace
+    int ftarget0 = -1;                    // fused waves: first NsFinalTarget of the batch
   };
   struct Wave {
     std::vector<int> chunks;
@@ -80,7 +85,14 @@ class MuonEngine : public OptimizerEngine {
     int slot0 = 0, n_slots = 0;
     int vec0 = 0, n_vec = 0;
     double elems_matrix = 0.0, elems_vector = 0.0;  // owned elements (profile bytes)
-    NsSchedule sched[4];  // per GEMM mode (kEpiGram / kEpiPoly / kEpiUpdate)
+    NsSchedule sched[4];  // per GEMM mode (kEpiGram / kEpiPoly / kEpiUpdate / kEpiFinal)
+    // FINAL fusion (per tensor): the unfused chunks come first, so their
+    // momentum / apply tasks, tiles and slots are a prefix of the wave's
+    int nf_chunks = 0, nf_tasks = 0, nf_slots = 0;
+    long long nf_tiles = 0;
+    double nf_elems = 0.0;
+    int fslot0 = 0;                  // first row of the fused partial-sum tables
+    NsSchedule sched_last_update;    // last iteration: UPDATE over the unfused prefix
   };
   void release();
   const char* elementwise_name(int mode) const override;
@@ -104,6 +116,14 @@ class MuonEngine : public OptimizerEngine {
   MomentumMatrixTask* d_mtasks_ = nullptr;
   ApplyTask* d_atasks_ = nullptr;
   MomentumVectorTask* d_vtasks_ = nullptr;
+  // fused FINAL: per matrix slot a TMA target + its epilogue partials
+  NsFinalTarget* d_ftargets_ = nullptr;
+  double* d_fpartial_ = nullptr;
+  size_t fpartial_count_ = 0;
+  long long* d_fslot_begin_ = nullptr;
+  int* d_fslot_count_ = nullptr;
+  int* d_fslot_tensor_ = nullptr;
+  bool fuse_final_ = true;        // OSH_FUSE_FINAL=0: UPDATE + apply_update everywhere
   bool symmetric_ = true;
   bool double_buffer_ = false;
   bool reorder_ = false;          // small waves first and last (set_wave_reorder)

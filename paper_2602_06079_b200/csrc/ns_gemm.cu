@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace osh {
@@ -23,7 +24,7 @@ using namespace osh::sm100;
 // computes a 256 x 256 tile: each CTA stages its 128 rows of A and its half
 // (128 rows / columns) of B; the leader CTA issues tcgen05.mma.cta_group::2
 // and each CTA's TMEM receives its 128 accumulator rows.
-template <int CG>
+template <int MODE, int CG>
 struct Cfg {
   static constexpr uint32_t kRowsA = 128;                 // A rows per CTA
   static constexpr uint32_t kTileM = 128 * CG;            // output rows per tile
@@ -31,16 +32,21 @@ struct Cfg {
   static constexpr uint32_t kStageA = kRowsA * kNsBK * 2; // 16 KiB
   static constexpr uint32_t kStageB = kRowsB * kNsBK * 2; // 32 or 16 KiB
 #ifndef OSH_CG2_STAGES
-#define OSH_CG2_STAGES 5  // 5 x 32 KiB leaves ~49 KiB for co-resident update kernels
+#define OSH_CG2_STAGES 5  // 5 x 32 KiB leaves ~66 KiB for co-resident update kernels
 #endif
-  static constexpr int kStages = CG == 1 ? 4 : OSH_CG2_STAGES;
+  // FINAL stages W / replica boxes (48 KiB): one stage fewer
+  static constexpr int kStages = (CG == 1 ? 4 : OSH_CG2_STAGES) - (MODE == kEpiFinal ? 1 : 0);
 };
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kEpiStageFloats = 32 * 33;  // per epilogue warp: 32x32 fp32 transpose tile
-template <int CG>
+// kEpiFinal staging per epilogue warp: kFinBufs 32x32 fp32 W boxes in flight
+constexpr int kFinBufs = 3;
+constexpr uint32_t kFinWBox = 32 * 32 * 4;
+constexpr uint32_t kFinBytes = 4 * kFinBufs * kFinWBox;
+template <int MODE, int CG>
 constexpr uint32_t smem_bytes() {
-  return 1024 + Cfg<CG>::kStages * (Cfg<CG>::kStageA + Cfg<CG>::kStageB) + 256 +
-         4 * kEpiStageFloats * 4;
+  // [1 KiB align][stage ring][FINAL staging][barriers 256 B]
+  return 1024 + Cfg<MODE, CG>::kStages * (Cfg<MODE, CG>::kStageA + Cfg<MODE, CG>::kStageB) +
+         (MODE == kEpiFinal ? kFinBytes : 0) + 256;
 }
 constexpr int kRasterGroup = 8;
 
@@ -223,10 +229,195 @@ __device__ __forceinline__ void store_row32_sym(__nv_bfloat16* out, long long ld
   }
 }
 
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_evict_first(uint32_t smem_dst, const void* src,
+                                                       uint32_t src_bytes, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(smem_dst),
+               "l"(src), "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_global_v4_evict_first(void* dst, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_global_v4_evict_first(void* dst, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// kEpiFinal epilogue of one warp (32 rows of the CTA's 128). W is staged per
+// 32-column chunk as a 32 x 32 fp32 box in shared memory, kFinBufs - 1 chunks
+// ahead, by cp.async (the LSU path: no contention with the operand TMA
+// stream; the first boxes are requested before the tile's accumulator is
+// ready). Box row r is one 128-byte segment of a W row; its 16-byte pieces
+// are XOR-swizzled (piece k of row r at k ^ (r & 7)), so the coalesced copies
+// (one instruction = 4 whole rows), a lane's walk along its own row and a
+// lane's walk down a column are all free of bank conflicts. Not transposed
+// (W = X, [M][N]) lane = X row = box row; transposed (W = X^T, [N][M]) box
+// rows are W rows n and lane = m walks down its column. The updated box goes
+// back to W, and its bf16 copy to the replica, with coalesced 16-byte stores.
+// sum (lr*update)^2 of the warp goes to one partial slot per (tile, CTA,
+// warp): the update norm is summed later in a fixed order.
+template <int CG>
+__device__ __forceinline__ void final_epilogue(const NsGemmParams& P, int it_begin, int it_end,
+                                               int it_step, bool sched, uint32_t rank, int q,
+                                               int lane, uint32_t tmem_base, uint64_t* tfull_bar,
+                                               uint64_t* tempty_bar, uint8_t* fin) {
+  float* box0 = reinterpret_cast<float*>(fin + q * kFinBufs * kFinWBox);
+  const uint32_t box0_s = smem_u32(box0);
+  const int sw = lane & 7;
+  const int crow = lane >> 3, cpiece = lane & 7;  // coalesced W copies: 4 rows x 8 pieces
+  const int rrow = lane >> 2, rpiece = lane & 3;  // coalesced replica stores: 8 rows x 4 pieces
+  // W and the replica stream through L2 once: evict them first so the
+  // operand panels the other tiles reuse stay resident
+  const uint64_t pol = l2_policy_evict_first();
+  uint32_t acc = 0, acc_phase = 0;
+  for (int it = it_begin; it < it_end; it += it_step) {
+    const int t = sched ? __ldg(P.sched + it) : it;
+    const TileCoord c = decode_tile(P, t);
+    const NsGemmProblem& pr = P.prob[c.p];
+    const NsFinalTarget& ft = pr.final_targets[c.b];
+    const int transposed = ft.transposed;
+    float* const W = ft.w;
+    __nv_bfloat16* const rep = ft.replica;
+    const int M = pr.M, N = pr.N;
+    const int x_row0 = c.tm * (128 * CG) + static_cast<int>(rank) * 128 + q * 32;  // X' rows (m)
+    const int row = x_row0 + lane;
+    const int nch = min(kNsBN / 32, (N - c.tn * kNsBN + 31) / 32);
+    const float s = pr.scale != nullptr ? __ldg(pr.scale + c.b) : 1.f;
+    // W geometry of chunk ch's box: box row r is W row (grow0 + r), columns
+    // [gcol0, gcol0 + 32); the W row pitch is ld, valid rows < nrow, cols < ld
+    const int ld = transposed ? M : N, nrow = transposed ? N : M;
+    const auto geom = [&](int ch, int& grow0, int& gcol0) {
+      const int xc = c.tn * kNsBN + ch * 32;
+      if (transposed) { grow0 = xc; gcol0 = x_row0; } else { grow0 = x_row0; gcol0 = xc; }
+    };
+    const auto request = [&](int ch) {  // always commits a group (maybe empty)
+      if (ch < nch) {
+        int grow0, gcol0;
+        geom(ch, grow0, gcol0);
+        const uint32_t dst = box0_s + (ch % kFinBufs) * kFinWBox;
+        const int gc = gcol0 + 4 * cpiece;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 4 * i + crow;
+          const bool v = grow0 + r < nrow && gc < ld;
+          const float* src = v ? W + static_cast<long long>(grow0 + r) * ld + gc : W;
+          cp_async16_evict_first(dst + r * 128 + 16 * (cpiece ^ (r & 7)), src, v ? 16u : 0u, pol);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int ch = 0; ch < kFinBufs - 1; ++ch) request(ch);
+    mbar_wait(&tfull_bar[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kNsBN;
+    float sq = 0.f;  // this lane's (lr*update)^2 over the tile (fixed order)
+#pragma unroll 1
+    for (int ch = 0; ch < nch; ++ch) {
+      request(ch + kFinBufs - 1);  // the buffer it fills was released at the end of chunk ch - 1
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + ch * 32, r);
+      tmem_ld_wait();
+      const int col0 = c.tn * kNsBN + ch * 32;
+      float u[32];
+      if (P.alpha != 0.f && row < M)
+        load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, N, u);
+      else
+#pragma unroll
+        for (int j = 0; j < 32; ++j) u[j] = 0.f;
+      float sq4[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const bool ok = row < M && col0 + j < N;
+        u[j] = ok ? P.lr * (s * (P.alpha * u[j] + __uint_as_float(r[j]))) : 0.f;
+        sq4[j & 3] = fmaf(u[j], u[j], sq4[j & 3]);
+      }
+      sq += (sq4[0] + sq4[1]) + (sq4[2] + sq4[3]);
+      cp_async_wait<kFinBufs - 1>();  // chunk ch's box: this lane's copies landed
+      __syncwarp();                    // ... and every lane's
+      float* box = box0 + (ch % kFinBufs) * (kFinWBox / 4);
+      if (!transposed) {  // lane = box row
+        float* br = box + lane * 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float4* p4 = reinterpret_cast<float4*>(br + 4 * (k ^ sw));
+          float4 x = *p4;
+          x.x -= u[4 * k + 0];
+          x.y -= u[4 * k + 1];
+          x.z -= u[4 * k + 2];
+          x.w -= u[4 * k + 3];
+          *p4 = x;
+        }
+      } else {  // lane = box column
+#pragma unroll
+        for (int j = 0; j < 32; ++j) box[j * 32 + 4 * ((lane >> 2) ^ (j & 7)) + (lane & 3)] -= u[j];
+      }
+      __syncwarp();
+      int grow0, gcol0;
+      geom(ch, grow0, gcol0);
+      {  // W: 8 instructions of 4 whole box rows
+        const int gc = gcol0 + 4 * cpiece;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + crow;
+          if (grow0 + rr < nrow && gc < ld)
+            st_global_v4_evict_first(W + static_cast<long long>(grow0 + rr) * ld + gc,
+                                     *reinterpret_cast<const float4*>(box + rr * 32 + 4 * (cpiece ^ (rr & 7))),
+                                     pol);
+        }
+      }
+      if (rep != nullptr) {  // replica: 4 instructions of 8 whole box rows (64 bytes each)
+        const int gc = gcol0 + 8 * rpiece;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = 8 * i + rrow;
+          if (grow0 + rr < nrow && gc < ld) {
+            const float4 a = *reinterpret_cast<const float4*>(box + rr * 32 + 4 * ((2 * rpiece) ^ (rr & 7)));
+            const float4 b = *reinterpret_cast<const float4*>(box + rr * 32 + 4 * ((2 * rpiece + 1) ^ (rr & 7)));
+            uint4 h;
+            h.x = pack_bf16(a.x, a.y);
+            h.y = pack_bf16(a.z, a.w);
+            h.z = pack_bf16(b.x, b.y);
+            h.w = pack_bf16(b.z, b.w);
+            st_global_v4_evict_first(rep + static_cast<long long>(grow0 + rr) * ld + gc, h, pol);
+          }
+        }
+      }
+      __syncwarp();  // the box is free for the request of chunk ch + kFinBufs
+    }
+    cp_async_wait<0>();  // (only empty groups remain)
+    double dsq = static_cast<double>(sq);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsq += __shfl_xor_sync(0xffffffffu, dsq, o);
+    if (lane == 0) {
+      const int tile_local = c.tm * pr.tiles_n + c.tn;
+      ft.partial[(tile_local * CG + static_cast<int>(rank)) * 4 + q] = dsq;
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
+    else mbar_arrive(&tempty_bar[acc]);
+    acc ^= 1;
+    if (acc == 0) acc_phase ^= 1;
+  }
+}
+
 template <int MODE, int CG>
 __global__ void __launch_bounds__(kNsThreads, 1)
     ns_gemm_kernel(const __grid_constant__ NsGemmParams P) {
-  using C = Cfg<CG>;
+  using C = Cfg<MODE, CG>;
   constexpr int kStages = C::kStages;
   constexpr uint32_t kStageBytesA = C::kStageA, kStageBytesB = C::kStageB;
   extern __shared__ uint8_t smem_raw[];
@@ -234,12 +425,12 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = base;
   uint8_t* smem_b = base + kStages * kStageBytesA;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_b + kStages * kStageBytesB);
+  uint8_t* fin = smem_b + kStages * kStageBytesB;  // 1 KiB aligned (kEpiFinal staging)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(fin + (MODE == kEpiFinal ? kFinBytes : 0));
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  float* epi_stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -355,13 +546,16 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp >= 4 && MODE == kEpiFinal) {
+    final_epilogue<CG>(P, it_begin, it_end, it_step, sched, rank, warp & 3, lane, tmem_base,
+                       tfull_bar, tempty_bar, fin);
   } else if (warp >= 4) {
     // ---------------------------------------------------------- epilogue
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     uint32_t acc = 0, acc_phase = 0;
     for (int it = it_begin; it < it_end; it += it_step) {
-        const int t = sched ? __ldg(P.sched + it) : it;
+      const int t = sched ? __ldg(P.sched + it) : it;
       const TileCoord c = decode_tile(P, t);
       const NsGemmProblem& pr = P.prob[c.p];
       const int row_base = c.tm * C::kTileM + rank * C::kRowsA;
@@ -371,7 +565,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kNsBN;
-      double sq = 0.0;
 #pragma unroll 1
       for (int chunk = 0; chunk < kNsBN / 32; ++chunk) {
         uint32_t r[32];
@@ -379,7 +572,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         tmem_ld_wait();
         const int col0 = c.tn * kNsBN + chunk * 32;
         if (col0 >= pr.N) continue;  // warp-uniform
-        if (MODE != kEpiFinal && !row_ok) continue;
+        if (!row_ok) continue;
         float v[32];
         if constexpr (MODE == kEpiGram) {
 #pragma unroll
@@ -445,66 +638,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             store_row32(d + 2 * sg, col0, pr.N, v);
             store_row32(d + 3 * sg, col0, pr.N, v);
           }
-        } else {  // kEpiFinal: every lane takes part (warp-level transpose below)
-          float upd[32];
-          if (row_ok) {
-            load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              upd[j] = (col0 + j < pr.N)
-                           ? P.lr * (s * (P.alpha * v[j] + __uint_as_float(r[j])))
-                           : 0.f;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) upd[j] = 0.f;
-          }
-          const NsFinalTarget ft = pr.final_targets[c.b];
-          if (ft.transposed) {
-            // W is X^T ([N][M]): for a fixed column the 32 lanes hold 32
-            // consecutive rows of X = 32 consecutive floats of W.
-            if (row_ok) {
-#pragma unroll 8
-              for (int j = 0; j < 32; ++j) {
-                const int col = col0 + j;
-                if (col >= pr.N) break;
-                const size_t idx = static_cast<size_t>(col) * pr.M + row;
-                const float w = ft.w[idx] - upd[j];
-                ft.w[idx] = w;
-                if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
-                sq += static_cast<double>(upd[j]) * static_cast<double>(upd[j]);
-              }
-            }
-          } else {
-            // W is X ([M][N]): transpose the warp's 32x32 block through shared
-            // memory so each access covers 32 consecutive columns of one row.
-            float* buf = epi_stage + quarter * kEpiStageFloats;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = upd[j];
-            __syncwarp();
-            const int rbase = row_base + quarter * 32;
-            const int col = col0 + lane;
-#pragma unroll 4
-            for (int rr = 0; rr < 32; ++rr) {
-              const int rw = rbase + rr;
-              if (rw < pr.M && col < pr.N) {
-                const float u = buf[rr * 33 + lane];
-                const size_t idx = static_cast<size_t>(rw) * pr.N + col;
-                const float w = ft.w[idx] - u;
-                ft.w[idx] = w;
-                if (ft.replica != nullptr) ft.replica[idx] = __float2bfloat16_rn(w);
-                sq += static_cast<double>(u) * static_cast<double>(u);
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-      if constexpr (MODE == kEpiFinal) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0 && sq != 0.0) {
-          double* dst = pr.final_targets[c.b].sq_norm;
-          if (dst != nullptr) atomicAdd(dst, sq);
         }
       }
       tc_fence_before();
@@ -577,7 +710,7 @@ int sm_count() {
 template <int MODE, int CG>
 cudaError_t launch_mode(const NsGemmParams& P, cudaStream_t stream) {
   static bool configured = false;
-  constexpr uint32_t smem = smem_bytes<CG>();
+  constexpr uint32_t smem = smem_bytes<MODE, CG>();
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(ns_gemm_kernel<MODE, CG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -625,6 +758,29 @@ int sym_tiles(int tiles_m, int tiles_n, int tile_m) {
 }
 
 }  // namespace
+
+bool final_target_ok(const void* w, const void* replica, int M, int N, int transposed) {
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int inner = transposed ? M : N;  // contiguous extent of W in elements
+  if (w == nullptr || !a16(w) || inner % 4 != 0) return false;
+  return replica == nullptr || (a16(replica) && inner % 8 == 0);
+}
+
+bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
+                       int transposed, double* partial) {
+  std::memset(t, 0, sizeof(*t));
+  if (!final_target_ok(w, replica, M, N, transposed) || partial == nullptr) return false;
+  t->w = w;
+  t->replica = replica;
+  t->partial = partial;
+  t->transposed = transposed;
+  return true;
+}
+
+int final_partials(int M, int N) {
+  const int cg = cta_group();
+  return ((M + 128 * cg - 1) / (128 * cg)) * ((N + kNsBN - 1) / kNsBN) * cg * 4;
+}
 
 void ns_gemm_set_cta_group(int cg) { g_cta_group = (cg == 1) ? 1 : 2; }
 int ns_gemm_cta_group() { return cta_group(); }

@@ -43,15 +43,27 @@ enum NsEpilogue : int {
                    //   (hi*lo + lo*hi + hi*hi)
 };
 
-// Where the last Newton-Schulz step of one matrix lands: the fp32 master
-// weight (and its bf16 replica) in the tensor's ORIGINAL orientation.
+// Where the last Newton-Schulz step of one matrix lands (kEpiFinal): the fp32
+// master weight and its bf16 replica in the tensor's ORIGINAL orientation.
+// The epilogue streams W through shared memory in 32 x 32 boxes (cp.async,
+// prefetched while the tile's MMAs run) and writes W and the replica in
+// 128 / 64-byte row segments, so the weight update costs one read and one
+// write of W and one replica write — no separate streaming pass.
 struct NsFinalTarget {
-  float* w;                   // [rows][cols] row-major fp32 master weight
-  __nv_bfloat16* replica;     // bf16 copy of the same tensor (nullable)
-  double* sq_norm;            // += ||lr * update||_F^2 (nullable)
-  int transposed;             // 1: the tensor is X^T (rows > cols in the reference)
+  float* w;                // fp32 W: not transposed [M][N], transposed [N][M]
+  __nv_bfloat16* replica;  // bf16 replica, same geometry (nullable)
+  double* partial;         // per (tile, CTA of the pair, epilogue warp): sum of (lr*update)^2
+  int transposed;          // 1: the tensor is X^T (rows > cols in the reference)
   int pad_;
 };
+
+// One target for an M x N iterate (M <= N). W and the replica must be
+// 16-byte aligned and their row pitch a multiple of 16 bytes
+// (final_target_ok). `partial` needs final_partials(M, N) doubles.
+bool final_target_ok(const void* w, const void* replica, int M, int N, int transposed);
+bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
+                       int transposed, double* partial);
+int final_partials(int M, int N);  // tiles * CTAs per tile * 4 epilogue warps
 
 struct alignas(64) NsGemmProblem {
   CUtensorMap tmA;  // [batch][M][K], K-major, box {64, 128, 1}

@@ -1,4 +1,5 @@
 """Times the grouped tcgen05 NS GEMM at the Qwen3-8B shape classes (CUDA events)."""
+import ctypes
 import json
 import sys
 
@@ -15,17 +16,17 @@ def mref(t):
     return m
 
 
-def bench(mode, probs, alpha=0.0, beta=0.0, iters=5):
+def bench(mode, probs, alpha=0.0, beta=0.0, iters=5, lr=0.0):
     arr = (_lib.GemmProblem * len(probs))(*probs)
     s = torch.cuda.current_stream().cuda_stream
     L = _lib.lib()
     for _ in range(2):
-        _lib.check(L.osh_ns_gemm(mode, arr, len(probs), alpha, beta, 0.0, s))
+        _lib.check(L.osh_ns_gemm(mode, arr, len(probs), alpha, beta, lr, s))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):
-        _lib.check(L.osh_ns_gemm(mode, arr, len(probs), alpha, beta, 0.0, s))
+        _lib.check(L.osh_ns_gemm(mode, arr, len(probs), alpha, beta, lr, s))
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters
@@ -47,6 +48,21 @@ def main():
         p = _lib.GemmProblem(); p.a = mref(a); p.b = mref(x); p.b_mn_major = 1; p.out = mref(o_mn); p.aux = mref(x)
         t = bench(2, [p], 3.4445); f = 2.0 * bt * m * m * n
         out[f"update_{bt}x{m}x{n}"] = {"ms": t, "tflops": f / t / 1e9}
+        p.aux = _lib.MatrixRef()
+        t = bench(2, [p], 0.0)
+        out[f"update_noaux_{bt}x{m}x{n}"] = {"ms": t, "tflops": f / t / 1e9}
+        # FINAL: W -= lr * (A X) in the epilogue, W fp32 in both orientations
+        if bt * m * n <= 4 * 4096 * 12288:
+            for tr in (0, 1):
+                w = torch.zeros(bt, n, m, device="cuda") if tr else torch.zeros(bt, m, n, device="cuda")
+                rep = torch.empty(w.shape, device="cuda", dtype=torch.bfloat16)
+                tg = (_lib.FinalTarget * bt)()
+                for i in range(bt):
+                    tg[i].w = w[i].data_ptr(); tg[i].replica = rep[i].data_ptr(); tg[i].transposed = tr
+                p.final_targets = ctypes.addressof(tg)
+                t = bench(3, [p], 0.0, lr=0.02)
+                out[f"final_t{tr}_{bt}x{m}x{n}"] = {"ms": t, "tflops": f / t / 1e9}
+                del w, rep
         del x, a, o_mm, o_mn
         torch.cuda.empty_cache()
     # cuBLAS reference point for the same shapes

@@ -118,8 +118,11 @@ def test_update_mn_major(batch, m, n):
 
 
 @pytest.mark.parametrize("transposed", [0, 1])
-def test_final_weight_update(transposed):
-    batch, m, n = 2, 128, 384
+@pytest.mark.parametrize("batch,m,n,alpha", [(2, 128, 384, A), (1, 256, 512, 0.0), (3, 200, 328, 0.0),
+                                             (1, 96, 1000, A), (1, 8, 24, 0.0)])
+def test_final_weight_update(transposed, batch, m, n, alpha):
+    """FINAL: W -= lr * (alpha X + B X) straight from the accumulator, W and
+    the bf16 replica moved by TMA boxes in the tensor's stored orientation."""
     x = padded(batch, m, n, scale=0.1)
     bm = padded(batch, m, m, scale=0.1, seed=2)
     w0 = torch.randn(batch, m, n, device="cuda")
@@ -128,29 +131,48 @@ def test_final_weight_update(transposed):
     else:
         w = w0.clone()
     rep = torch.zeros(w.shape, device="cuda", dtype=torch.bfloat16)
-    sq = torch.zeros(batch, device="cuda", dtype=torch.float64)
-    tg = (_lib.FinalTarget * batch)()
+    sq = torch.full((batch,), 0.5, device="cuda", dtype=torch.float64)  # accumulates (+=)
+    tg = (_lib.FinalTarget * batch)()   # host array (osh.h)
     for i in range(batch):
         tg[i].w = w[i].data_ptr()
         tg[i].replica = rep[i].data_ptr()
         tg[i].sq_norm = sq[i:].data_ptr()
         tg[i].transposed = transposed
-    tg_dev = torch.frombuffer(bytearray(tg), dtype=torch.uint8).cuda()
     p = _lib.GemmProblem()
     p.a = mref(bm)
     p.b = mref(x)
     p.b_mn_major = 1
     p.aux = mref(x)
-    p.final_targets = tg_dev.data_ptr()
+    p.final_targets = ctypes.addressof(tg)
     lr = 0.02
-    run(3, [p], alpha=A, lr=lr)
-    upd = lr * (A * x.float() + bm.float() @ x.float())
+    run(3, [p], alpha=alpha, lr=lr)
+    upd = lr * (alpha * x.float() + bm.float() @ x.float())
     ref = w0 - upd
     got = w.transpose(1, 2) if transposed else w
     assert (got - ref).abs().max().item() < 1e-3 * upd.abs().max().item() + 1e-6
     assert torch.equal(rep, w.bfloat16())
-    want_sq = (upd.double() ** 2).sum(dim=(1, 2))
+    want_sq = 0.5 + (upd.double() ** 2).sum(dim=(1, 2))
     assert torch.allclose(sq, want_sq, rtol=1e-2)
+
+
+def test_final_rejects_unaligned_pitch():
+    """A row pitch TMA cannot address is refused (the engine then keeps the
+    streaming update path for that wave)."""
+    m, n = 8, 22
+    x = padded(1, m, n, ld=24, scale=0.1)
+    bm = padded(1, m, m, scale=0.1, seed=2)
+    w = torch.zeros(1, m, n, device="cuda")
+    tg = (_lib.FinalTarget * 1)()
+    tg[0].w = w.data_ptr()
+    p = _lib.GemmProblem()
+    p.a = mref(bm)
+    p.b = mref(x, cols=n)
+    p.b_mn_major = 1
+    p.aux = mref(x, cols=n)
+    p.final_targets = ctypes.addressof(tg)
+    arr = (_lib.GemmProblem * 1)(p)
+    st = _lib.lib().osh_ns_gemm(3, arr, 1, 0.0, 0.0, 0.02, torch.cuda.current_stream().cuda_stream)
+    assert st == 19  # OSH_ERR_ARG
 
 
 def test_grouped_problems_one_launch():
