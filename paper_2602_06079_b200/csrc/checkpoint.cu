@@ -84,6 +84,12 @@ struct File {
   ~File() {
     if (f) std::fclose(f);
   }
+  // flush + close, reporting a failed final write-back (ENOSPC, EIO)
+  bool close() {
+    FILE* g = f;
+    f = nullptr;
+    return g != nullptr && std::fflush(g) == 0 && std::fclose(g) == 0;
+  }
 };
 
 }  // namespace
@@ -108,9 +114,12 @@ extern "C" osh_status osh_ctx_save_state(osh_ctx* ctx, const char* path) {
   h.step_counter = ctx->engine->step_counter();
   h.n_records = regs.size();
   h.extra_bytes = ctx->engine->extra_state_bytes();
+  // written next to the target and renamed into place: a failed or
+  // interrupted save never destroys the previous checkpoint
+  const std::string tmp = std::string(path) + ".tmp";
   File out;
-  out.f = std::fopen(path, "wb");
-  if (out.f == nullptr) return osh::fail(OSH_ERR_FORMAT, std::string("cannot open ") + path);
+  out.f = std::fopen(tmp.c_str(), "wb");
+  if (out.f == nullptr) return osh::fail(OSH_ERR_FORMAT, "cannot open " + tmp);
   bool ok = std::fwrite(&h, sizeof(h), 1, out.f) == 1;
   std::vector<float> buf;
   for (const Region& r : regs) {
@@ -128,7 +137,14 @@ extern "C" osh_status osh_ctx_save_state(osh_ctx* ctx, const char* path) {
                             cudaMemcpyDeviceToHost));
     ok = ok && std::fwrite(extra.data(), 1, extra.size(), out.f) == extra.size();
   }
-  if (!ok) return osh::fail(OSH_ERR_FORMAT, std::string("short write to ") + path);
+  if (!out.close() || !ok) {
+    std::remove(tmp.c_str());
+    return osh::fail(OSH_ERR_FORMAT, "short write to " + tmp);
+  }
+  if (std::rename(tmp.c_str(), path) != 0) {
+    std::remove(tmp.c_str());
+    return osh::fail(OSH_ERR_FORMAT, std::string("cannot rename ") + tmp + " to " + path);
+  }
   return OSH_OK;
 }
 
@@ -148,10 +164,27 @@ extern "C" osh_status osh_ctx_load_state(osh_ctx* ctx, const char* path) {
   if (h.optimizer != ctx->optimizer || h.dp_rank != ctx->rank || h.dp_size != ctx->size ||
       h.tp_rank != ctx->tp_rank || h.tp_size != ctx->tp_size ||
       h.n_params != static_cast<int32_t>(ctx->params.size()) || h.plan_hash != plan_hash(ctx) ||
-      h.n_records != regs.size() || h.extra_bytes != ctx->engine->extra_state_bytes())
+      h.grad_dtype != ctx->grad_dtype || h.n_records != regs.size() ||
+      h.extra_bytes != ctx->engine->extra_state_bytes())
     return osh::fail(OSH_ERR_FORMAT, std::string(path) +
-                                         ": checkpoint belongs to a different rank, plan, model "
-                                         "or optimizer");
+                                         ": checkpoint belongs to a different rank, plan, model, "
+                                         "gradient dtype or optimizer");
+  // validation pass: every record header and the exact file length, before
+  // any device state is touched (a bad file never leaves the ctx half restored)
+  const long data0 = std::ftell(in.f);
+  for (const Region& r : regs) {
+    int32_t pid = -1;
+    int64_t numel = -1;
+    if (std::fread(&pid, sizeof(pid), 1, in.f) != 1 || std::fread(&numel, sizeof(numel), 1, in.f) != 1 ||
+        pid != r.pid || numel != r.numel ||
+        std::fseek(in.f, static_cast<long>(8 * numel), SEEK_CUR) != 0)
+      return osh::fail(OSH_ERR_FORMAT, std::string(path) + ": tensor record mismatch");
+  }
+  const long expect_end = std::ftell(in.f) + static_cast<long>(h.extra_bytes);
+  if (std::fseek(in.f, 0, SEEK_END) != 0 || std::ftell(in.f) != expect_end)
+    return osh::fail(OSH_ERR_FORMAT, std::string(path) + ": truncated or oversized");
+  if (std::fseek(in.f, data0, SEEK_SET) != 0)
+    return osh::fail(OSH_ERR_FORMAT, std::string(path) + ": seek failed");
   std::vector<float> buf;
   for (const Region& r : regs) {
     int32_t pid = -1;

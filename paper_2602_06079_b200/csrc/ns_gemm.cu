@@ -8,6 +8,7 @@
 // tile i+1. Tiles of all problems are linearised and strided over the grid.
 #include "ns_gemm.cuh"
 #include "sm100.cuh"
+#include "status.hpp"
 
 #include <algorithm>
 #include <cstdio>
@@ -695,28 +696,15 @@ bool make_map(CUtensorMap* map, const NsMatrixRef& m, uint32_t box_cols, uint32_
          CUDA_SUCCESS;
 }
 
-int sm_count() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  });
-  return n;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int MODE, int CG>
 cudaError_t launch_mode(const NsGemmParams& P, cudaStream_t stream) {
-  static bool configured = false;
   constexpr uint32_t smem = smem_bytes<MODE, CG>();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ns_gemm_kernel<MODE, CG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = set_max_dynamic_smem(reinterpret_cast<const void*>(ns_gemm_kernel<MODE, CG>),
+                                           static_cast<int>(smem));
+      e != cudaSuccess)
+    return e;
   if constexpr (CG == 1) {
     const int grid = std::min(P.total_tiles, sm_count());
     ns_gemm_kernel<MODE, 1><<<grid, kNsThreads, smem, stream>>>(P);

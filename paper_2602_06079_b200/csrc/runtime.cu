@@ -124,6 +124,12 @@ void free_layout(osh_ctx* ctx) {
 
 namespace osh {
 
+cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cast_f32_bf16_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
 // Issues ops [begin, end) of the ctx's collective schedule on `st`; ops of
 // one group id go inside one ncclGroupStart / ncclGroupEnd.
 osh_status issue_ops(osh_ctx* ctx, int begin, int end, cudaStream_t st) {
@@ -156,10 +162,12 @@ osh_status issue_ops(osh_ctx* ctx, int begin, int end, cudaStream_t st) {
   return OSH_OK;
 }
 
-// The bf16 replica from the owners' fp32 masters: every rank casts the
-// tensors it owns into its replica slots, then the AG-v leg of the schedule
-// broadcasts each slice from its owner (the plan's cut owners, or the layer
-// owners under NV-layerwise; tp_size == 1 — with TP the next step refreshes it).
+// The bf16 replica from the owners' fp32 masters (checkpoint resume): every
+// rank casts the tensors it owns into its replica slots; with TP the hosts
+// cast their full masters and scatter each rank its shard (the step's
+// pack + scatter path); then the AG-v leg of the schedule broadcasts each
+// slice from its owner (the plan's cut owners, or the layer owners under
+// NV-layerwise).
 osh_status refresh_replica(osh_ctx* ctx) {
   cudaStream_t cs = ctx->compute;
   for (size_t p = 0; p < ctx->params.size(); ++p) {
@@ -169,7 +177,10 @@ osh_status refresh_replica(osh_ctx* ctx) {
                                                      ctx->replica + ctx->flat_off[p], n);
   }
   OSH_CUDA_TRY(cudaGetLastError());
-  if (distributed(ctx) && ctx->tp_size == 1 && !ctx->sched_ag.empty()) {
+  if (ctx->tp_size > 1)
+    if (osh_status st = tp_refresh_replica(ctx, cs); st != OSH_OK) return st;
+  const bool ag = ctx->comm_mode == OSH_COMM_NCCL && ctx->size > 1 && ctx->comm != nullptr;
+  if (ag && !ctx->sched_ag.empty()) {
     const int b0 = ctx->sched_ag.front().first, b1 = ctx->sched_ag.back().second;
     if (osh_status st = issue_ops(ctx, b0, b1, cs); st != OSH_OK) return st;
   }

@@ -142,9 +142,11 @@ namespace osh {
 // TP helpers (tp.cu)
 osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
 osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
+osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs);  // checkpoint resume
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);
 osh_status refresh_replica(osh_ctx* ctx);  // runtime.cu (checkpoint load)
+cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
 // NVLS helpers (nvls.cu)
 osh_status nvls_setup(osh_ctx* ctx, size_t grad_bytes, size_t replica_bytes, bool required);
 void nvls_free(osh_ctx* ctx);

@@ -1,5 +1,6 @@
 // Blocked-SOAP kernels (see soap_kernels.cuh).
 #include "soap_kernels.cuh"
+#include "status.hpp"
 
 #include "elementwise_util.cuh"
 
@@ -675,14 +676,12 @@ cudaError_t launch_soap_adam(const SoapAdamTask* d, int n, long long tiles, int 
 cudaError_t launch_soap_basis(const SoapBasisTask* d, int n, float shift, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   // dynamic shared memory: est, nrm (float) and order (int) of the largest matrix
-  static int max_n = 4096;
+  constexpr int max_n = 4096;
   const size_t smem = static_cast<size_t>(max_n) * 12;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(soap_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  if (cudaError_t e = set_max_dynamic_smem(reinterpret_cast<const void*>(soap_basis_kernel),
+                                           static_cast<int>(smem));
+      e != cudaSuccess)
+    return e;
   soap_basis_kernel<<<n, kBasisThreads, smem, s>>>(d, shift);
   return cudaGetLastError();
 }
@@ -710,12 +709,10 @@ cudaError_t launch_soap_split(const SoapSplitTask* d, int n, long long tiles, cu
 
 cudaError_t launch_soap_chol_inv(const SoapCholTask* d, int n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(soap_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kCholSmem));
-    attr = true;
-  }
+  if (cudaError_t e = set_max_dynamic_smem(reinterpret_cast<const void*>(soap_chol_inv_kernel),
+                                           static_cast<int>(kCholSmem));
+      e != cudaSuccess)
+    return e;
   soap_chol_inv_kernel<<<n, kCholThreads, kCholSmem, s>>>(d);
   return cudaGetLastError();
 }

@@ -1,6 +1,10 @@
 #include "status.hpp"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <set>
+#include <utility>
 
 namespace osh {
 namespace {
@@ -29,6 +33,32 @@ cudaError_t dev_alloc(void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   return e;
+}
+
+cudaError_t set_max_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, dev}) != 0) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
+}
+
+int device_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> counts;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = counts.find(dev);
+  if (it != counts.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  counts[dev] = n;
+  return n;
 }
 
 }  // namespace osh

@@ -19,6 +19,13 @@ osh_status fail(osh_status code, const std::string& msg);
 cudaError_t dev_alloc(void** p, size_t bytes);
 bool debug_poison();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `kernel` on the CURRENT
+// device, set once per (kernel, device); thread-safe (contexts on several GPUs
+// may share one process).
+cudaError_t set_max_dynamic_smem(const void* kernel, int bytes);
+// Multiprocessor count of the current device (cached per device).
+int device_sm_count();
+
 }  // namespace osh
 
 #define OSH_CUDA_TRY(expr)                                                          \

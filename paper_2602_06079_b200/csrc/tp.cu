@@ -72,6 +72,47 @@ cudaError_t upload_vec(T** dst, const std::vector<T>& src) {
 
 }  // namespace
 
+// Host -> peers: each TP rank's updated bf16 shard of every group-g item
+// lands in its replica slot (tp_pack must have run on `st`'s timeline).
+osh_status issue_tp_scatter(osh_ctx* ctx, int g, cudaStream_t st) {
+  const int T = ctx->tp_size, me = ctx->tp_rank;
+  TP_NCCL(ncclGroupStart());
+  for (osh_ctx::TpItem& it : ctx->tp_items) {
+    if (it.group != g) continue;
+    const size_t shard = static_cast<size_t>(it.full_rows * it.full_cols / T);
+    if (it.host != me) {
+      TP_NCCL(ncclRecv(ctx->replica + ctx->flat_off[it.pid], shard, ncclBfloat16, it.host,
+                       ctx->tp_comm, st));
+      continue;
+    }
+    for (int t = 0; t < T; ++t) {
+      if (t == me) continue;
+      const void* src = it.split_dim == 0
+                            ? static_cast<const void*>(it.rep_full + t * shard)
+                            : static_cast<const void*>(reinterpret_cast<__nv_bfloat16*>(it.stage) +
+                                                       t * shard);
+      TP_NCCL(ncclSend(src, shard, ncclBfloat16, t, ctx->tp_comm, st));
+    }
+  }
+  TP_NCCL(ncclGroupEnd());
+  return OSH_OK;
+}
+
+// The TP-plane part of the replica from the hosts' fp32 masters (checkpoint
+// resume): cast every hosted full master, pack each rank's shard and scatter
+// it, group by group, all on `cs`.
+osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs) {
+  for (osh_ctx::TpItem& it : ctx->tp_items)
+    if (it.w != nullptr)
+      OSH_CUDA_TRY(cast_to_bf16(it.w, it.rep_full, it.full_rows * it.full_cols, cs));
+  for (int g = 0; g < ctx->tp_groups; ++g) {
+    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
+                                    ctx->tp_pack_tiles[g], cs));
+    if (osh_status st = issue_tp_scatter(ctx, g, cs); st != OSH_OK) return st;
+  }
+  return OSH_OK;
+}
+
 void* grad_ptr(osh_ctx* ctx, int pid) {
   const size_t es = gsize(ctx);
   if (ctx->grad_owned != nullptr && ctx->owner[pid] == ctx->rank) {
@@ -280,25 +321,7 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
     OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
     OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
     // ---- scatter updated bf16 shards into every rank's replica slot
-    TP_NCCL(ncclGroupStart());
-    for (osh_ctx::TpItem& it : ctx->tp_items) {
-      if (it.group != g) continue;
-      const size_t shard = static_cast<size_t>(it.full_rows * it.full_cols / T);
-      if (it.host != me) {
-        TP_NCCL(ncclRecv(ctx->replica + ctx->flat_off[it.pid], shard, ncclBfloat16, it.host,
-                         ctx->tp_comm, ts));
-        continue;
-      }
-      for (int t = 0; t < T; ++t) {
-        if (t == me) continue;
-        const void* src = it.split_dim == 0
-                              ? static_cast<const void*>(it.rep_full + t * shard)
-                              : static_cast<const void*>(reinterpret_cast<__nv_bfloat16*>(it.stage) +
-                                                         t * shard);
-        TP_NCCL(ncclSend(src, shard, ncclBfloat16, t, ctx->tp_comm, ts));
-      }
-    }
-    TP_NCCL(ncclGroupEnd());
+    if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ts));
   OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_done_ev, 0));

@@ -42,6 +42,7 @@ def main():
     opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
     announce = len(sys.argv) > 4 and sys.argv[4] == "buckets"  # osh_bucket_ready, reverse order
     host = len(sys.argv) > 4 and sys.argv[4] == "host"  # e2e entry: host gradients / replica
+    ckpt = len(sys.argv) > 4 and sys.argv[4] == "ckpt"  # save / reload into a fresh ctx
     strategy = sys.argv[5] if len(sys.argv) > 5 else "sharded"  # or the sc / nv-layerwise baselines
     gdt = sys.argv[6] if len(sys.argv) > 6 else "f32"  # bf16: NVLS reduces bf16x8 with fp32 accumulation
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -99,18 +100,36 @@ def main():
         except Exception:
             pass
     replica = {p.id: eng.read_param(p.id, "replica") for p in params}
+    ckpt_ok = True
+    if ckpt:
+        # a FRESH ctx (zeroed replica) restored from this rank's file must
+        # rebuild every rank's full replica from the owners' masters
+        import tempfile
+        path = os.path.join(tempfile.gettempdir(), f"osh_ckpt_{os.getpid()}.osh")
+        eng.save_state(path)
+        eng.close()
+        uid2 = [nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(uid2, src=0)
+        eng = DistributedMuon(params, cap, plan, rank=rank, device=local, comm="nccl",
+                              nccl_uid=uid2[0], grad_dtype=gdt, collectives=coll, optimizer=opt,
+                              shampoo=(SCFG if opt == "shampoo" else SOCFG if opt == "soap" else None),
+                              strategy=strategy)
+        eng.load_state(path)
+        os.remove(path)
+        again = {p.id: eng.read_param(p.id, "replica") for p in params}
+        ckpt_ok = all(np.array_equal(again[k], replica[k]) for k in replica)
     if host:  # the replica the step copied out must equal the device replica
         off = 0
         for p in params:
             assert np.array_equal(hrep[off:off + p.numel].float().numpy(), replica[p.id].reshape(-1))
             off += p.numel
     gathered = [None] * world
-    td.all_gather_object(gathered, (mine, norms, replica))
+    td.all_gather_object(gathered, (mine, norms, replica, ckpt_ok))
     eng.close()
     if rank != 0:
         return 0
     weights, gnorms = {}, np.full((steps, len(params)), -1.0)
-    for m, n, _ in gathered:
+    for m, n, _, _ in gathered:
         weights.update(m)
         for s in range(steps):
             gnorms[s] = np.where(n[s] >= 0, n[s], gnorms[s])
@@ -147,7 +166,8 @@ def main():
                 rnorms[s, p.id] = SO.soap_apply(st[p.id], socfg, w[p.id], g.reshape(w[p.id].shape), s)
             else:
                 rnorms[s, p.id] = O.muon_apply(p.is_matrix, cfg, w[p.id], mom[p.id], g)
-    report, ok = {}, sched_ok
+    ckpt_all = all(g[3] for g in gathered)
+    report, ok = {}, sched_ok and ckpt_all
     for p in params:
         got, ref = weights[p.id].reshape(-1), w[p.id].reshape(-1)
         e_w = float(np.abs(got - ref).max() / np.abs(ref).max())
@@ -178,7 +198,8 @@ def main():
                           "replica_bitexact": rep_ok, "ok": good}
     print(json.dumps({"world": world, "steps": steps, "collectives": path, "optimizer": opt,
                       "bucket_ready": announce, "host_buffers": host, "strategy": strategy,
-                      "grad_dtype": gdt, "schedule_matches": sched_ok, "ok": ok,
+                      "grad_dtype": gdt, "schedule_matches": sched_ok,
+                      "checkpoint_replica_ok": ckpt_all if ckpt else None, "ok": ok,
                       "params": report}))
     return 0 if ok else 1
 

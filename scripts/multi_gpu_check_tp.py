@@ -51,6 +51,7 @@ def bf16(x):
 def main():
     D, T = int(sys.argv[1]), int(sys.argv[2])
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    ckpt = len(sys.argv) > 4 and sys.argv[4] == "ckpt"  # save / reload: replica rebuilt?
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == D * T
     d, t = rank // T, rank % T
@@ -96,8 +97,26 @@ def main():
         except Exception:
             pass  # TP-plane tensor hosted by the other TP rank
     replica = {p.id: eng.read_param(p.id, "replica", shape=shards[p.id].shape) for p in full}
+    ckpt_ok = True
+    if ckpt:
+        # every rank saves its state, a FRESH ctx (zero replica) loads it: the
+        # TP hosts' masters must come back as every rank's replica shards
+        import tempfile
+        path = os.path.join(tempfile.gettempdir(), f"osh_tp_ckpt_{os.getpid()}.osh")
+        eng.save_state(path)
+        eng.close()
+        mine2 = {"dp": nccl_unique_id() if d == 0 else None, "tp": nccl_unique_id() if t == 0 else None}
+        ids2 = [None] * world
+        td.all_gather_object(ids2, mine2)
+        eng = DistributedMuon(full, cap, plan, rank=d, device=local, comm="nccl",
+                              nccl_uid=ids2[t]["dp"], grad_dtype="f32", tp_rank=t, tp_size=T,
+                              tp_uid=ids2[d * T]["tp"], tp_capacity=200_000)
+        eng.load_state(path)
+        os.remove(path)
+        again = {p.id: eng.read_param(p.id, "replica", shape=shards[p.id].shape) for p in full}
+        ckpt_ok = all(np.array_equal(again[k], replica[k]) for k in replica)
     gathered = [None] * world
-    td.all_gather_object(gathered, (d, t, res, norms, replica))
+    td.all_gather_object(gathered, (d, t, res, norms, replica, ckpt_ok))
     eng.close()
     if rank != 0:
         return 0
@@ -122,7 +141,7 @@ def main():
     ok, report = True, {}
     for p in full:
         plane = p.tp_split != P.TP_NONE and not p.vocab_space
-        found = [(gt, r[p.id]) for (gd, gt, r, _, _) in gathered if p.id in r]
+        found = [(gt, r[p.id]) for (gd, gt, r, _, _, _) in gathered if p.id in r]
         if not found:
             ok = False
             report[p.name] = {"ok": False, "why": "no rank returned it"}
@@ -138,12 +157,15 @@ def main():
         e_w = float(np.abs(got_full - ref_full).max() / np.abs(ref_full).max())
         tol = 2.5e-3 if p.is_matrix else 1e-5
         rep_ok = all(np.array_equal(rep[p.id].reshape(-1), bf16(shard_of(got_full, p, T, gt)).reshape(-1))
-                     for (gd, gt, _, _, rep) in gathered)
+                     for (gd, gt, _, _, rep, _) in gathered)
         good = e_w <= tol and rep_ok
         ok &= good
         report[p.name] = {"owner": int(owners[p.id]), "tp_plane": plane, "w": f"{e_w:.2e}",
                           "replica_bitexact": rep_ok, "ok": good}
-    print(json.dumps({"dp": D, "tp": T, "steps": steps, "ok": ok, "params": report}))
+    ckpt_ok = all(g[5] for g in gathered)
+    ok &= ckpt_ok
+    print(json.dumps({"dp": D, "tp": T, "steps": steps, "checkpoint_replica_ok": ckpt_ok if ckpt else None,
+                      "ok": ok, "params": report}))
     return 0 if ok else 1
 
 

@@ -111,3 +111,40 @@ def test_checkpoint_refuses_other_plan_or_rank(tmp_path):
     with pytest.raises(_lib.OshError) as e:
         m2[0].load_state(str(tmp_path / "r0.osh"))
     assert e.value.code == 7
+
+
+def test_damaged_checkpoint_leaves_state_untouched(tmp_path):
+    """A truncated file, or one saved with another gradient dtype, is refused
+    before any device state is written; saving goes through a temporary file
+    that is renamed into place (no '.tmp' left behind)."""
+    ps = params()
+    a = make(ps, 1, "muon")
+    for p in ps:
+        a[0].load_param(p.id, O.init_weight(p.shape, p.id, SEED))
+    steps(a, ps, 0, 2)
+    path = tmp_path / "r0.osh"
+    a[0].save_state(str(path))
+    assert path.exists() and not (tmp_path / "r0.osh.tmp").exists()
+    before = snapshot(a, ps)
+    raw = path.read_bytes()
+    cut = tmp_path / "cut.osh"
+    cut.write_bytes(raw[: len(raw) - 4096])
+    b = make(ps, 1, "muon")
+    for p in ps:
+        b[0].load_param(p.id, np.zeros(p.shape, np.float32))
+    pristine = snapshot(b, ps)
+    with pytest.raises(_lib.OshError) as e:
+        b[0].load_state(str(cut))
+    assert e.value.code == 7
+    after = snapshot(b, ps)
+    for k in pristine[0]:
+        assert np.array_equal(pristine[0][k], after[0][k]), k  # nothing half restored
+    plan = P.plan_dp(ps, 600_000, 1, "alpha-balanced", "numel", 1.0)
+    with DistributedMuon(ps, 600_000, plan, comm="none", grad_dtype="bf16") as bf:
+        with pytest.raises(_lib.OshError) as e:
+            bf.load_state(str(path))
+        assert e.value.code == 7
+    b[0].load_state(str(path))  # the intact file still restores exactly
+    got = snapshot(b, ps)
+    for k in before[0]:
+        assert np.array_equal(before[0][k], got[0][k]), k

@@ -110,3 +110,22 @@ def test_dp4_nccl_matches_oracle():
 
 def test_dp4_auto_matches_oracle():
     _run(4, "multi_gpu_check.py", 3, "auto")
+
+
+@pytest.mark.parametrize("strategy,coll", [("nv-layerwise", "nccl"), ("sharded", "auto")])
+def test_dp2_checkpoint_restores_replica(strategy, coll):
+    # a fresh ctx restored from each rank's file rebuilds every rank's replica
+    # (NV-layerwise: broadcast from the layer owners, not the plan's cuts)
+    res = _run(2, "multi_gpu_check.py", 2, coll, "muon", "ckpt", strategy)
+    assert res["checkpoint_replica_ok"] is True
+
+
+def test_tp2_checkpoint_restores_replica():
+    # TP hosts cast their full masters and scatter the shards on resume
+    res = _run(2, "multi_gpu_check_tp.py", 1, 2, 2, "ckpt")
+    assert res["checkpoint_replica_ok"] is True
+
+
+def test_dp2_tp2_checkpoint_restores_replica():
+    res = _run(4, "multi_gpu_check_tp.py", 2, 2, 2, "ckpt")
+    assert res["checkpoint_replica_ok"] is True
