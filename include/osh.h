@@ -393,7 +393,15 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
  * EVERY bucket (any order, the same order on every rank) before osh_step —
  * which then only waits for them — or none. */
 osh_status osh_bucket_ready(osh_ctx* ctx, int32_t bucket, void* stream);
+/* Waits for the ctx's streams. Every host wait of the library (this, the
+ * host-buffer osh_step, checkpoint resume) is a watchdog: it polls the NCCL
+ * communicators' async errors, and when a collective reports an error or does
+ * not complete within the timeout (default 600 s, OSH_COMM_TIMEOUT_S or
+ * osh_ctx_set_timeout) the communicators are aborted (ncclCommAbort) and the
+ * call returns OSH_ERR_NCCL instead of hanging; the ctx then refuses further
+ * steps and must be destroyed. */
 osh_status osh_ctx_sync(osh_ctx* ctx);
+osh_status osh_ctx_set_timeout(osh_ctx* ctx, double seconds);
 /* The ctx's compute stream (cudaStream_t): the step's last event is recorded
  * on it, so events recorded here bracket whole steps. */
 osh_status osh_ctx_stream(osh_ctx* ctx, void** stream);

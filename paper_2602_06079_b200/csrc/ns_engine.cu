@@ -116,15 +116,16 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   // owns few others) forms a wave of its own; the rest keep the target size
   if (min_waves > 1) cap = std::min(cap, (total_ws + min_waves - 1) / min_waves);
 
-  // FINAL fusion is a property of the TENSOR (TMA/vector-addressable W and a
-  // local replica), never of the wave it lands in, so results do not depend
+  // FINAL fusion is a property of the TENSOR (vector-addressable W and
+  // replica; an NVLS replica is written with multimem.st, fusing the AG-v into
+  // the epilogue), never of the wave it lands in, so results do not depend
   // on how the plan groups tensors (sharded == replicated bit for bit).
   const char* ff = std::getenv("OSH_FUSE_FINAL");
   fuse_final_ = !(ff != nullptr && std::strcmp(ff, "0") == 0);
   std::vector<char> fused_t(tensors.size(), 0);
   for (size_t i = 0; i < tensors.size(); ++i) {
     const MuonTensorDesc& t = tensors[i];
-    if (!t.is_matrix || !fuse_final_ || t.rep_mc) continue;
+    if (!t.is_matrix || !fuse_final_) continue;
     const Shape s = shape_of(t.rows, t.cols);
     fused_t[i] = final_target_ok(t.w, t.replica, s.m, s.n, t.rows > t.cols ? 1 : 0) ? 1 : 0;
   }
@@ -371,7 +372,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     for (size_t i = 0; i < ftargets.size(); ++i) {
       const MuonTensorDesc& t = tensors[ftargets[i].ti];
       if (!make_final_target(&ft[i], t.w, t.replica, ftargets[i].m, ftargets[i].n,
-                             t.rows > t.cols ? 1 : 0, d_fpartial_ + ftargets[i].poff))
+                             t.rows > t.cols ? 1 : 0, d_fpartial_ + ftargets[i].poff, t.rep_mc))
         return fail(OSH_ERR_CUDA, "MuonEngine: cannot encode the FINAL TMA maps");
     }
     OSH_CUDA_TRY(upload(&d_ftargets_, ft));

@@ -7,6 +7,7 @@
 // The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
 // tile i+1. Tiles of all problems are linearised and strided over the grid.
 #include "ns_gemm.cuh"
+#include "elementwise_util.cuh"
 #include "sm100.cuh"
 #include "status.hpp"
 
@@ -393,7 +394,9 @@ __device__ __forceinline__ void final_epilogue(const NsGemmParams& P, int it_beg
             h.y = pack_bf16(a.z, a.w);
             h.z = pack_bf16(b.x, b.y);
             h.w = pack_bf16(b.z, b.w);
-            st_global_v4_evict_first(rep + static_cast<long long>(grow0 + rr) * ld + gc, h, pol);
+            __nv_bfloat16* rd = rep + static_cast<long long>(grow0 + rr) * ld + gc;
+            if (ft.rep_mc) ew::mc_store16(rd, h);  // AG-v fused: the switch writes every GPU
+            else st_global_v4_evict_first(rd, h, pol);
           }
         }
       }
@@ -413,6 +416,7 @@ __device__ __forceinline__ void final_epilogue(const NsGemmParams& P, int it_beg
     acc ^= 1;
     if (acc == 0) acc_phase ^= 1;
   }
+  __threadfence_system();  // multicast replica stores are visible before the step's end barrier
 }
 
 template <int MODE, int CG>
@@ -755,13 +759,14 @@ bool final_target_ok(const void* w, const void* replica, int M, int N, int trans
 }
 
 bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
-                       int transposed, double* partial) {
+                       int transposed, double* partial, int rep_mc) {
   std::memset(t, 0, sizeof(*t));
   if (!final_target_ok(w, replica, M, N, transposed) || partial == nullptr) return false;
   t->w = w;
   t->replica = replica;
   t->partial = partial;
   t->transposed = transposed;
+  t->rep_mc = replica != nullptr && rep_mc ? 1 : 0;
   return true;
 }
 

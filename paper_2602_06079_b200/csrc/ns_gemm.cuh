@@ -54,7 +54,7 @@ struct NsFinalTarget {
   __nv_bfloat16* replica;  // bf16 replica, same geometry (nullable)
   double* partial;         // per (tile, CTA of the pair, epilogue warp): sum of (lr*update)^2
   int transposed;          // 1: the tensor is X^T (rows > cols in the reference)
-  int pad_;
+  int rep_mc;              // replica is an NVLS multicast address: multimem.st to every GPU
 };
 
 // One target for an M x N iterate (M <= N). W and the replica must be
@@ -62,7 +62,7 @@ struct NsFinalTarget {
 // (final_target_ok). `partial` needs final_partials(M, N) doubles.
 bool final_target_ok(const void* w, const void* replica, int M, int N, int transposed);
 bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
-                       int transposed, double* partial);
+                       int transposed, double* partial, int rep_mc = 0);
 int final_partials(int M, int N);  // tiles * CTAs per tile * 4 epilogue warps
 
 struct alignas(64) NsGemmProblem {

@@ -2,10 +2,12 @@
 #include "runtime.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "status.hpp"
@@ -124,6 +126,41 @@ void free_layout(osh_ctx* ctx) {
 
 namespace osh {
 
+osh_status abort_comms(osh_ctx* ctx, const std::string& why) {
+  if (ctx->comm != nullptr) ncclCommAbort(ctx->comm);
+  if (ctx->tp_comm != nullptr) ncclCommAbort(ctx->tp_comm);
+  ctx->comm = nullptr;
+  ctx->tp_comm = nullptr;
+  ctx->aborted = true;
+  return fail(OSH_ERR_NCCL, why + " (communicators aborted; destroy this ctx)");
+}
+
+osh_status wait_stream(osh_ctx* ctx, cudaStream_t stream) {
+  if (ctx->comm == nullptr && ctx->tp_comm == nullptr) {
+    OSH_CUDA_TRY(cudaStreamSynchronize(stream));
+    return OSH_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int polls = 0;; ++polls) {
+    const cudaError_t q = cudaStreamQuery(stream);
+    if (q == cudaSuccess) return OSH_OK;
+    if (q != cudaErrorNotReady)
+      return fail(OSH_ERR_CUDA, std::string("stream wait: ") + cudaGetErrorString(q));
+    for (ncclComm_t c : {ctx->comm, ctx->tp_comm}) {
+      if (c == nullptr) continue;
+      ncclResult_t ae = ncclSuccess;
+      if (ncclCommGetAsyncError(c, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress))
+        return abort_comms(ctx, std::string("NCCL async error: ") + ncclGetErrorString(ae));
+    }
+    const double waited =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (waited > ctx->timeout_s)
+      return abort_comms(ctx, "collective did not complete within " + std::to_string(ctx->timeout_s) +
+                                  " s (a peer rank stalled or died)");
+    if (polls > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   cast_f32_bf16_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
@@ -184,8 +221,7 @@ osh_status refresh_replica(osh_ctx* ctx) {
     const int b0 = ctx->sched_ag.front().first, b1 = ctx->sched_ag.back().second;
     if (osh_status st = issue_ops(ctx, b0, b1, cs); st != OSH_OK) return st;
   }
-  OSH_CUDA_TRY(cudaStreamSynchronize(cs));
-  return OSH_OK;
+  return wait_stream(ctx, cs);
 }
 
 // RS-v of bucket b on the comm stream: the owner of each slice receives the
@@ -235,6 +271,8 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
   ctx->rank = dp_rank;
   ctx->size = dp_size;
   ctx->comm_mode = comm_mode;
+  if (const char* to = std::getenv("OSH_COMM_TIMEOUT_S"); to != nullptr && std::atof(to) > 0.0)
+    ctx->timeout_s = std::atof(to);
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking));
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   int prio_low = 0, prio_high = 0;
@@ -344,7 +382,7 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
   cudaStreamSynchronize(ctx->d2h_stream);
   free_layout(ctx);
   if (ctx->comm != nullptr) ncclCommDestroy(ctx->comm);
-  if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);
+  if (ctx->tp_comm != nullptr) ncclCommDestroy(ctx->tp_comm);  // (nullptr once aborted)
   if (ctx->tp_stream != nullptr) {
     cudaStreamSynchronize(ctx->tp_stream);
     cudaStreamDestroy(ctx->tp_stream);
@@ -917,6 +955,8 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
                     void* host_replica_out) {
   if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
   if (cfg == nullptr) return osh::fail(OSH_ERR_ARG, "null cfg");
+  if (ctx->aborted || (ctx->comm_mode == OSH_COMM_NCCL && ctx->size > 1 && ctx->comm == nullptr))
+    return osh::fail(OSH_ERR_NCCL, "osh_step: the communicators were aborted by the watchdog");
   const size_t gbytes = grad_esize(ctx->grad_dtype) * static_cast<size_t>(ctx->total_numel);
   const bool dist = distributed(ctx);
   cudaStream_t cs = ctx->compute, ns = ctx->comm_stream;
@@ -1019,7 +1059,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     ctx->last_timing.gemm_launches = s.launches_gemm;
     ctx->last_timing.elementwise_launches = s.launches_elementwise;
     ctx->last_timing.gemm_flops = s.gemm_flops;
-    if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+    if (host_replica_out != nullptr) return osh::wait_stream(ctx, cs);
     return OSH_OK;
   }
   if (dist && ctx->strategy != OSH_STRAT_SHARDED) {
@@ -1067,7 +1107,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     ctx->last_timing.gemm_launches = s.launches_gemm;
     ctx->last_timing.elementwise_launches = s.launches_elementwise;
     ctx->last_timing.gemm_flops = s.gemm_flops;
-    if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+    if (host_replica_out != nullptr) return osh::wait_stream(ctx, cs);
     return OSH_OK;
   }
   if (dist && !marked) {
@@ -1143,7 +1183,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   ctx->last_timing.gemm_launches = s.launches_gemm;
   ctx->last_timing.elementwise_launches = s.launches_elementwise;
   ctx->last_timing.gemm_flops = s.gemm_flops;
-  if (host_replica_out != nullptr) OSH_CUDA_TRY(cudaStreamSynchronize(cs));
+  if (host_replica_out != nullptr) return osh::wait_stream(ctx, cs);
   return OSH_OK;
 }
 
@@ -1171,15 +1211,16 @@ osh_status osh_bucket_ready(osh_ctx* ctx, int32_t bucket, void* stream) {
 
 osh_status osh_ctx_sync(osh_ctx* ctx) {
   if (osh_status st = check_ctx(ctx, false); st != OSH_OK) return st;
-  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->compute));
-  OSH_CUDA_TRY(cudaStreamSynchronize(ctx->comm_stream));
-  if (ctx->comm != nullptr) {
-    ncclResult_t async_err = ncclSuccess;
-    OSH_NCCL_TRY(ncclCommGetAsyncError(ctx->comm, &async_err));
-    if (async_err != ncclSuccess)
-      return osh::fail(OSH_ERR_NCCL, std::string("NCCL async error: ") +
-                                         ncclGetErrorString(async_err));
-  }
+  if (osh_status st = osh::wait_stream(ctx, ctx->compute); st != OSH_OK) return st;
+  if (osh_status st = osh::wait_stream(ctx, ctx->comm_stream); st != OSH_OK) return st;
+  if (ctx->aborted) return osh::fail(OSH_ERR_NCCL, "communicators were aborted by the watchdog");
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_timeout(osh_ctx* ctx, double seconds) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (!(seconds > 0.0)) return osh::fail(OSH_ERR_CONFIG, "timeout must be positive");
+  ctx->timeout_s = seconds;
   return OSH_OK;
 }
 

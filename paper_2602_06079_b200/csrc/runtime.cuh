@@ -106,6 +106,11 @@ struct osh_ctx {
   std::vector<std::pair<int, int>> sched_rs, sched_ag;
   bool layout_ready = false;
   osh_step_timing last_timing{};
+  // watchdog (osh::wait_stream): host waits poll the streams and the NCCL
+  // communicators' async errors; past timeout_s the communicators are
+  // aborted and the ctx refuses further collective work
+  double timeout_s = 600.0;
+  bool aborted = false;
 
   // ---- tensor parallelism: micro-group gather -> host Muon -> scatter
   // (paper Alg. 2; state keyed by (dp owner, tp host) as in
@@ -146,6 +151,10 @@ osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs);  // checkpoint res
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);
 osh_status refresh_replica(osh_ctx* ctx);  // runtime.cu (checkpoint load)
+// Waits for `stream` like cudaStreamSynchronize, but polls the ctx's NCCL
+// communicators: an async NCCL error, or no completion within
+// ctx->timeout_s, aborts them (ncclCommAbort) and returns OSH_ERR_NCCL.
+osh_status wait_stream(osh_ctx* ctx, cudaStream_t stream);
 cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
 // NVLS helpers (nvls.cu)
 osh_status nvls_setup(osh_ctx* ctx, size_t grad_bytes, size_t replica_bytes, bool required);

@@ -222,6 +222,12 @@ class DistributedMuon:
     def sync(self) -> None:
         _lib.check(_lib.lib().osh_ctx_sync(self._ctx))
 
+    def set_timeout(self, seconds: float) -> None:
+        """Watchdog timeout of the ctx's host waits (osh_ctx_set_timeout): a
+        collective that does not complete in time aborts the communicators
+        and raises OshError (code 17) instead of hanging."""
+        _lib.check(_lib.lib().osh_ctx_set_timeout(self._ctx, float(seconds)))
+
     def timing(self) -> dict:
         t = _lib.StepTiming()
         _lib.check(_lib.lib().osh_last_timing(self._ctx, ctypes.byref(t)))

@@ -129,3 +129,10 @@ def test_tp2_checkpoint_restores_replica():
 def test_dp2_tp2_checkpoint_restores_replica():
     res = _run(4, "multi_gpu_check_tp.py", 2, 2, 2, "ckpt")
     assert res["checkpoint_replica_ok"] is True
+
+
+def test_dp2_watchdog_turns_dead_peer_into_error():
+    # a peer dies mid-run: the survivor's step returns OSH_ERR_NCCL within the
+    # timeout (communicators aborted) instead of hanging
+    res = _run(2, "watchdog_check.py")
+    assert res["status"] == 17 and res["next_step_status"] == 17
