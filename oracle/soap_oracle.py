@@ -44,6 +44,13 @@ rounding noise a QR of a singular matrix returns — this is what makes the
 basis a deterministic function of the inputs on both the fp64 oracle and
 the fp32 GPU path.
 
+Elongated blocks (one side more than twice the other, e.g. 333 x 96): the
+long side's statistics have rank <= the short side, so more than half of its
+eigenbasis would be an arbitrary basis of the null space — a function of
+rounding, not of the data. That side is not rotated (Q = I, order =
+identity, never refreshed): one-sided SOAP on the short side, the Adam
+second moment living in the half-rotated space.
+
 Vectors and vocabulary-space matrices: elementwise Adam with the same b1,
 b2, eps and bias correction (also skipped on the first call).
 """
@@ -85,12 +92,20 @@ def qr_pos(y: np.ndarray) -> np.ndarray:
     return q * d
 
 
-def refresh_basis(s: np.ndarray, q: np.ndarray, cfg: SoapConfig, iters: int
-                  ) -> Tuple[np.ndarray, np.ndarray]:
+def frozen(n: int, other: int) -> bool:
+    """The side of size n of an n x other block keeps Q = I (elongated block)."""
+    return n > 2 * other
+
+
+def refresh_basis(s: np.ndarray, q: np.ndarray, cfg: SoapConfig, iters: int,
+                  other: int = None) -> Tuple[np.ndarray, np.ndarray]:
     """One (or `iters`) shifted power-iteration steps; returns (Q, order of
-    the LAST step) — the permutation V must follow."""
+    the LAST step) — the permutation V must follow. A frozen side (`other` =
+    the block's other dimension) keeps its basis."""
     n = s.shape[0]
     order = np.arange(n)
+    if other is not None and frozen(n, other):
+        return q, order
     c = cfg.shift * float(np.linalg.norm(s))
     if c == 0.0:
         return q, order
@@ -141,8 +156,8 @@ def soap_apply(st: SoapTensorState, cfg: SoapConfig, w: np.ndarray, g: np.ndarra
             gs = g[r0:r0 + p, c0:c0 + q]
             st.L[k] = (1.0 - bs) * (gs @ gs.T)
             st.R[k] = (1.0 - bs) * (gs.T @ gs)
-            st.QL[k], _ = refresh_basis(st.L[k], st.QL[k], cfg, cfg.init_iters)
-            st.QR[k], _ = refresh_basis(st.R[k], st.QR[k], cfg, cfg.init_iters)
+            st.QL[k], _ = refresh_basis(st.L[k], st.QL[k], cfg, cfg.init_iters, q)
+            st.QR[k], _ = refresh_basis(st.R[k], st.QR[k], cfg, cfg.init_iters, p)
         return 0.0
     t = step
     bc1, bc2 = 1.0 - cfg.beta1 ** t, 1.0 - cfg.beta2 ** t
@@ -164,8 +179,8 @@ def soap_apply(st: SoapTensorState, cfg: SoapConfig, w: np.ndarray, g: np.ndarra
         st.L[k] = bs * st.L[k] + (1.0 - bs) * (gs @ gs.T)
         st.R[k] = bs * st.R[k] + (1.0 - bs) * (gs.T @ gs)
         if step % cfg.precond_every == 0:
-            st.QL[k], ol = refresh_basis(st.L[k], st.QL[k], cfg, 1)
-            st.QR[k], orr = refresh_basis(st.R[k], st.QR[k], cfg, 1)
+            st.QL[k], ol = refresh_basis(st.L[k], st.QL[k], cfg, 1, q)
+            st.QR[k], orr = refresh_basis(st.R[k], st.QR[k], cfg, 1, p)
             st.V[k] = st.V[k][ol, :][:, orr]
     w -= upd
     return float(np.linalg.norm(upd))

@@ -221,6 +221,10 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       k.Mp = off; off += pq4 * k.nb;
       k.l.n = k.p; k.l.ld = k.ldp;
       k.r.n = k.q; k.r.ld = k.ldq;
+      // elongated blocks: the long side's statistics have rank <= the short
+      // side, so its basis stays the identity (one-sided SOAP; soap_oracle.py)
+      k.l.frozen = k.p > 2 * k.q;
+      k.r.frozen = k.q > 2 * k.p;
       for (Side* sd : {&k.l, &k.r}) {  // refresh sub-batches
         sd->rb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(
                                       static_cast<size_t>(k.nb), rws_cap / refresh_ws(sd->n, sd->ld))));
@@ -533,6 +537,15 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_update_sq_), sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(cudaMemset(d_update_sq_, 0, sizeof(double) * std::max(n_tensors_, 1)));
   OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_order_), sizeof(int) * static_cast<size_t>(std::max(n_orders, 1))));
+  {  // identity orders: what a frozen side keeps (refreshed sides overwrite theirs)
+    std::vector<int> ident(static_cast<size_t>(std::max(n_orders, 1)), 0);
+    for (const Wave& w : waves_)
+      for (const Cls& k : w.cls)
+        for (const Side* sd : {&k.l, &k.r})
+          for (int i = 0; i < k.nb; ++i)
+            for (int j = 0; j < sd->n; ++j) ident[static_cast<size_t>(sd->order0 + sd->n * i + j)] = j;
+    OSH_CUDA_TRY(cudaMemcpy(d_order_, ident.data(), sizeof(int) * ident.size(), cudaMemcpyHostToDevice));
+  }
   {
     const std::vector<float> bs(static_cast<size_t>(max_nb_), static_cast<float>(1.0 - cfg_.beta2));
     OSH_CUDA_TRY(upload(&d_bscale_, bs));
@@ -653,7 +666,8 @@ osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
 osh_status SoapEngine::refresh(const Wave& w, int iters, bool permute_v, cudaStream_t s) {
   for (const Cls& k : w.cls)
     for (const Side* sd : {&k.l, &k.r})
-      if (osh_status st = refresh_side(*sd, iters, s); st != OSH_OK) return st;
+      if (!sd->frozen)
+        if (osh_status st = refresh_side(*sd, iters, s); st != OSH_OK) return st;
   if (permute_v && w.vperm.count > 0) {
     OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 5, 0.0, 0.0, s, [&] {
       return launch_soap_vperm(d_vperm_ + w.vperm.first, w.vperm.count, w.vperm.tiles, s);

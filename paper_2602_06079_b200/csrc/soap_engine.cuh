@@ -71,6 +71,7 @@ class SoapEngine : public OptimizerEngine {
   };
   struct Side {                    // one side (L or R) of a class: nb matrices of n x n
     int n = 0, ld = 0;
+    bool frozen = false;           // elongated block: this side keeps Q = I (soap_oracle.frozen)
     size_t S = 0, Q = 0;           // state: statistics [n][ld] fp32, basis column-major fp32
     int order0 = 0;                // first order entry (d_order_)
     int basis0 = 0;                // first soap_basis task

@@ -4,8 +4,9 @@ specification oracle/soap_oracle.py on the same inputs.
 Parity is UNPINNED against the reference (it has no SOAP mathematics, only
 its cost, cost.hpp:47-48,68-75); the oracle is this build's specification.
 Stated tolerances (bf16 G / M / Q / N' operands with fp32 accumulation, fp32
-statistics, second moment and basis; the basis refresh in fp32 cuBLAS /
-cuSOLVER CholeskyQR2):
+statistics, second moment and basis; the basis refresh by this library's
+bf16x6 tcgen05 products and its Cholesky kernel, CholeskyQR2; elongated
+blocks rotate only their short side, soap_oracle.frozen):
   TOL_DW  relative Frobenius error of the last step's update per tensor  <= 5e-2
           (and of the total change W_final - W_init)
   TOL_W   max elementwise error of the final weights                    <= lr

@@ -130,3 +130,17 @@ def test_bf16_rounding_matches_torch():
                         [0.0, -0.0, 1.0, 1.00390625, 1.01171875, -3.5]])
     ref = torch.from_numpy(x.astype(np.float32)).bfloat16().double().numpy()
     np.testing.assert_array_equal(S._bf16(x), ref)
+
+
+def test_elongated_block_rotates_only_its_short_side():
+    """A p x q block with p > 2q keeps Q_L = I (its statistics have rank <= q:
+    most of that basis would be rounding noise); Q_R is refreshed."""
+    cfg = S.SoapConfig(block=512, precond_every=1)
+    st = S.SoapTensorState((300, 60), cfg, True)
+    w = np.zeros((300, 60))
+    g = np.random.default_rng(3).standard_normal((300, 60))
+    for step in range(3):
+        S.soap_apply(st, cfg, w, g, step)
+    assert np.array_equal(st.QL[0], np.eye(300))
+    assert not np.allclose(st.QR[0], np.eye(60))
+    assert S.frozen(300, 60) and not S.frozen(60, 300) and not S.frozen(200, 100)
