@@ -1,61 +1,30 @@
 // Elementwise Muon kernels (see muon_kernels.cuh for the math and bytes).
 #include "muon_kernels.cuh"
 
-#include <algorithm>
-
 #include "elementwise_util.cuh"
-#include "status.hpp"
 
 namespace osh {
 namespace {
 
 using namespace ew;
 
-// Task of linear tile t: binary search for a CTA's first tile, then a
-// forward walk (a persistent CTA's tiles ascend by the grid size).
-template <typename Task>
-__device__ __forceinline__ int find_task(const Task* tasks, int n_tasks, long long t, int cur) {
-  if (cur < 0) {
-    int lo = 0, hi = n_tasks - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tasks[mid].tile_start <= t) lo = mid;
-      else hi = mid - 1;
-    }
-    return lo;
-  }
-  while (cur + 1 < n_tasks && tasks[cur + 1].tile_start <= t) ++cur;
-  return cur;
-}
-
-// One 64x64 tile of one matrix per iteration of a persistent CTA (grid-
-// stride over the wave's tiles); 256 threads = 8 rows x 32 columns per pass,
-// so every global access is a coalesced 128-byte (fp32) or 64-byte (bf16)
-// warp transaction. The per-tile sum of m^2 is one fixed-order block sum.
+// One 64x64 tile of one matrix per CTA; 256 threads = 8 rows x 32 columns
+// per pass, so every global access is a coalesced 128-byte (fp32) or
+// 64-byte (bf16) warp transaction.
 template <typename G>
-__device__ __forceinline__ void momentum_tile(const MomentumMatrixTask& T, long long local,
-                                              float beta, __nv_bfloat16 (*tile)[kTile + 2],
-                                              double* red);
-
-template <typename G>
-__global__ void __launch_bounds__(256) momentum_matrix_kernel(const MomentumMatrixTask* tasks,
-                                                              int n_tasks, long long total_tiles,
-                                                              float beta) {
+__global__ void __launch_bounds__(256, 4) momentum_matrix_kernel(const MomentumMatrixTask* tasks,
+                                                              int n_tasks, float beta) {
   __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
   __shared__ double red[8];
-  int cur = -1;
-  for (long long t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-    cur = find_task(tasks, n_tasks, t, cur);
-    const MomentumMatrixTask T = tasks[cur];
-    momentum_tile<G>(T, t - T.tile_start, beta, tile, red);
-    __syncthreads();  // tile / red are reused by the next tile
+  const long long t = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
   }
-}
-
-template <typename G>
-__device__ __forceinline__ void momentum_tile(const MomentumMatrixTask& T, long long local,
-                                              float beta, __nv_bfloat16 (*tile)[kTile + 2],
-                                              double* red) {
+  const MomentumMatrixTask T = tasks[lo];
+  const long long local = t - T.tile_start;
   const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
   const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -169,30 +138,23 @@ __device__ __forceinline__ void momentum_tile(const MomentumMatrixTask& T, long 
   if (threadIdx.x == 0) T.partial[local] = tile_sum;
 }
 
-__device__ __forceinline__ void apply_tile(ApplyTask T, long long local, float lrate,
-                                           __nv_bfloat16 (*tile)[kTile + 2], double* red);
-
-// W -= lr * X_k per 64x64 tile, persistent grid-stride like the momentum pass.
-// X values are bf16, so a bf16 staging tile is exact and keeps the CTA at
-// 8.5 KB of shared memory: small enough to co-reside with a persistent
-// Newton-Schulz GEMM CTA when the update of one wave overlaps the next.
 __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* tasks, int n_tasks,
-                                                          long long total_tiles, float lrate,
-                                                          int use_alt) {
+                                                          float lrate, int use_alt) {
+  // X values are bf16, so a bf16 staging tile is exact and keeps the CTA at
+  // 8.5 KB of shared memory: small enough to co-reside with a persistent
+  // Newton-Schulz GEMM CTA when the update of one wave overlaps the next
   __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
   __shared__ double red[8];
-  int cur = -1;
-  for (long long t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-    cur = find_task(tasks, n_tasks, t, cur);
-    ApplyTask T = tasks[cur];
-    if (use_alt) T.x = T.x_alt;
-    apply_tile(T, t - T.tile_start, lrate, tile, red);
-    __syncthreads();
+  const long long t = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
   }
-}
-
-__device__ __forceinline__ void apply_tile(ApplyTask T, long long local, float lrate,
-                                           __nv_bfloat16 (*tile)[kTile + 2], double* red) {
+  ApplyTask T = tasks[lo];
+  if (use_alt) T.x = T.x_alt;
+  const long long local = t - T.tile_start;
   const int r0 = static_cast<int>(local / T.tiles_c) * kTile;
   const int c0 = static_cast<int>(local % T.tiles_c) * kTile;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -402,23 +364,11 @@ cudaError_t launch_momentum_matrix(const MomentumMatrixTask* d_tasks, int n_task
                                    cudaStream_t s) {
   if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
   if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
-  // persistent: enough CTAs to fill every SM at full occupancy, each walking
-  // the wave's tiles with a grid stride
-  static thread_local int occ[2] = {0, 0};
-  const int k = grad_dtype == kGradBF16 ? 0 : 1;
-  if (occ[k] == 0) {
-    if (grad_dtype == kGradBF16)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[k], momentum_matrix_kernel<__nv_bfloat16>, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[k], momentum_matrix_kernel<float>, 256, 0);
-    if (occ[k] < 1) occ[k] = 1;
-  }
-  const long long cap = static_cast<long long>(device_sm_count()) * occ[k];
-  const dim3 grid(static_cast<unsigned>(std::min(total_tiles, cap)));
+  const dim3 grid(static_cast<unsigned>(total_tiles));
   if (grad_dtype == kGradBF16)
-    momentum_matrix_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(d_tasks, n_tasks, total_tiles, beta);
+    momentum_matrix_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
   else
-    momentum_matrix_kernel<float><<<grid, 256, 0, s>>>(d_tasks, n_tasks, total_tiles, beta);
+    momentum_matrix_kernel<float><<<grid, 256, 0, s>>>(d_tasks, n_tasks, beta);
   return cudaGetLastError();
 }
 
@@ -426,14 +376,8 @@ cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long
                                 float lr, int use_alt, cudaStream_t s) {
   if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
   if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
-  static thread_local int occ = 0;
-  if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_update_kernel, 256, 0);
-    if (occ < 1) occ = 1;
-  }
-  const long long cap = static_cast<long long>(device_sm_count()) * occ;
-  apply_update_kernel<<<static_cast<unsigned>(std::min(total_tiles, cap)), 256, 0, s>>>(
-      d_tasks, n_tasks, total_tiles, lr, use_alt);
+  apply_update_kernel<<<static_cast<unsigned>(total_tiles), 256, 0, s>>>(d_tasks, n_tasks, lr,
+                                                                          use_alt);
   return cudaGetLastError();
 }
 
