@@ -53,6 +53,7 @@ cudaError_t OptimizerEngine::timed_gemm(int mode, const NsProblemDesc* pd, int n
                 std::to_string(pd[q].b_mn_major ? pd[q].b.cols : pd[q].b.rows) + "x" +
                 std::to_string(pd[q].a.cols);
     }
+    if (sched != nullptr && sched->kb != nullptr && mode == kEpiGram) t.what += ":stream-k";
     cudaEventRecord(t.a, s);
   }
   const cudaError_t err = ns_gemm_launch(mode, pd, np, alpha, beta, lr, s, sched);

@@ -26,6 +26,7 @@ struct MuonTensorDesc {
   __nv_bfloat16* replica = nullptr;  // bf16 replica slot (nullable)
   int g_mc = 0;    // g is an NVLS multicast address (read the cross-GPU sum)
   int rep_mc = 0;  // replica is an NVLS multicast address (store to every GPU)
+  __nv_bfloat16* replica_local = nullptr;  // rep_mc: this GPU's own copy of the slot
 };
 
 struct NsLaunchStats {

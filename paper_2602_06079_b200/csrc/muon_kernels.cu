@@ -1,6 +1,8 @@
 // Elementwise Muon kernels (see muon_kernels.cuh for the math and bytes).
 #include "muon_kernels.cuh"
 
+#include <algorithm>
+
 #include "elementwise_util.cuh"
 
 namespace osh {
@@ -259,6 +261,22 @@ __global__ void __launch_bounds__(256) apply_update_kernel(const ApplyTask* task
   if (threadIdx.x == 0) T.partial[local] = tile_sum;
 }
 
+__global__ void __launch_bounds__(256) mc_copy_kernel(const McCopyTask* tasks, int n_tasks,
+                                                      long long total_vecs) {
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < total_vecs; v += 256ll * gridDim.x) {
+    int lo = 0, hi = n_tasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tasks[mid].vec_start <= v) lo = mid;
+      else hi = mid - 1;
+    }
+    const McCopyTask& T = tasks[lo];
+    const long long i = 8 * (v - T.vec_start);
+    mc_store16(T.dst + i, *reinterpret_cast<const uint4*>(T.src + i));
+  }
+  __threadfence_system();  // the multicast stores land before the step's end barrier
+}
+
 __global__ void __launch_bounds__(256) partial_sums_kernel(const double* partial,
                                                            const long long* begin,
                                                            const int* count, const int* target,
@@ -378,6 +396,14 @@ cudaError_t launch_apply_update(const ApplyTask* d_tasks, int n_tasks, long long
   if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
   apply_update_kernel<<<static_cast<unsigned>(total_tiles), 256, 0, s>>>(d_tasks, n_tasks, lr,
                                                                           use_alt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mc_copy(const McCopyTask* d_tasks, int n_tasks, long long total_vecs,
+                           cudaStream_t s) {
+  if (n_tasks == 0 || total_vecs == 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((total_vecs + 255) / 256, 148ll * 8);
+  mc_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_tasks, n_tasks, total_vecs);
   return cudaGetLastError();
 }
 

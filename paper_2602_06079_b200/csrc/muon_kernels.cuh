@@ -79,6 +79,17 @@ cudaError_t launch_partial_sums(const double* partial, const long long* begin, c
 
 // Strided 2-D copies of 16-bit blocks (TP gather / scatter staging):
 // dst[r*ldd + c] = src[r*lds + c], r < rows, c < cols, for every task.
+// NVLS AG-v of fused FINAL tensors: the owner's freshly written local bf16
+// slot is re-stored through the multicast address (every GPU's replica).
+struct McCopyTask {
+  const __nv_bfloat16* src;  // local replica slot
+  __nv_bfloat16* dst;        // multicast address of the same slot
+  long long n;               // elements (multiple of 8)
+  long long vec_start;       // first 8-element vector of this task (prefix sum)
+};
+cudaError_t launch_mc_copy(const McCopyTask* d_tasks, int n_tasks, long long total_vecs,
+                           cudaStream_t s);
+
 struct CopyTask {
   const uint16_t* src;
   uint16_t* dst;

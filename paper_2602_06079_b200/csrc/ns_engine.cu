@@ -57,9 +57,9 @@ MuonEngine::~MuonEngine() { release(); }
 
 const char* MuonEngine::elementwise_name(int mode) const {
   static const char* kNames[] = {"momentum_vector", "momentum_matrix", "ns_scales", "apply_update",
-                                 "partial_sums"};
+                                 "partial_sums", "mc_broadcast"};
   const int i = mode - kModeElementwise;
-  return i >= 0 && i < 5 ? kNames[i] : "elementwise";
+  return i >= 0 && i < 6 ? kNames[i] : "elementwise";
 }
 
 void MuonEngine::release() {
@@ -70,8 +70,11 @@ void MuonEngine::release() {
                   static_cast<void*>(d_mtasks_), static_cast<void*>(d_atasks_),
                   static_cast<void*>(d_vtasks_), static_cast<void*>(d_ftargets_),
                   static_cast<void*>(d_fpartial_), static_cast<void*>(d_fslot_begin_),
-                  static_cast<void*>(d_fslot_count_), static_cast<void*>(d_fslot_tensor_)})
+                  static_cast<void*>(d_fslot_count_), static_cast<void*>(d_fslot_tensor_),
+                  static_cast<void*>(d_sk_ws_), static_cast<void*>(d_mctasks_)})
     cudaFree(p);
+  d_sk_ws_ = nullptr;
+  d_mctasks_ = nullptr;
   d_ftargets_ = nullptr;
   d_fpartial_ = nullptr;
   fpartial_count_ = 0;
@@ -117,8 +120,9 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   if (min_waves > 1) cap = std::min(cap, (total_ws + min_waves - 1) / min_waves);
 
   // FINAL fusion is a property of the TENSOR (vector-addressable W and
-  // replica; an NVLS replica is written with multimem.st, fusing the AG-v into
-  // the epilogue), never of the wave it lands in, so results do not depend
+  // replica; with NVLS the epilogue writes this GPU's slot and run_post
+  // re-stores it through the multicast address), never of the wave it lands
+  // in, so results do not depend
   // on how the plan groups tensors (sharded == replicated bit for bit).
   const char* ff = std::getenv("OSH_FUSE_FINAL");
   fuse_final_ = !(ff != nullptr && std::strcmp(ff, "0") == 0);
@@ -127,7 +131,11 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     const MuonTensorDesc& t = tensors[i];
     if (!t.is_matrix || !fuse_final_) continue;
     const Shape s = shape_of(t.rows, t.cols);
-    fused_t[i] = final_target_ok(t.w, t.replica, s.m, s.n, t.rows > t.cols ? 1 : 0) ? 1 : 0;
+    const __nv_bfloat16* rep = t.rep_mc ? t.replica_local : t.replica;
+    fused_t[i] = (!t.rep_mc || t.replica_local != nullptr) &&
+                         final_target_ok(t.w, rep, s.m, s.n, t.rows > t.cols ? 1 : 0)
+                     ? 1
+                     : 0;
   }
   // chunk key: (m, n), n negated for fused tensors (a class splits by fusion)
   const auto key_of = [&](int i) {
@@ -188,6 +196,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     size_t poff;
   };
   std::vector<FTarget> ftargets;
+  std::vector<McCopyTask> mctasks;
   std::vector<long long> fslot_begin;
   std::vector<int> fslot_count, fslot_tensor;
 
@@ -236,6 +245,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     std::stable_partition(order.begin(), order.end(), [](const std::pair<int, int>& k) { return k.second > 0; });
     size_t off = double_buffer_ && (wi & 1) ? half : 0;
     w.fslot0 = static_cast<int>(fslot_begin.size());
+    w.mc0 = static_cast<int>(mctasks.size());
     for (const auto& cls : order) {
       const bool cfused = cls.second < 0;
       if (!cfused) ++w.nf_chunks;
@@ -275,6 +285,12 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
           ns_gemm_set_cta_group(cg0);
           const int cnt = std::max(p1, p2);
           ftargets.push_back({ti, s.m, s.n, fpartial_count_});
+          if (t.rep_mc) {  // NVLS: re-store the local slot through the multicast address
+            const long long n = static_cast<long long>(t.rows) * t.cols;
+            mctasks.push_back({t.replica_local, t.replica, n, w.mc_vecs});
+            w.mc_vecs += n / 8;
+            ++w.n_mc;
+          }
           fslot_begin.push_back(static_cast<long long>(fpartial_count_));
           fslot_count.push_back(cnt);
           fslot_tensor.push_back(ti);
@@ -371,11 +387,15 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     std::vector<NsFinalTarget> ft(ftargets.size());
     for (size_t i = 0; i < ftargets.size(); ++i) {
       const MuonTensorDesc& t = tensors[ftargets[i].ti];
-      if (!make_final_target(&ft[i], t.w, t.replica, ftargets[i].m, ftargets[i].n,
-                             t.rows > t.cols ? 1 : 0, d_fpartial_ + ftargets[i].poff, t.rep_mc))
+      // NVLS: FINAL writes this GPU's own slot; run_post re-stores it through
+      // the multicast address (multimem.st from the epilogue stalls the MMAs)
+      __nv_bfloat16* rep = t.rep_mc ? t.replica_local : t.replica;
+      if (!make_final_target(&ft[i], t.w, rep, ftargets[i].m, ftargets[i].n,
+                             t.rows > t.cols ? 1 : 0, d_fpartial_ + ftargets[i].poff))
         return fail(OSH_ERR_CUDA, "MuonEngine: cannot encode the FINAL TMA maps");
     }
     OSH_CUDA_TRY(upload(&d_ftargets_, ft));
+    OSH_CUDA_TRY(upload(&d_mctasks_, mctasks));
     OSH_CUDA_TRY(upload(&d_fslot_begin_, fslot_begin));
     OSH_CUDA_TRY(upload(&d_fslot_count_, fslot_count));
     OSH_CUDA_TRY(upload(&d_fslot_tensor_, fslot_tensor));
@@ -385,13 +405,49 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   fold_a_ = !(aux != nullptr && std::strcmp(aux, "1") == 0);
   const char* lpt = std::getenv("OSH_GEMM_LPT");
   lpt_ = !(lpt != nullptr && std::strcmp(lpt, "0") == 0);
+  const char* skv = std::getenv("OSH_STREAM_K");
+  stream_k_ = !(skv != nullptr && std::strcmp(skv, "0") == 0);
+  int sk_slots = 0;  // partial slots of the largest stream-K GRAM
   sched_symmetric_ = symmetric_;
   for (Wave& w : waves_) {
     if (w.n_tasks == 0 || !lpt_) continue;
     NsProblemDesc pd[3][kMaxProblems];
     problems(w, 0, pd[0], pd[1], pd[2]);
     const int modes[3] = {kEpiGram, kEpiPoly, kEpiUpdate};
+    if (stream_k_) {  // GRAM of few long-K tiles (vocabulary matrices): stream-K
+      std::vector<int> tl, off, slot, fix;
+      std::vector<int2> kb;
+      int total = 0, n_slots = 0;
+      const int units = ns_gemm_stream_k_schedule(pd[0], static_cast<int>(w.chunks.size()), &tl, &off,
+                                                  &kb, &slot, &fix, &n_slots, &total);
+      if (units > 0) {
+        NsSchedule& sc = w.sched[kEpiGram];
+        int* d_tl = nullptr;
+        int* d_off = nullptr;
+        int* d_slot = nullptr;
+        int* d_fix = nullptr;
+        int2* d_kb = nullptr;
+        OSH_CUDA_TRY(upload(&d_tl, tl));
+        OSH_CUDA_TRY(upload(&d_off, off));
+        OSH_CUDA_TRY(upload(&d_slot, slot));
+        OSH_CUDA_TRY(upload(&d_fix, fix));
+        OSH_CUDA_TRY(upload(&d_kb, kb));
+        for (int* p : {d_tl, d_off, d_slot, d_fix}) sched_mem_.push_back(p);
+        sched_mem_.push_back(reinterpret_cast<int*>(d_kb));
+        sc.tiles = d_tl;
+        sc.off = d_off;
+        sc.units = units;
+        sc.total_tiles = total;
+        sc.kb = d_kb;
+        sc.slot = d_slot;
+        sc.fix = d_fix;
+        sc.n_fix = static_cast<int>(fix.size() / 6);
+        sc.n_slots = n_slots;
+        sk_slots = std::max(sk_slots, n_slots);
+      }
+    }
     for (int m = 0; m < 3; ++m) {
+      if (m == 0 && w.sched[kEpiGram].kb != nullptr) continue;  // stream-K above
       std::vector<int> tl, off;
       int total = 0;
       const int units = ns_gemm_schedule(modes[m], pd[m], static_cast<int>(w.chunks.size()), &tl, &off, &total);
@@ -435,6 +491,12 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       sc.units = units;
       sc.total_tiles = total;
     }
+  }
+  if (sk_slots > 0) {  // one fp32 partial workspace, reused by every wave's stream-K GRAM
+    OSH_CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&d_sk_ws_),
+                           sizeof(float) * static_cast<size_t>(sk_slots) * 256 * kNsBN));
+    for (Wave& w : waves_)
+      if (w.sched[kEpiGram].kb != nullptr) w.sched[kEpiGram].ws = d_sk_ws_;
   }
   OSH_CUDA_TRY(cudaDeviceSynchronize());
   return OSH_OK;
@@ -554,8 +616,13 @@ osh_status MuonEngine::run_post(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
   const auto timed = [&](int mode, double bytes, auto&& launch) {
     return timed_elementwise(mode, bytes, elems, s, launch);
   };
-  // fused tensors: W and the replica were written by FINAL; their norms are
-  // the FINAL epilogue partials
+  // fused tensors: W and the replica were written by FINAL (NVLS: this GPU's
+  // slot, now spread to every GPU through the multicast address — the AG-v);
+  // their norms are the FINAL epilogue partials
+  if (w.n_mc > 0)
+    OSH_CUDA_TRY(timed(kModeElementwise + 5, 2.0 * static_cast<double>(w.mc_vecs) * 8, [&] {
+      return launch_mc_copy(d_mctasks_ + w.mc0, w.n_mc, w.mc_vecs, s);
+    }));
   if (w.nf_slots < w.n_slots)
     OSH_CUDA_TRY(timed(kModeElementwise + 4, 0.0, [&] {
       return launch_partial_sums(d_fpartial_, d_fslot_begin_ + w.fslot0, d_fslot_count_ + w.fslot0,

@@ -92,6 +92,8 @@ class MuonEngine : public OptimizerEngine {
     long long nf_tiles = 0;
     double nf_elems = 0.0;
     int fslot0 = 0;                  // first row of the fused partial-sum tables
+    int mc0 = 0, n_mc = 0;           // NVLS: multicast re-store tasks of fused tensors
+    long long mc_vecs = 0;
     NsSchedule sched_last_update;    // last iteration: UPDATE over the unfused prefix
   };
   void release();
@@ -118,12 +120,15 @@ class MuonEngine : public OptimizerEngine {
   MomentumVectorTask* d_vtasks_ = nullptr;
   // fused FINAL: per matrix slot a TMA target + its epilogue partials
   NsFinalTarget* d_ftargets_ = nullptr;
+  McCopyTask* d_mctasks_ = nullptr;
   double* d_fpartial_ = nullptr;
   size_t fpartial_count_ = 0;
   long long* d_fslot_begin_ = nullptr;
   int* d_fslot_count_ = nullptr;
   int* d_fslot_tensor_ = nullptr;
   bool fuse_final_ = true;        // OSH_FUSE_FINAL=0: UPDATE + apply_update everywhere
+  bool stream_k_ = true;          // OSH_STREAM_K=0: whole-tile LPT schedules for every GRAM
+  float* d_sk_ws_ = nullptr;      // stream-K partial tiles (fp32, 256 x 256 per slot)
   bool symmetric_ = true;
   bool double_buffer_ = false;
   bool reorder_ = false;          // small waves first and last (set_wave_reorder)

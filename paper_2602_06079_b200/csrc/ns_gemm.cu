@@ -7,7 +7,6 @@
 // The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
 // tile i+1. Tiles of all problems are linearised and strided over the grid.
 #include "ns_gemm.cuh"
-#include "elementwise_util.cuh"
 #include "sm100.cuh"
 #include "status.hpp"
 
@@ -394,9 +393,7 @@ __device__ __forceinline__ void final_epilogue(const NsGemmParams& P, int it_beg
             h.y = pack_bf16(a.z, a.w);
             h.z = pack_bf16(b.x, b.y);
             h.w = pack_bf16(b.z, b.w);
-            __nv_bfloat16* rd = rep + static_cast<long long>(grow0 + rr) * ld + gc;
-            if (ft.rep_mc) ew::mc_store16(rd, h);  // AG-v fused: the switch writes every GPU
-            else st_global_v4_evict_first(rd, h, pol);
+            st_global_v4_evict_first(rep + static_cast<long long>(grow0 + rr) * ld + gc, h, pol);
           }
         }
       }
@@ -416,7 +413,6 @@ __device__ __forceinline__ void final_epilogue(const NsGemmParams& P, int it_beg
     acc ^= 1;
     if (acc == 0) acc_phase ^= 1;
   }
-  __threadfence_system();  // multicast replica stores are visible before the step's end barrier
 }
 
 template <int MODE, int CG>
@@ -485,10 +481,15 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         const int t = sched ? __ldg(P.sched + it) : it;
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
-        const int nkb = (pr.K + kNsBK - 1) / kNsBK;
+        int kb0 = 0, kb1 = (pr.K + kNsBK - 1) / kNsBK;
+        if (sched && P.seg_kb != nullptr) {
+          const int2 r = __ldg(P.seg_kb + it);
+          kb0 = r.x;
+          kb1 = r.y;
+        }
         const int a_row = c.tm * C::kTileM + rank * C::kRowsA;
         const int b_row = c.tn * kNsBN + rank * C::kRowsB;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // the leader's full barrier counts the bytes of both CTAs of the pair
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
@@ -518,12 +519,17 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         const int t = sched ? __ldg(P.sched + it) : it;
         const TileCoord c = decode_tile(P, t);
         const NsGemmProblem& pr = P.prob[c.p];
-        const int nkb = (pr.K + kNsBK - 1) / kNsBK;
+        int kb0 = 0, kb1 = (pr.K + kNsBK - 1) / kNsBK;
+        if (sched && P.seg_kb != nullptr) {
+          const int2 r = __ldg(P.seg_kb + it);
+          kb0 = r.x;
+          kb1 = r.y;
+        }
         const bool mn = pr.b_mn_major != 0;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kNsBN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
@@ -534,9 +540,9 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             const uint64_t bdesc = mn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
                                       : smem_desc_sw128(b0 + k * 32, 16, 1024);
             if constexpr (CG == 2)
-              umma_bf16_cg2(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
+              umma_bf16_cg2(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
             else
-              umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb | k) != 0);
+              umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
           }
           if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
           else umma_commit(&empty_bar[stage]);
@@ -570,11 +576,23 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kNsBN;
+      // stream-K part of a tile: the raw accumulator to its partial slot
+      const int slot = (MODE == kEpiGram && sched && P.seg_slot != nullptr) ? __ldg(P.seg_slot + it) : -1;
 #pragma unroll 1
       for (int chunk = 0; chunk < kNsBN / 32; ++chunk) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + chunk * 32, r);
         tmem_ld_wait();
+        if (slot >= 0) {
+          float4* d = reinterpret_cast<float4*>(
+              P.seg_ws + (static_cast<size_t>(slot) * 256 + rank * C::kRowsA + row_in_tile) * kNsBN +
+              chunk * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            d[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          continue;
+        }
         const int col0 = c.tn * kNsBN + chunk * 32;
         if (col0 >= pr.N) continue;  // warp-uniform
         if (!row_ok) continue;
@@ -660,6 +678,44 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, kTmemCols);
     else tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// Stream-K fixup: every tile that was cut across units is the fixed-order
+// sum of its parts' partial slots, finished with the GRAM epilogue (scale,
+// bf16, symmetric mirror). blockIdx.x = split tile, blockIdx.y = 8-row band;
+// a thread sums 8 consecutive columns of one row.
+__global__ void __launch_bounds__(256) stream_k_fixup_kernel(const __grid_constant__ NsGemmParams P,
+                                                             const int* fix) {
+  const int* f = fix + 6 * blockIdx.x;
+  const NsGemmProblem& pr = P.prob[f[0]];
+  const int b = f[1], tm = f[2], tn = f[3], slot0 = f[4], ns = f[5];
+  const int lr = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int lc = (threadIdx.x & 31) * 8;
+  if (lr >= P.tile_m) return;
+  const int row = tm * P.tile_m + lr, col0 = tn * kNsBN + lc;
+  if (row >= pr.M || col0 >= pr.N) return;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < ns; ++k) {  // parts in k-block order
+    const float4* src = reinterpret_cast<const float4*>(
+        P.seg_ws + (static_cast<size_t>(slot0 + k) * 256 + lr) * kNsBN + lc);
+    const float4 x = src[0], y = src[1];
+    acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+    acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+  }
+  const float sc = pr.scale != nullptr ? __ldg(pr.scale + b) : 1.f;
+  __nv_bfloat16* out = pr.out + b * pr.out_bstride;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int col = col0 + j;
+    if (col >= pr.N) break;
+    const __nv_bfloat16 v = __float2bfloat16_rn(sc * acc[j]);
+    if (!pr.symmetric) {
+      out[row * pr.out_ld + col] = v;
+    } else {
+      if (col >= row) out[row * pr.out_ld + col] = v;
+      if (col > row) out[static_cast<long long>(col) * pr.out_ld + row] = v;
+    }
   }
 }
 
@@ -759,14 +815,13 @@ bool final_target_ok(const void* w, const void* replica, int M, int N, int trans
 }
 
 bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
-                       int transposed, double* partial, int rep_mc) {
+                       int transposed, double* partial) {
   std::memset(t, 0, sizeof(*t));
   if (!final_target_ok(w, replica, M, N, transposed) || partial == nullptr) return false;
   t->w = w;
   t->replica = replica;
   t->partial = partial;
   t->transposed = transposed;
-  t->rep_mc = replica != nullptr && rep_mc ? 1 : 0;
   return true;
 }
 
@@ -847,6 +902,152 @@ int ns_gemm_schedule(int mode, const NsProblemDesc* probs, int num_problems,
   return units;
 }
 
+int ns_gemm_stream_k_schedule(const NsProblemDesc* probs, int num_problems,
+                              std::vector<int>* tiles_out, std::vector<int>* off_out,
+                              std::vector<int2>* kb_out, std::vector<int>* slot_out,
+                              std::vector<int>* fix_out, int* n_slots, int* total_out) {
+  if (num_problems < 1 || num_problems > kMaxProblems) return 0;
+  const int cg = cta_group();
+  const int tile_m = 128 * cg;
+  // linear tiles (the kernel's decode order: problem, batch, tile) and their k-blocks
+  struct T {
+    int p, b, tm, tn, nkb;
+  };
+  std::vector<T> ts;
+  for (int i = 0; i < num_problems; ++i) {
+    const NsProblemDesc& d = probs[i];
+    const int M = d.a.rows, K = d.a.cols, N = d.b_mn_major ? d.b.cols : d.b.rows;
+    const bool sym = d.symmetric && M == N;
+    const int tmn = (M + tile_m - 1) / tile_m, tnn = (N + kNsBN - 1) / kNsBN;
+    const int nkb = (K + kNsBK - 1) / kNsBK;
+    for (int b = 0; b < d.a.batch; ++b) {
+      if (sym) {  // column-major over the upper-triangle tiles (decode_tile)
+        for (int tn = 0; tn < tnn; ++tn)
+          for (int tm = 0; tm < std::min(tmn, (kNsBN * tn + kNsBN - 1) / tile_m + 1); ++tm)
+            ts.push_back({i, b, tm, tn, nkb});
+      } else {  // grouped rasterisation (decode_tile)
+        for (int rem = 0; rem < tmn * tnn; ++rem) {
+          const int span = kRasterGroup * tnn, group = rem / span, first_m = group * kRasterGroup;
+          const int gsz = std::min(tmn - first_m, kRasterGroup), r2 = rem - group * span;
+          ts.push_back({i, b, first_m + r2 % gsz, r2 / gsz, nkb});
+        }
+      }
+    }
+  }
+  const int n_tiles = static_cast<int>(ts.size());
+  const int units_max = cg == 2 ? sm_count() / 2 : sm_count();
+  const int U = std::min(n_tiles, units_max);
+  if (U < 2) return 0;
+  // Segments are cut PER MATRIX, as if the matrix ran alone on the GPU: its
+  // k-blocks (tile after tile) in units_max equal ranges. The cut points, and
+  // so the fixed-order sums of the parts, depend only on the matrix's own
+  // shape — never on what shares the launch — so a tensor's result does not
+  // depend on the plan (sharded == replicated bit for bit).
+  struct Seg {
+    int tile;
+    int2 kb;
+    long long cost;
+  };
+  std::vector<Seg> segs;
+  std::vector<int> n_parts(static_cast<size_t>(n_tiles), 0);
+  bool any = false;
+  for (size_t first = 0; first < ts.size();) {
+    size_t last = first;  // tiles of one matrix (problem, batch) are contiguous
+    while (last < ts.size() && ts[last].p == ts[first].p && ts[last].b == ts[first].b) ++last;
+    const int mt = static_cast<int>(last - first), nkb = ts[first].nkb;
+    const long long rounds = (mt + units_max - 1) / units_max;
+    const bool split = nkb >= 256 && mt > units_max && rounds <= 4 && mt % units_max != 0;
+    if (!split) {
+      for (size_t i = first; i < last; ++i) segs.push_back({static_cast<int>(i), make_int2(0, nkb), nkb + 2});
+    } else {
+      any = true;
+      const long long W = static_cast<long long>(mt) * nkb;
+      for (int u = 0; u < units_max; ++u) {
+        long long pos = W * u / units_max;
+        const long long e = W * (u + 1) / units_max;
+        while (pos < e) {
+          const int local = static_cast<int>(pos / nkb);
+          const long long stop = std::min(e, static_cast<long long>(local + 1) * nkb);
+          const int2 r = make_int2(static_cast<int>(pos - static_cast<long long>(local) * nkb),
+                                   static_cast<int>(stop - static_cast<long long>(local) * nkb));
+          segs.push_back({static_cast<int>(first) + local, r, (stop - pos) + 2});
+          pos = stop;
+        }
+      }
+    }
+    first = last;
+  }
+  if (!any) return 0;
+  for (const Seg& g : segs) ++n_parts[static_cast<size_t>(g.tile)];
+  // units: a launch holding one split matrix only takes its segments unit by
+  // unit (perfect balance); mixed launches balance all segments by LPT
+  std::vector<std::vector<int>> lists(static_cast<size_t>(U));
+  if (segs.size() >= static_cast<size_t>(units_max) && U == units_max &&
+      std::all_of(ts.begin(), ts.end(), [&](const T& t) { return t.p == ts[0].p && t.b == ts[0].b; })) {
+    // rebuild the per-unit split of the single matrix
+    const long long W = static_cast<long long>(n_tiles) * ts[0].nkb;
+    size_t k = 0;
+    for (int u = 0; u < U; ++u) {
+      const long long e = W * (u + 1) / U;
+      while (k < segs.size() &&
+             static_cast<long long>(segs[k].tile) * ts[0].nkb + segs[k].kb.x < e)
+        lists[static_cast<size_t>(u)].push_back(static_cast<int>(k++));
+    }
+  } else {
+    std::vector<size_t> order(segs.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t x, size_t y) { return segs[x].cost > segs[y].cost; });
+    std::vector<long long> load(static_cast<size_t>(U), 0);
+    for (const size_t i : order) {
+      int u = 0;
+      for (int v = 1; v < U; ++v)
+        if (load[static_cast<size_t>(v)] < load[static_cast<size_t>(u)]) u = v;
+      load[static_cast<size_t>(u)] += segs[i].cost;
+      lists[static_cast<size_t>(u)].push_back(static_cast<int>(i));
+    }
+  }
+  tiles_out->clear();
+  kb_out->clear();
+  slot_out->clear();
+  fix_out->clear();
+  off_out->assign(1, 0);
+  for (const auto& l : lists) {
+    for (const int i : l) {
+      tiles_out->push_back(segs[static_cast<size_t>(i)].tile);
+      kb_out->push_back(segs[static_cast<size_t>(i)].kb);
+      slot_out->push_back(-1);
+    }
+    off_out->push_back(static_cast<int>(tiles_out->size()));
+  }
+  std::vector<std::vector<int2>> pieces(static_cast<size_t>(n_tiles));  // parts of split tiles
+  for (const Seg& g : segs)
+    if (n_parts[static_cast<size_t>(g.tile)] > 1) pieces[static_cast<size_t>(g.tile)].push_back(g.kb);
+  // slots for the parts of split tiles, in k order; fixup entries
+  int slots = 0;
+  std::vector<int> first_slot(static_cast<size_t>(n_tiles), -1);
+  for (int i = 0; i < n_tiles; ++i) {
+    if (pieces[static_cast<size_t>(i)].size() < 2) continue;
+    first_slot[static_cast<size_t>(i)] = slots;
+    const T& d = ts[static_cast<size_t>(i)];
+    fix_out->insert(fix_out->end(), {d.p, d.b, d.tm, d.tn, slots,
+                                     static_cast<int>(pieces[static_cast<size_t>(i)].size())});
+    slots += static_cast<int>(pieces[static_cast<size_t>(i)].size());
+  }
+  // a part's slot = its rank in k order among its tile's parts (fixup order)
+  for (size_t k = 0; k < tiles_out->size(); ++k) {
+    const int ti = (*tiles_out)[k];
+    if (first_slot[static_cast<size_t>(ti)] < 0) continue;
+    int rank = 0;
+    for (const int2& pc : pieces[static_cast<size_t>(ti)])
+      if (pc.x < (*kb_out)[k].x) ++rank;
+    (*slot_out)[k] = first_slot[static_cast<size_t>(ti)] + rank;
+  }
+  *n_slots = slots;
+  *total_out = n_tiles;
+  return U;
+}
+
 cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problems, float alpha,
                            float beta, float lr, cudaStream_t stream, const NsSchedule* sched) {
   if (num_problems < 1 || num_problems > kMaxProblems) return cudaErrorInvalidValue;
@@ -911,11 +1112,24 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     if (mode == kEpiSplit && d.out_seg < pr.N) return cudaErrorInvalidValue;
   }
   P.total_tiles = tiles;
+  bool stream_k = false;
   if (sched != nullptr && sched->tiles != nullptr && sched->total_tiles == tiles &&
       sched->units == std::min(tiles, cg == 2 ? sm_count() / 2 : sm_count())) {
     P.sched = sched->tiles;
     P.sched_off = sched->off;
     P.sched_units = sched->units;
+    if (sched->kb != nullptr && mode == kEpiGram) {
+      P.seg_kb = sched->kb;
+      P.seg_slot = sched->slot;
+      P.seg_ws = sched->ws;
+      stream_k = sched->n_fix > 0;
+    }
+  }
+  if (stream_k) {
+    const cudaError_t e = cg == 2 ? launch_mode<kEpiGram, 2>(P, stream) : launch_mode<kEpiGram, 1>(P, stream);
+    if (e != cudaSuccess) return e;
+    stream_k_fixup_kernel<<<dim3(static_cast<unsigned>(sched->n_fix), 32), 256, 0, stream>>>(P, sched->fix);
+    return cudaGetLastError();
   }
   if (cg == 2) {
     switch (mode) {

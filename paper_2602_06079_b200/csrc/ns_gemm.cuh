@@ -54,7 +54,7 @@ struct NsFinalTarget {
   __nv_bfloat16* replica;  // bf16 replica, same geometry (nullable)
   double* partial;         // per (tile, CTA of the pair, epilogue warp): sum of (lr*update)^2
   int transposed;          // 1: the tensor is X^T (rows > cols in the reference)
-  int rep_mc;              // replica is an NVLS multicast address: multimem.st to every GPU
+  int pad_;
 };
 
 // One target for an M x N iterate (M <= N). W and the replica must be
@@ -62,7 +62,7 @@ struct NsFinalTarget {
 // (final_target_ok). `partial` needs final_partials(M, N) doubles.
 bool final_target_ok(const void* w, const void* replica, int M, int N, int transposed);
 bool make_final_target(NsFinalTarget* t, float* w, __nv_bfloat16* replica, int M, int N,
-                       int transposed, double* partial, int rep_mc = 0);
+                       int transposed, double* partial);
 int final_partials(int M, int N);  // tiles * CTAs per tile * 4 epilogue warps
 
 struct alignas(64) NsGemmProblem {
@@ -92,6 +92,13 @@ struct NsGemmParams {
   const int* sched;      // optional: tiles of unit u are sched[sched_off[u] .. sched_off[u+1])
   const int* sched_off;
   int sched_units;       // units (clusters / CTAs) the schedule was built for
+  // stream-K (kEpiGram only, with a schedule): entry i covers k-blocks
+  // [seg_kb[i].x, seg_kb[i].y) of its tile; seg_slot[i] >= 0 means a PART of
+  // the tile, whose raw fp32 accumulator goes to seg_ws slot seg_slot[i]
+  // ([256 rows][256 cols] per slot) for the fixup pass to sum in slot order
+  const int2* seg_kb;
+  const int* seg_slot;
+  float* seg_ws;
   int tile_m;  // output rows per tile: 128 (cta_group::1) or 256 (cta_group::2)
   float alpha, beta, lr;
 };
@@ -117,11 +124,21 @@ struct NsProblemDesc {
 };
 
 // A cost-balanced static tile schedule for one grouped launch (device arrays).
+// Stream-K schedules (kEpiGram) also carry per-entry k-block ranges and
+// partial slots, the fixup table of the split tiles (6 ints each: problem,
+// batch, tile row, tile col, first slot, slot count) and the fp32 partial
+// workspace (n_slots x 256 x 256).
 struct NsSchedule {
   const int* tiles = nullptr;
   const int* off = nullptr;
   int units = 0;
   int total_tiles = 0;
+  const int2* kb = nullptr;
+  const int* slot = nullptr;
+  const int* fix = nullptr;
+  int n_fix = 0;
+  int n_slots = 0;
+  float* ws = nullptr;
 };
 
 // Launches one grouped GEMM. Returns a cudaError_t (cudaSuccess on success).
@@ -137,6 +154,17 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
 // a tail. Fills per-unit tile lists; returns the unit count (0 on error).
 int ns_gemm_schedule(int mode, const NsProblemDesc* probs, int num_problems,
                      std::vector<int>* tiles, std::vector<int>* off, int* total_tiles);
+
+// Stream-K schedule of a GRAM launch with few, long-K tiles: the launch's
+// k-blocks (tile by tile, in linear tile order) are cut into one contiguous
+// range per unit, so every unit gets the same MMA work and no tile round is
+// left half empty. Tiles cut across units are finished by a fixup pass that
+// sums their parts in a fixed order (deterministic). Returns the unit count,
+// or 0 when stream-K would not shorten the launch (enough tiles already).
+int ns_gemm_stream_k_schedule(const NsProblemDesc* probs, int num_problems,
+                              std::vector<int>* tiles, std::vector<int>* off,
+                              std::vector<int2>* kb, std::vector<int>* slot,
+                              std::vector<int>* fix, int* n_slots, int* total_tiles);
 
 // UMMA CTA group used by subsequent launches: 2 (default; CTA pairs, 256x256
 // tiles) or 1 (single-CTA 128x256 tiles). OSH_GEMM_CTA_GROUP=1 overrides.

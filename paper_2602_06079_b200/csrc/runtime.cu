@@ -297,6 +297,8 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
     OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->tp_stream, cudaStreamNonBlocking));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_start_ev, cudaEventDisableTiming));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_done_ev, cudaEventDisableTiming));
+    OSH_CUDA_TRY(cudaEventCreate(&ctx->tp_begin_ev));
+    OSH_CUDA_TRY(cudaEventCreate(&ctx->tp_end_ev));
   }
   *out = ctx.release();
   return OSH_OK;
@@ -388,6 +390,8 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
     cudaStreamDestroy(ctx->tp_stream);
     cudaEventDestroy(ctx->tp_start_ev);
     cudaEventDestroy(ctx->tp_done_ev);
+    cudaEventDestroy(ctx->tp_begin_ev);
+    cudaEventDestroy(ctx->tp_end_ev);
   }
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->compute);
@@ -608,6 +612,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     if (ctx->nvls) {
       t.replica = ctx->mc_replica + ctx->flat_off[p];  // multimem.st to every rank (AG-v fused)
       t.rep_mc = 1;
+      t.replica_local = ctx->replica + ctx->flat_off[p];
     }
     ctx->engine_index[p] = static_cast<int>(tensors.size());
     tensors.push_back(t);
@@ -1126,6 +1131,16 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     return d2h_buckets(ctx, io, b, ctx->ag_ev[b]);
   };
   int ag_next = 0;
+  if (ctx->tp_size > 1) {
+    // micro-group gathers need every reduced shard of the TP plane: they go
+    // out on the TP stream once the whole reduce-scatter (or H2D) landed,
+    // overlapping the DP waves below
+    std::vector<cudaEvent_t> ready;
+    if (dist) ready = ctx->rs_ev;
+    else if (io.h2d) ready = ctx->h2d_ev;
+    ready.push_back(ctx->ev[0]);
+    if (osh_status st = osh::tp_gather(ctx, ready); st != OSH_OK) return st;
+  }
   if (!dist && ctx->tp_size == 1) {
     if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
   } else {
@@ -1150,11 +1165,9 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     }
   }
   if (ctx->tp_size > 1) {
-    // micro groups need every reduced shard of the TP plane: wait for the
-    // whole reduce-scatter, then gather / compute / scatter group by group
-    if (dist)
-      for (int b = 0; b < nb; ++b) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
-    if (osh_status st = osh::tp_step(ctx, *cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
+    if (osh_status st = osh::tp_compute(ctx, *cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
   if (dist) {
@@ -1183,6 +1196,11 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   ctx->last_timing.gemm_launches = s.launches_gemm;
   ctx->last_timing.elementwise_launches = s.launches_elementwise;
   ctx->last_timing.gemm_flops = s.gemm_flops;
+  for (const auto& e : ctx->tp_engines) {  // the micro-group engines are part of the step
+    ctx->last_timing.gemm_launches += e->stats().launches_gemm;
+    ctx->last_timing.elementwise_launches += e->stats().launches_elementwise;
+    ctx->last_timing.gemm_flops += e->stats().gemm_flops;
+  }
   if (host_replica_out != nullptr) return osh::wait_stream(ctx, cs);
   return OSH_OK;
 }
@@ -1243,6 +1261,7 @@ osh_status osh_ctx_stream(osh_ctx* ctx, void** stream) {
 osh_status osh_ctx_profile_gemm(osh_ctx* ctx, int32_t enable) {
   if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
   ctx->engine->set_profile(enable != 0);
+  for (auto& e : ctx->tp_engines) e->set_profile(enable != 0);  // TP micro-group engines too
   return OSH_OK;
 }
 
@@ -1253,13 +1272,23 @@ osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t re
   int n = 0;
   ctx->engine->read_profile(&n, &out->flops, &out->exec_flops, &out->ms, reset != 0);
   out->launches = n;
+  for (auto& e : ctx->tp_engines) {  // the micro-group engines' GEMMs are part of the step
+    int k = 0;
+    double f = 0.0, x = 0.0, ms = 0.0;
+    e->read_profile(&k, &f, &x, &ms, reset != 0);
+    out->launches += k;
+    out->flops += f;
+    out->exec_flops += x;
+    out->ms += ms;
+  }
   return OSH_OK;
 }
 
 osh_status osh_gemm_profile_dump(osh_ctx* ctx, char* buf, size_t cap, size_t* len) {
   if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
   if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
-  const std::string s = ctx->engine->profile_text();
+  std::string s = ctx->engine->profile_text();
+  for (auto& e : ctx->tp_engines) s += e->profile_text();
   if (len != nullptr) *len = s.size();
   if (buf != nullptr && cap > 0) {
     const size_t n = std::min(s.size(), cap - 1);
@@ -1292,6 +1321,8 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
   else
     for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
       t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
+  if (ctx->tp_size > 1 && ctx->tp_begin_ev != nullptr)  // + the micro groups (gathers overlap the waves)
+    t.compute_ms += span(ctx->tp_begin_ev, ctx->tp_end_ev);
   t.ag_ms = ms(2, 3);  // all-gather tail exposed after the last wave
   t.d2h_ms = ms(3, 4);
   t.total_ms = ms(5, 4);

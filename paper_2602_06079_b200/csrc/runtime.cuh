@@ -119,6 +119,7 @@ struct osh_ctx {
   ncclComm_t tp_comm = nullptr;
   cudaStream_t tp_stream = nullptr;       // TP gathers / scatters (overlap the group GEMMs)
   cudaEvent_t tp_start_ev = nullptr, tp_done_ev = nullptr;
+  cudaEvent_t tp_begin_ev = nullptr, tp_end_ev = nullptr;  // tp_compute span (compute_ms)
   std::vector<cudaEvent_t> tp_gather_ev, tp_pack_ev;  // per micro group
   uint64_t tp_c_max = 268435456ull;  // 512 MiB of bf16 (optishard_cli.cpp:77-82,198)
   std::vector<optishard::ParamSpec> params_full;  // full shapes; `params` is the shard view
@@ -146,7 +147,11 @@ struct osh_ctx {
 namespace osh {
 // TP helpers (tp.cu)
 osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
-osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
+// TP step in two halves: tp_gather (TP stream, after `ready`) is issued
+// before the DP waves so the gathers overlap them; tp_compute (on cs) runs
+// each group's full-matrix Muon after its gather, then packs and scatters.
+osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready);
+osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
 osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs);  // checkpoint resume
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);

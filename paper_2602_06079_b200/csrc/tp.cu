@@ -276,17 +276,17 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
   return OSH_OK;
 }
 
-osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
+// The TP transfers run on their own stream: all gathers are issued first
+// (group order) as soon as the reduced gradients exist — they overlap the DP
+// waves of the step — the compute of group g waits only for gather g, and
+// the scatter of group g follows its pack, so the gathers / scatters of other
+// groups overlap the Newton-Schulz GEMMs. Every TP rank issues the same
+// collective sequence on tp_comm (gathers 0..G-1, then scatters 0..G-1).
+osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready) {
   const int T = ctx->tp_size, me = ctx->tp_rank;
   const size_t es = gsize(ctx);
-  // The TP transfers run on their own stream: all gathers are issued first
-  // (group order), the compute of group g waits only for gather g, and the
-  // scatter of group g follows its pack — so the gathers / scatters of other
-  // groups overlap the Newton-Schulz GEMMs. Every TP rank issues the same
-  // collective sequence on tp_comm (gathers 0..G-1, then scatters 0..G-1).
   cudaStream_t ts = ctx->tp_stream;
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_start_ev, cs));
-  OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_start_ev, 0));
+  for (cudaEvent_t e : ready) OSH_CUDA_TRY(cudaStreamWaitEvent(ts, e, 0));
   for (int g = 0; g < ctx->tp_groups; ++g) {
     // ---- gather reduced-gradient shards to the hosts
     TP_NCCL(ncclGroupStart());
@@ -307,6 +307,11 @@ osh_status tp_step(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
     TP_NCCL(ncclGroupEnd());
     OSH_CUDA_TRY(cudaEventRecord(ctx->tp_gather_ev[g], ts));
   }
+  return OSH_OK;
+}
+
+osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
+  cudaStream_t ts = ctx->tp_stream;
   for (int g = 0; g < ctx->tp_groups; ++g) {
     OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
     OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),

@@ -198,3 +198,37 @@ def test_bf16_gradients_close_to_fp32():
         rel = np.abs(a[0][p.id] - b[0][p.id]).max() / np.abs(a[0][p.id]).max()
         print("bf16-vs-f32", p.name, rel)
         assert rel < TOL_W, (p.name, rel)
+
+
+def test_stream_k_gram_matches_oracle_and_is_plan_invariant():
+    """A 4096 x 16384 matrix's GRAM (136 symmetric 256 x 256 tiles, 256
+    k-blocks: more tiles than CTA pairs, a part-empty last round) runs
+    stream-K: its k-blocks are cut into equal ranges per CTA pair and the
+    tiles cut across pairs are finished by a fixed-order fixup. The cut points
+    depend only on the matrix, so the result is the same bits whichever plan /
+    wave the tensor lands in, and it matches the fp64 oracle."""
+    params = [P.ParamSpec(0, "wide", (4096, 16384)), P.ParamSpec(1, "m", (1024, 3072)),
+              P.ParamSpec(2, "v", (4096,))]
+    one = run_gpu(params, 100_000_000, 1, 1, 1)
+    two = run_gpu(params, 100_000_000, 2, 1, 1)
+    for p in params:
+        assert np.array_equal(one[0][p.id], two[0][p.id]), p.name
+    O.set_fast_blas(True)
+    try:
+        ref = oracle_run(params, 1, 1)
+    finally:
+        O.set_fast_blas(False)
+    errs = errors(params, one, ref)
+    print({p.name: {k: f"{v:.2e}" for k, v in errs[p.id].items()} for p in params})
+    assert_within(params, errs)
+    # the launch really was stream-K
+    plan = P.plan_dp(params, 100_000_000, 1, "alpha-balanced", "numel", 1.0)
+    with DistributedMuon(params, 100_000_000, plan, comm="none") as c:
+        c.fill_synthetic(1, "weights")
+        c.fill_synthetic(2, "grads")
+        c.profile_gemm(True)
+        c.step()
+        c.sync()
+        grams = [w for mode, _, _, _, w in c.gemm_profile_launches() if mode == "gram"]
+        c.profile_gemm(False)
+    assert grams and all("stream-k" in w for w in grams if "16384" in w), grams
