@@ -405,8 +405,12 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   fold_a_ = !(aux != nullptr && std::strcmp(aux, "1") == 0);
   const char* lpt = std::getenv("OSH_GEMM_LPT");
   lpt_ = !(lpt != nullptr && std::strcmp(lpt, "0") == 0);
+  // tail-split GRAM (ns_gemm_stream_k_schedule) is opt-in: under the B200's
+  // power cap the part-empty last round of a vocabulary GRAM costs nothing
+  // measurable (idle SMs leave the busy ones more power), while the partial
+  // slots cost traffic — DESIGN.md §3, profiles/r02_stream_k_ab.json
   const char* skv = std::getenv("OSH_STREAM_K");
-  stream_k_ = !(skv != nullptr && std::strcmp(skv, "0") == 0);
+  stream_k_ = skv != nullptr && std::strcmp(skv, "1") == 0;
   int sk_slots = 0;  // partial slots of the largest stream-K GRAM
   sched_symmetric_ = symmetric_;
   for (Wave& w : waves_) {

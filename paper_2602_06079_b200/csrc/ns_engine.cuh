@@ -127,7 +127,7 @@ class MuonEngine : public OptimizerEngine {
   int* d_fslot_count_ = nullptr;
   int* d_fslot_tensor_ = nullptr;
   bool fuse_final_ = true;        // OSH_FUSE_FINAL=0: UPDATE + apply_update everywhere
-  bool stream_k_ = true;          // OSH_STREAM_K=0: whole-tile LPT schedules for every GRAM
+  bool stream_k_ = false;         // OSH_STREAM_K=1: tail-split GRAM for few long-K tiles
   float* d_sk_ws_ = nullptr;      // stream-K partial tiles (fp32, 256 x 256 per slot)
   bool symmetric_ = true;
   bool double_buffer_ = false;
