@@ -376,6 +376,12 @@ def run_ours(a, dist: Dist):
         torch.cuda.synchronize()
         dist.barrier()
         eng.sync()
+        # N > 1 (sharded, TP 1): each rank reads back the parameters it updated
+        # (its owned slices, as soon as its wave is done); the full replica
+        # stays all-gathered on the devices for the next forward pass
+        owned_out = N > 1 and T == 1 and a.strategy == "sharded"
+        if owned_out:
+            eng.set_host_output("owned")
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(a.e2e_steps):
@@ -383,7 +389,9 @@ def run_ours(a, dist: Dist):
         f1.record(stream)
         f1.synchronize()
         e2e_ms = f0.elapsed_time(f1) / a.e2e_steps
-        e2e = {"e2e_ms": e2e_ms, "h2d": total * hg.element_size(), "d2h": total * 2}
+        e2e = {"e2e_ms": e2e_ms, "h2d": total * hg.element_size(),
+               "d2h": (info["owned_numel"] if owned_out else total) * 2,
+               "d2h_what": "own updated slices" if owned_out else "full bf16 replica"}
         del hg, hr
 
     rec = {"ms": ms, "prof": prof, "prof_steps": prof_steps, "by_mode": by_mode, "last": last, "info": info, "e2e": e2e,
@@ -483,7 +491,9 @@ def run_ours(a, dist: Dist):
         e = max(r["e2e"]["e2e_ms"] for r in allrec)
         out["e2e"] = {"value": round(e, 3), "unit": "ms",
                       "h2d_bytes_per_step": allrec[0]["e2e"]["h2d"],
-                      "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"]}
+                      "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"],
+                      "note": "per rank: H2D its full local bf16 gradient (pinned), D2H "
+                              + allrec[0]["e2e"]["d2h_what"] + "; bytes are rank 0's"}
     if a.optimizer == "soap":
         rms = max(r["refresh_ms"] for r in allrec)
         out["soap"] = {"block": a.shampoo_block, "precond_every": a.precond_every,

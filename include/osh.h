@@ -382,7 +382,14 @@ osh_status osh_fill_synthetic(osh_ctx* ctx, uint64_t seed, int32_t what, float s
 
 /* One distributed Muon step: [H2D host_grads (flat, grad dtype) ->]
  * RS-v -> owner Muon -> AG-v [-> D2H updated replica into host_replica_out].
- * Either host pointer may be NULL (device-resident data). */
+ * Either host pointer may be NULL (device-resident data). What host_replica_out
+ * receives (osh_ctx_set_host_output): OSH_HOST_OUT_REPLICA (default) the
+ * whole all-gathered replica; OSH_HOST_OUT_OWNED on a sharded multi-rank ctx
+ * only the slices this rank updated (at their flat offsets; the rest of the
+ * buffer is left untouched) — the rank's result, copied as soon as its wave
+ * finishes, without waiting for the all-gather. */
+enum { OSH_HOST_OUT_REPLICA = 0, OSH_HOST_OUT_OWNED = 1 };
+osh_status osh_ctx_set_host_output(osh_ctx* ctx, int32_t mode);
 osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
                     void* host_replica_out);
 /* Gradient bucket `bucket` is complete in the grad buffer (its writes were

@@ -185,6 +185,7 @@ def _declare(L: ctypes.CDLL) -> None:
          POINTER(c_int32)),
         ("osh_ctx_comm_schedule", c_int32, c_void_p, POINTER(CollOp), c_int32, POINTER(c_int32)),
         ("osh_ctx_set_timeout", c_int32, c_void_p, c_double),
+        ("osh_ctx_set_host_output", c_int32, c_void_p, c_int32),
         ("osh_write_state", c_int32, c_void_p, c_int32, c_int32, POINTER(c_float)),
         ("osh_muon_apply_host", c_int32, c_int32, POINTER(ParamDesc), POINTER(MuonCfgC),
          POINTER(c_double), POINTER(c_double), POINTER(c_double), POINTER(c_double)),

@@ -865,8 +865,37 @@ struct HostIo {
   bool nvls_out = false;   // NVLS: a cross-rank barrier per bucket precedes its D2H
 };
 
+// OSH_HOST_OUT_OWNED on a sharded multi-rank ctx: each rank reads back only
+// the slices it updated (its result); otherwise the whole replica bucket.
+bool owned_out(const osh_ctx* ctx) {
+  return ctx->host_out_owned && distributed(ctx) && ctx->tp_size == 1 &&
+         ctx->strategy == OSH_STRAT_SHARDED;
+}
+
+osh_status copy_bucket_out(osh_ctx* ctx, void* host, int b, cudaStream_t st) {
+  const int nb = static_cast<int>(ctx->cuts.size());
+  int64_t b0 = ctx->bucket_base[b];
+  int64_t b1 = b + 1 < nb ? ctx->bucket_base[b + 1] : ctx->total_numel;
+  if (owned_out(ctx)) {
+    b1 = ctx->bucket_base[b] + ctx->cuts[b][ctx->rank + 1];
+    b0 = ctx->bucket_base[b] + ctx->cuts[b][ctx->rank];
+  }
+  if (b1 > b0)
+    OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<__nv_bfloat16*>(host) + b0, ctx->replica + b0,
+                                 2 * static_cast<size_t>(b1 - b0), cudaMemcpyDeviceToHost, st));
+  return OSH_OK;
+}
+
 osh_status d2h_buckets(osh_ctx* ctx, HostIo& io, int upto, cudaEvent_t ready) {
   if (io.replica_out == nullptr || upto < io.d2h_next) return OSH_OK;
+  if (owned_out(ctx)) {  // own slices only: final on this rank, no cross-rank wait
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ready, 0));
+    for (int b = io.d2h_next; b <= upto; ++b)
+      if (osh_status st = copy_bucket_out(ctx, io.replica_out, b, ctx->d2h_stream); st != OSH_OK)
+        return st;
+    io.d2h_next = upto + 1;
+    return OSH_OK;
+  }
   if (io.nvls_out) {
     // every rank's multicast stores into these buckets must have landed: one
     // barrier per bucket on the comm stream (same count and order on every
@@ -907,15 +936,12 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   // barriers issued in the same order on every rank
   auto wave_done = [&](int w) -> osh_status {
     OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-    if (io.replica_out != nullptr && !io.nvls_out) {
+    if (io.replica_out != nullptr && (!io.nvls_out || owned_out(ctx))) {
+      // (owned slices need no cross-rank barrier: this rank wrote them)
       OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->wave_end[w], 0));
-      for (const int b : ctx->wave_done_buckets[static_cast<size_t>(w)]) {
-        const int64_t b0 = ctx->bucket_base[b];
-        const int64_t b1 = b + 1 < nb ? ctx->bucket_base[b + 1] : ctx->total_numel;
-        OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<__nv_bfloat16*>(io.replica_out) + b0,
-                                     ctx->replica + b0, 2 * static_cast<size_t>(b1 - b0),
-                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
-      }
+      for (const int b : ctx->wave_done_buckets[static_cast<size_t>(w)])
+        if (osh_status st = copy_bucket_out(ctx, io.replica_out, b, ctx->d2h_stream); st != OSH_OK)
+          return st;
       if (w + 1 == nw) io.d2h_next = nb;  // every bucket is out
       return OSH_OK;
     }
@@ -1232,6 +1258,14 @@ osh_status osh_ctx_sync(osh_ctx* ctx) {
   if (osh_status st = osh::wait_stream(ctx, ctx->compute); st != OSH_OK) return st;
   if (osh_status st = osh::wait_stream(ctx, ctx->comm_stream); st != OSH_OK) return st;
   if (ctx->aborted) return osh::fail(OSH_ERR_NCCL, "communicators were aborted by the watchdog");
+  return OSH_OK;
+}
+
+osh_status osh_ctx_set_host_output(osh_ctx* ctx, int32_t mode) {
+  if (ctx == nullptr) return osh::fail(OSH_ERR_ARG, "null osh_ctx");
+  if (mode != OSH_HOST_OUT_REPLICA && mode != OSH_HOST_OUT_OWNED)
+    return osh::fail(OSH_ERR_ARG, "unknown host output mode");
+  ctx->host_out_owned = mode == OSH_HOST_OUT_OWNED;
   return OSH_OK;
 }
 

@@ -111,6 +111,7 @@ struct osh_ctx {
   // aborted and the ctx refuses further collective work
   double timeout_s = 600.0;
   bool aborted = false;
+  bool host_out_owned = false;  // osh_step host output: own slices only (OSH_HOST_OUT_OWNED)
 
   // ---- tensor parallelism: micro-group gather -> host Muon -> scatter
   // (paper Alg. 2; state keyed by (dp owner, tp host) as in

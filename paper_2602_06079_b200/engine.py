@@ -222,6 +222,12 @@ class DistributedMuon:
     def sync(self) -> None:
         _lib.check(_lib.lib().osh_ctx_sync(self._ctx))
 
+    def set_host_output(self, mode: str) -> None:
+        """What step(host_replica_out=...) receives: "replica" (the whole
+        all-gathered bf16 replica, default) or "owned" (only the slices this
+        rank updated, at their flat offsets)."""
+        _lib.check(_lib.lib().osh_ctx_set_host_output(self._ctx, {"replica": 0, "owned": 1}[mode]))
+
     def set_timeout(self, seconds: float) -> None:
         """Watchdog timeout of the ctx's host waits (osh_ctx_set_timeout): a
         collective that does not complete in time aborts the communicators

@@ -41,7 +41,8 @@ def main():
     coll = sys.argv[2] if len(sys.argv) > 2 else "auto"
     opt = sys.argv[3] if len(sys.argv) > 3 else "muon"
     announce = len(sys.argv) > 4 and sys.argv[4] == "buckets"  # osh_bucket_ready, reverse order
-    host = len(sys.argv) > 4 and sys.argv[4] == "host"  # e2e entry: host gradients / replica
+    host = len(sys.argv) > 4 and sys.argv[4] in ("host", "host_owned")  # e2e entry: host buffers
+    host_owned = len(sys.argv) > 4 and sys.argv[4] == "host_owned"  # D2H of own slices only
     ckpt = len(sys.argv) > 4 and sys.argv[4] == "ckpt"  # save / reload into a fresh ctx
     strategy = sys.argv[5] if len(sys.argv) > 5 else "sharded"  # or the sc / nv-layerwise baselines
     gdt = sys.argv[6] if len(sys.argv) > 6 else "f32"  # bf16: NVLS reduces bf16x8 with fp32 accumulation
@@ -72,6 +73,9 @@ def main():
     norms = []
     total = sum(p.numel for p in params)
     hrep = torch.empty(total, dtype=torch.bfloat16).pin_memory() if host else None
+    if host_owned:
+        eng.set_host_output("owned")
+        hrep.view(torch.int16).fill_(-1)  # sentinel: slices of other ranks stay untouched
     for step in range(steps):
         if host:
             hg = torch.from_numpy(np.concatenate(
@@ -121,7 +125,11 @@ def main():
     if host:  # the replica the step copied out must equal the device replica
         off = 0
         for p in params:
-            assert np.array_equal(hrep[off:off + p.numel].float().numpy(), replica[p.id].reshape(-1))
+            got = hrep[off:off + p.numel]
+            if host_owned and owners[p.id] != rank:  # another rank's result: untouched
+                assert bool((got.view(torch.int16) == -1).all()), p.name
+            else:
+                assert np.array_equal(got.float().numpy(), replica[p.id].reshape(-1)), p.name
             off += p.numel
     gathered = [None] * world
     td.all_gather_object(gathered, (mine, norms, replica, ckpt_ok))

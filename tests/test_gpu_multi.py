@@ -68,10 +68,12 @@ def test_dp2_nccl_bucket_ready_matches_oracle():
 
 
 def test_dp2_host_buffers_nvls_and_nccl():
-    # the e2e entry (host gradients in, replica out) on both collective paths
+    # the e2e entry (host gradients in, replica out) on both collective paths,
+    # whole replica and own slices only (OSH_HOST_OUT_OWNED)
     for coll in ("auto", "nccl"):
-        res = _run(2, "multi_gpu_check.py", 2, coll, "muon", "host")
-        assert res["host_buffers"]
+        for mode in ("host", "host_owned"):
+            res = _run(2, "multi_gpu_check.py", 2, coll, "muon", mode)
+            assert res["host_buffers"]
 
 
 @pytest.mark.parametrize("strategy", ["sc", "nv-layerwise"])
