@@ -1191,9 +1191,21 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     }
   }
   if (ctx->tp_size > 1) {
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));  // every DP (non-TP-plane) wave is done
     OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
     if (osh_status st = osh::tp_compute(ctx, *cfg, cs); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
+    if (dist) {
+      // AG-v per bucket, in bucket order on every rank, as soon as the DP
+      // waves and the last micro group with a TP item in the bucket have
+      // scattered — overlapping the remaining groups' Newton-Schulz
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[1], 0));
+      for (; ag_next < nb; ++ag_next) {
+        const int g = ctx->tp_bucket_group[static_cast<size_t>(ag_next)];
+        if (g >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->tp_scatter_ev[g], 0));
+        if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+      }
+    }
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
   if (dist) {

@@ -121,7 +121,8 @@ struct osh_ctx {
   cudaStream_t tp_stream = nullptr;       // TP gathers / scatters (overlap the group GEMMs)
   cudaEvent_t tp_start_ev = nullptr, tp_done_ev = nullptr;
   cudaEvent_t tp_begin_ev = nullptr, tp_end_ev = nullptr;  // tp_compute span (compute_ms)
-  std::vector<cudaEvent_t> tp_gather_ev, tp_pack_ev;  // per micro group
+  std::vector<cudaEvent_t> tp_gather_ev, tp_pack_ev, tp_scatter_ev;  // per micro group
+  std::vector<int> tp_bucket_group;  // per bucket: last micro group with an item in it (-1)
   uint64_t tp_c_max = 268435456ull;  // 512 MiB of bf16 (optishard_cli.cpp:77-82,198)
   std::vector<optishard::ParamSpec> params_full;  // full shapes; `params` is the shard view
   struct TpItem {

@@ -129,8 +129,11 @@ void tp_free(osh_ctx* ctx) {
   ctx->tp_engines.clear();
   for (cudaEvent_t e : ctx->tp_gather_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->tp_pack_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->tp_scatter_ev) cudaEventDestroy(e);
   ctx->tp_gather_ev.clear();
   ctx->tp_pack_ev.clear();
+  ctx->tp_scatter_ev.clear();
+  ctx->tp_bucket_group.clear();
   for (CopyTask* p : ctx->d_tp_unpack) cudaFree(p);
   for (CopyTask* p : ctx->d_tp_pack) cudaFree(p);
   ctx->d_tp_unpack.clear();
@@ -261,9 +264,17 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
   }
   ctx->tp_gather_ev.assign(ctx->tp_groups, nullptr);
   ctx->tp_pack_ev.assign(ctx->tp_groups, nullptr);
+  ctx->tp_scatter_ev.assign(ctx->tp_groups, nullptr);
   for (int g = 0; g < ctx->tp_groups; ++g) {
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_gather_ev[g], cudaEventDisableTiming));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_pack_ev[g], cudaEventDisableTiming));
+    OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_scatter_ev[g], cudaEventDisableTiming));
+  }
+  // a bucket's AG-v may go once the last group with a TP item in it scattered
+  ctx->tp_bucket_group.assign(ctx->cuts.size(), -1);
+  for (const osh_ctx::TpItem& it : ctx->tp_items) {
+    int& g = ctx->tp_bucket_group[static_cast<size_t>(ctx->bucket_of[it.pid])];
+    g = std::max(g, it.group);
   }
   for (int g = 0; g < ctx->tp_groups; ++g) {
     CopyTask* u = nullptr;
@@ -327,6 +338,7 @@ osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
     OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
     // ---- scatter updated bf16 shards into every rank's replica slot
     if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_scatter_ev[g], ts));
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ts));
   OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_done_ev, 0));
