@@ -75,6 +75,13 @@ class OptimizerEngine {
   virtual void set_step_counter(long long) {}
 
   const NsLaunchStats& stats() const { return stats_; }  // since begin_step()
+  // Engine tensor indices of wave w, in the order build() received them
+  // (empty when the engine does not record them): lets a single-rank step
+  // move host data wave by wave instead of bucket by bucket.
+  const std::vector<int>& wave_tensors(int w) const {
+    static const std::vector<int> kNone;
+    return w >= 0 && w < static_cast<int>(wave_tensors_.size()) ? wave_tensors_[w] : kNone;
+  }
   // Per-launch CUDA-event timing of every launch (roofline reporting); the
   // read_profile totals cover the GEMMs only, profile_text lists all launches.
   void set_profile(bool on) { profile_ = on; }
@@ -119,6 +126,7 @@ class OptimizerEngine {
   virtual const char* elementwise_name(int mode) const;
 
   NsLaunchStats stats_;
+  std::vector<std::vector<int>> wave_tensors_;
   bool profile_ = false;
   std::vector<Timed> timed_;
   std::vector<cudaEvent_t> event_pool_;

@@ -92,6 +92,7 @@ void MuonEngine::release() {
   sched_mem_.clear();
   chunks_.clear();
   waves_.clear();
+  wave_tensors_.clear();
 }
 
 osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int grad_dtype,
@@ -199,6 +200,8 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   std::vector<McCopyTask> mctasks;
   std::vector<long long> fslot_begin;
   std::vector<int> fslot_count, fslot_tensor;
+
+  wave_tensors_ = wave_members;
 
   // ---- chunks (one per class per wave), slots, tables
   std::vector<MomentumMatrixTask> mtasks;

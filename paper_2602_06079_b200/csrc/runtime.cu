@@ -103,6 +103,7 @@ void free_layout(osh_ctx* ctx) {
   destroy_events(ctx->pre_ev);
   destroy_events(ctx->ns_ev);
   destroy_events(ctx->h2d_ev);
+  destroy_events(ctx->h2d_wave_ev);
   destroy_events(ctx->ag_ev);
   if (ctx->nvls) {
     osh::nvls_free(ctx);
@@ -684,6 +685,36 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
     }
   }
   ctx->overlap = ctx->overlap && ctx->engine->double_buffered() && ctx->engine->num_waves() > 1;
+  {  // single rank: per-wave host transfer ranges (every tensor owned, each in one wave)
+    ctx->wave_io = false;
+    ctx->wave_ranges.clear();
+    destroy_events(ctx->h2d_wave_ev);
+    const int nw = ctx->engine->num_waves();
+    std::vector<int> param_of(static_cast<size_t>(ctx->engine->num_tensors()), -1);
+    for (size_t p = 0; p < ctx->params.size(); ++p)
+      if (ctx->engine_index[p] >= 0) param_of[static_cast<size_t>(ctx->engine_index[p])] = static_cast<int>(p);
+    int64_t covered = 0;
+    bool ok = ctx->size == 1 && ctx->tp_size == 1 && nw > 0;
+    for (int w = 0; w < nw && ok; ++w) {
+      const std::vector<int>& ts = ctx->engine->wave_tensors(w);
+      if (ts.empty()) ok = false;
+      std::vector<std::pair<int64_t, int64_t>> r;
+      for (const int ti : ts) {
+        const int p = param_of[static_cast<size_t>(ti)];
+        if (p < 0) {
+          ok = false;
+          break;
+        }
+        const int64_t off = ctx->flat_off[static_cast<size_t>(p)], cnt = ctx->params[static_cast<size_t>(p)].numel;
+        if (!r.empty() && r.back().first + r.back().second == off) r.back().second += cnt;
+        else r.emplace_back(off, cnt);
+        covered += cnt;
+      }
+      ctx->wave_ranges.push_back(std::move(r));
+    }
+    ctx->wave_io = ok && covered == ctx->total_numel;
+    if (ctx->wave_io) OSH_CUDA_TRY(make_events(ctx->h2d_wave_ev, static_cast<size_t>(nw)));
+  }
   if (ctx->tp_size > 1)
     if (osh_status st = osh::tp_setup(ctx, static_cast<int64_t>(budget)); st != OSH_OK) return st;
   OSH_CUDA_TRY(make_events(ctx->rs_ev, ctx->cuts.size()));
@@ -863,6 +894,7 @@ struct HostIo {
   void* replica_out = nullptr;  // per-bucket D2H after each wave (nullptr: none)
   int d2h_next = 0;
   bool nvls_out = false;   // NVLS: a cross-rank barrier per bucket precedes its D2H
+  bool per_wave = false;   // single rank: H2D / D2H per wave (ctx->wave_ranges)
 };
 
 // OSH_HOST_OUT_OWNED on a sharded multi-rank ctx: each rank reads back only
@@ -924,6 +956,10 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   const int nw = eng.num_waves();
   const int nb = static_cast<int>(ctx->cuts.size());
   auto wait_input = [&](int w) -> osh_status {
+    if (io.per_wave) {
+      OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_wave_ev[static_cast<size_t>(w)], 0));
+      return OSH_OK;
+    }
     const std::vector<cudaEvent_t>* ev = io.wait_ev != nullptr ? io.wait_ev
                                          : io.h2d ? &ctx->h2d_ev : nullptr;
     if (ev != nullptr)  // every bucket of the wave (announced buckets may land out of order)
@@ -936,6 +972,15 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
   // barriers issued in the same order on every rank
   auto wave_done = [&](int w) -> osh_status {
     OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
+    if (io.replica_out != nullptr && io.per_wave) {  // exactly this wave's tensors
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->wave_end[w], 0));
+      for (const auto& [off, cnt] : ctx->wave_ranges[static_cast<size_t>(w)])
+        OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<__nv_bfloat16*>(io.replica_out) + off,
+                                     ctx->replica + off, 2 * static_cast<size_t>(cnt),
+                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
+      if (w + 1 == nw) io.d2h_next = nb;
+      return OSH_OK;
+    }
     if (io.replica_out != nullptr && (!io.nvls_out || owned_out(ctx))) {
       // (owned slices need no cross-rank barrier: this rank wrote them)
       OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->wave_end[w], 0));
@@ -1011,6 +1056,23 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   }
   if (marked) {
     io.h2d = true;  // waves / barriers wait for the announced buckets
+  } else if (host_grads != nullptr && pipelined && ctx->wave_io && !distributed(ctx)) {
+    // one rank: each wave's own tensors, in execution order (the first wave
+    // starts after its bytes, not after whole buckets)
+    io.h2d = true;
+    io.per_wave = true;
+    const size_t ges = grad_esize(ctx->grad_dtype);
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
+    for (size_t w = 0; w < ctx->wave_ranges.size(); ++w) {
+      for (const auto& [off, cnt] : ctx->wave_ranges[w])
+        OSH_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->grad) + ges * static_cast<size_t>(off),
+                                     static_cast<const uint8_t*>(host_grads) + ges * static_cast<size_t>(off),
+                                     ges * static_cast<size_t>(cnt), cudaMemcpyHostToDevice,
+                                     ctx->h2d_stream));
+      OSH_CUDA_TRY(cudaEventRecord(ctx->h2d_wave_ev[w], ctx->h2d_stream));
+    }
+    for (cudaEvent_t e : ctx->h2d_ev) OSH_CUDA_TRY(cudaEventRecord(e, ctx->h2d_stream));  // all landed
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
   } else if (host_grads != nullptr && pipelined) {
     io.h2d = true;
     OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
@@ -1026,7 +1088,10 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   } else if (host_grads != nullptr && !ctx->nvls) {  // (NVLS: copied in its branch)
     OSH_CUDA_TRY(cudaMemcpyAsync(ctx->grad, host_grads, gbytes, cudaMemcpyHostToDevice, cs));
   }
-  if (host_replica_out != nullptr && pipelined) io.replica_out = host_replica_out;
+  if (host_replica_out != nullptr && pipelined) {
+    io.replica_out = host_replica_out;
+    io.per_wave = io.per_wave || (ctx->wave_io && !distributed(ctx) && !marked);
+  }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[0], cs));
   const int nb = static_cast<int>(ctx->cuts.size());
   osh::OptimizerEngine& eng = *ctx->engine;

@@ -86,6 +86,12 @@ struct osh_ctx {
   std::vector<int> wave_final_upto;
   std::vector<std::vector<int>> wave_done_buckets;  // per wave: buckets it completes
   std::vector<int> h2d_bucket_order;
+  // single rank: per wave, the merged flat element ranges (offset, count) of
+  // its tensors; host gradients / replica then move wave by wave (the first
+  // wave waits for its own tensors only, the last wave's copy-out is its own)
+  bool wave_io = false;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> wave_ranges;
+  std::vector<cudaEvent_t> h2d_wave_ev;
   // NVLS-fused collectives (nvls.cu): grad / replica are symmetric windows,
   // the update kernels reduce / broadcast through their multicast addresses
   int coll_mode = 0;                    // OSH_COLL_AUTO / _NCCL / _NVLS
