@@ -67,7 +67,7 @@ class CtxInfo(ctypes.Structure):
                 ("n_owned", c_int32), ("n_buckets", c_int32), ("n_waves", c_int32),
                 ("workspace_bytes", c_int64), ("device_bytes", c_int64),
                 ("ns_flops_per_iter", c_double), ("collectives", c_int32),
-                ("reserved_", c_int32)]
+                ("reserved", c_int32)]
 
 
 class ShampooCfgC(ctypes.Structure):
