@@ -1223,76 +1223,52 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   };
   int ag_next = 0;
   if (ctx->tp_size > 1) {
-    // DP waves (this DP rank's non-TP-plane tensors) and micro groups run on
-    // cs in readiness order: a wave when its last bucket's reduce-scatter
-    // landed, a group when its gather (issued after the reduce-scatter of its
-    // last bucket) did. AG-v of a bucket follows its last wave and the last
-    // group with an item in it, overlapping the remaining work.
-    if (osh_status st = osh::tp_gather(ctx, dist ? &ctx->rs_ev : io.h2d ? &ctx->h2d_ev : nullptr,
-                                       ctx->ev[0]);
-        st != OSH_OK)
-      return st;
-    struct Item {
-      int ready, kind, idx;  // kind 0 = DP wave, 1 = micro group
-    };
-    std::vector<Item> items;
-    for (int w = 0; w < nw; ++w) items.push_back({eng.wave_last_bucket(w), 0, w});
-    for (const int g : ctx->tp_order) items.push_back({ctx->tp_group_ready[static_cast<size_t>(g)], 1, g});
-    std::stable_sort(items.begin(), items.end(),
-                     [](const Item& a, const Item& b) { return a.ready < b.ready; });
-    std::vector<int> last_wave(static_cast<size_t>(nb), -1);
-    for (int w = 0; w < nw; ++w)
-      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b)
-        last_wave[static_cast<size_t>(b)] = w;
-    bool first = true;
-    for (const Item& it : items) {
-      if (it.kind == 0) {
-        const int w = it.idx;
-        for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b) {
-          if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
-          else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
-        }
-        OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
-        if (first) OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
-        if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
-        OSH_CUDA_TRY(cudaGetLastError());
-        OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-      } else {
-        if (first) {
-          OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[it.idx], 0));
-          OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
-        }
-        if (osh_status st = osh::tp_compute_group(ctx, *cfg, cs, it.idx); st != OSH_OK) return st;
-      }
-      first = false;
-    }
-    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
-    if (osh_status st = osh::tp_finish(ctx, cs); st != OSH_OK) return st;
-    if (dist) {
-      for (; ag_next < nb; ++ag_next) {
-        const int w = last_wave[static_cast<size_t>(ag_next)];
-        const int g = ctx->tp_bucket_group[static_cast<size_t>(ag_next)];
-        if (w >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
-        if (g >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->tp_scatter_ev[g], 0));
-        if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
-      }
-    }
-  } else if (!dist) {
+    // micro-group gathers need every reduced shard of the TP plane: they go
+    // out on the TP stream once the whole reduce-scatter (or H2D) landed,
+    // overlapping the DP waves below
+    std::vector<cudaEvent_t> ready;
+    if (dist) ready = ctx->rs_ev;
+    else if (io.h2d) ready = ctx->h2d_ev;
+    ready.push_back(ctx->ev[0]);
+    if (osh_status st = osh::tp_gather(ctx, ready); st != OSH_OK) return st;
+  }
+  if (!dist && ctx->tp_size == 1) {
     if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
   } else {
     for (int w = 0; w < nw; ++w) {
-      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b)
-        OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
+      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b) {
+        if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
+        else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+      }
       OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
       if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaGetLastError());
       OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-      // buckets no later wave of this rank touches are final on this rank
-      const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
-      if (done >= ag_next) {
-        OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
-        for (; ag_next <= done; ++ag_next)
-          if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+      if (dist && ctx->tp_size == 1) {
+        // buckets no later wave of this rank touches are final on this rank
+        const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
+        if (done >= ag_next) {
+          OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
+          for (; ag_next <= done; ++ag_next)
+            if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+        }
+      }
+    }
+  }
+  if (ctx->tp_size > 1) {
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));  // every DP (non-TP-plane) wave is done
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
+    if (osh_status st = osh::tp_compute(ctx, *cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
+    if (dist) {
+      // AG-v per bucket, in bucket order on every rank, as soon as the DP
+      // waves and the last micro group with a TP item in the bucket have
+      // scattered — overlapping the remaining groups' Newton-Schulz
+      OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[1], 0));
+      for (; ag_next < nb; ++ag_next) {
+        const int g = ctx->tp_bucket_group[static_cast<size_t>(ag_next)];
+        if (g >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->tp_scatter_ev[g], 0));
+        if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
       }
     }
   }
@@ -1451,13 +1427,13 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
   const bool dist = distributed(ctx);
   t.rs_ms = dist && !ctx->rs_ev.empty() ? span(ctx->ev[0], ctx->rs_ev.back()) : 0.f;
   t.compute_ms = 0.f;  // busy time of the waves (excludes waiting for the RS)
-  if (ctx->tp_size > 1 && ctx->tp_begin_ev != nullptr)  // DP waves and micro groups interleaved
-    t.compute_ms = span(ctx->tp_begin_ev, ctx->tp_end_ev);
-  else if (ctx->overlap && !ctx->wave_begin.empty())
+  if (ctx->overlap && !ctx->wave_begin.empty())
     t.compute_ms = span(ctx->wave_begin.front(), ctx->wave_end.back());
   else
     for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
       t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
+  if (ctx->tp_size > 1 && ctx->tp_begin_ev != nullptr)  // + the micro groups (gathers overlap the waves)
+    t.compute_ms += span(ctx->tp_begin_ev, ctx->tp_end_ev);
   t.ag_ms = ms(2, 3);  // all-gather tail exposed after the last wave
   t.d2h_ms = ms(3, 4);
   t.total_ms = ms(5, 4);

@@ -128,9 +128,7 @@ struct osh_ctx {
   cudaEvent_t tp_start_ev = nullptr, tp_done_ev = nullptr;
   cudaEvent_t tp_begin_ev = nullptr, tp_end_ev = nullptr;  // tp_compute span (compute_ms)
   std::vector<cudaEvent_t> tp_gather_ev, tp_pack_ev, tp_scatter_ev;  // per micro group
-  std::vector<int> tp_bucket_group;  // per bucket: last micro group (exec order) with an item in it (-1)
-  std::vector<int> tp_group_ready;   // per group: last bucket holding one of its items
-  std::vector<int> tp_order;         // groups in execution (readiness) order
+  std::vector<int> tp_bucket_group;  // per bucket: last micro group with an item in it (-1)
   uint64_t tp_c_max = 268435456ull;  // 512 MiB of bf16 (optishard_cli.cpp:77-82,198)
   std::vector<optishard::ParamSpec> params_full;  // full shapes; `params` is the shard view
   struct TpItem {
@@ -157,14 +155,11 @@ struct osh_ctx {
 namespace osh {
 // TP helpers (tp.cu)
 osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
-// TP step: tp_gather (TP stream) issues every group's gather in execution
-// order, each after the reduce-scatter of its last bucket (per_bucket, or
-// only `start` when null); tp_compute_group (on cs) runs one group's
-// full-matrix Muon after its gather, then packs and scatters; tp_finish joins
-// the TP stream back into cs.
-osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>* per_bucket, cudaEvent_t start);
-osh_status tp_compute_group(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs, int g);
-osh_status tp_finish(osh_ctx* ctx, cudaStream_t cs);
+// TP step in two halves: tp_gather (TP stream, after `ready`) is issued
+// before the DP waves so the gathers overlap them; tp_compute (on cs) runs
+// each group's full-matrix Muon after its gather, then packs and scatters.
+osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready);
+osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
 osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs);  // checkpoint resume
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);

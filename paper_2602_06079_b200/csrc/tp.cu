@@ -270,27 +270,11 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_pack_ev[g], cudaEventDisableTiming));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_scatter_ev[g], cudaEventDisableTiming));
   }
-  // readiness of a group = the last bucket any of its items sits in (its
-  // gather may go once that bucket's reduce-scatter landed); groups run in
-  // readiness order — the plan fixes membership, not execution order, and
-  // the order is a function of the plan alone (the same on every TP rank)
-  ctx->tp_group_ready.assign(static_cast<size_t>(ctx->tp_groups), 0);
-  for (const osh_ctx::TpItem& it : ctx->tp_items) {
-    int& r = ctx->tp_group_ready[static_cast<size_t>(it.group)];
-    r = std::max(r, ctx->bucket_of[it.pid]);
-  }
-  ctx->tp_order.resize(static_cast<size_t>(ctx->tp_groups));
-  for (int g = 0; g < ctx->tp_groups; ++g) ctx->tp_order[static_cast<size_t>(g)] = g;
-  std::stable_sort(ctx->tp_order.begin(), ctx->tp_order.end(), [&](int a, int b) {
-    return ctx->tp_group_ready[static_cast<size_t>(a)] < ctx->tp_group_ready[static_cast<size_t>(b)];
-  });
-  // a bucket's AG-v may go once the last group (in execution order) with a
-  // TP item in it has scattered
+  // a bucket's AG-v may go once the last group with a TP item in it scattered
   ctx->tp_bucket_group.assign(ctx->cuts.size(), -1);
-  for (int k = 0; k < ctx->tp_groups; ++k) {
-    const int g = ctx->tp_order[static_cast<size_t>(k)];
-    for (const osh_ctx::TpItem& it : ctx->tp_items)
-      if (it.group == g) ctx->tp_bucket_group[static_cast<size_t>(ctx->bucket_of[it.pid])] = g;
+  for (const osh_ctx::TpItem& it : ctx->tp_items) {
+    int& g = ctx->tp_bucket_group[static_cast<size_t>(ctx->bucket_of[it.pid])];
+    g = std::max(g, it.group);
   }
   for (int g = 0; g < ctx->tp_groups; ++g) {
     CopyTask* u = nullptr;
@@ -309,15 +293,12 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
 // the scatter of group g follows its pack, so the gathers / scatters of other
 // groups overlap the Newton-Schulz GEMMs. Every TP rank issues the same
 // collective sequence on tp_comm (gathers 0..G-1, then scatters 0..G-1).
-osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>* per_bucket, cudaEvent_t start) {
+osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready) {
   const int T = ctx->tp_size, me = ctx->tp_rank;
   const size_t es = gsize(ctx);
   cudaStream_t ts = ctx->tp_stream;
-  OSH_CUDA_TRY(cudaStreamWaitEvent(ts, start, 0));
-  for (const int g : ctx->tp_order) {
-    if (per_bucket != nullptr)  // buckets land in order: the group's last one covers the rest
-      OSH_CUDA_TRY(cudaStreamWaitEvent(
-          ts, (*per_bucket)[static_cast<size_t>(ctx->tp_group_ready[static_cast<size_t>(g)])], 0));
+  for (cudaEvent_t e : ready) OSH_CUDA_TRY(cudaStreamWaitEvent(ts, e, 0));
+  for (int g = 0; g < ctx->tp_groups; ++g) {
     // ---- gather reduced-gradient shards to the hosts
     TP_NCCL(ncclGroupStart());
     for (osh_ctx::TpItem& it : ctx->tp_items) {
@@ -340,28 +321,26 @@ osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>* per_bucket, c
   return OSH_OK;
 }
 
-osh_status tp_compute_group(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs, int g) {
+osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
   cudaStream_t ts = ctx->tp_stream;
-  OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
-  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
-                                  ctx->tp_unpack_tiles[g], cs));
-  // ---- full-matrix Muon on the host
-  MuonEngine& eng = *ctx->tp_engines[g];
-  if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
-  for (int w = 0; w < eng.num_waves(); ++w)
-    if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
-  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
-                                  ctx->tp_pack_tiles[g], cs));
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
-  OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
-  // ---- scatter updated bf16 shards into every rank's replica slot
-  if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_scatter_ev[g], ts));
-  return OSH_OK;
-}
-
-osh_status tp_finish(osh_ctx* ctx, cudaStream_t cs) {
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ctx->tp_stream));
+  for (int g = 0; g < ctx->tp_groups; ++g) {
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
+    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
+                                    ctx->tp_unpack_tiles[g], cs));
+    // ---- full-matrix Muon on the host
+    MuonEngine& eng = *ctx->tp_engines[g];
+    if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
+    for (int w = 0; w < eng.num_waves(); ++w)
+      if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
+                                    ctx->tp_pack_tiles[g], cs));
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
+    // ---- scatter updated bf16 shards into every rank's replica slot
+    if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_scatter_ev[g], ts));
+  }
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ts));
   OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_done_ev, 0));
   return OSH_OK;
 }
