@@ -189,35 +189,6 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
       if (wi != first && wi != last) ordered.push_back(wave_members[wi]);
     ordered.push_back(wave_members[last]);
     wave_members.swap(ordered);
-    // Edge waves: the first wave's input and the last wave's output are what
-    // a step with host buffers cannot overlap (per-wave H2D before the first
-    // GEMMs, D2H after the last), so a few tensors of the first / last wave
-    // are split off into a small wave of their own (~1/64 of the owned
-    // elements, at most 64 M). OSH_EDGE_WAVES=0 keeps the waves whole.
-    const char* ev = std::getenv("OSH_EDGE_WAVES");
-    if (!(ev != nullptr && std::strcmp(ev, "0") == 0)) {
-      double total = 0.0;
-      for (const MuonTensorDesc& t : tensors) total += static_cast<double>(t.rows) * t.cols;
-      const double target = std::min(total / 64.0, 64.0 * (1 << 20));
-      const auto numel = [&](int ti) { return static_cast<double>(tensors[ti].rows) * tensors[ti].cols; };
-      // head of the first wave (from its front) and tail of the last (from its back)
-      for (int edge = 0; edge < 2; ++edge) {
-        std::vector<int>& src = edge == 0 ? wave_members.front() : wave_members.back();
-        if (src.size() < 2) continue;
-        std::vector<int> cut;
-        double acc = 0.0;
-        while (src.size() > 1 && (cut.empty() || acc + numel(edge == 0 ? src.front() : src.back()) <= target)) {
-          const int ti = edge == 0 ? src.front() : src.back();
-          acc += numel(ti);
-          cut.push_back(ti);
-          if (edge == 0) src.erase(src.begin());
-          else src.pop_back();
-        }
-        if (edge == 1) std::reverse(cut.begin(), cut.end());
-        if (edge == 0) wave_members.insert(wave_members.begin(), cut);
-        else wave_members.push_back(cut);
-      }
-    }
   }
 
   // fused FINAL targets: (tensor, m, n, partial offset) per fused matrix slot
