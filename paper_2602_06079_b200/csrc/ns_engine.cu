@@ -182,13 +182,48 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
     std::vector<size_t> idx(wave_members.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return elems[a] < elems[b]; });
-    const size_t first = idx[0], last = idx[1];
+    const char* tv = std::getenv("OSH_TAPER");
+    const bool taper = !(tv != nullptr && std::strcmp(tv, "0") == 0);
+    size_t first = idx[0], last = idx[1];
+    if (taper)  // the tail is tapered below: last = the smallest wave of several tensors
+      for (size_t k = 1; k < idx.size(); ++k)
+        if (wave_members[idx[k]].size() >= 4) {
+          last = idx[k];
+          break;
+        }
     std::vector<std::vector<int>> ordered;
     ordered.push_back(wave_members[first]);
     for (size_t wi = 0; wi < wave_members.size(); ++wi)
       if (wi != first && wi != last) ordered.push_back(wave_members[wi]);
     ordered.push_back(wave_members[last]);
     wave_members.swap(ordered);
+    // Tapered tail: with host buffers the bf16 replica of a wave leaves (D2H)
+    // while the next wave computes, so what stays exposed is the copy-out of
+    // the LAST wave. The last wave is cut into parts shrinking by ~0.7x toward
+    // the end (a part's compute covers the previous part's copy-out: D2H
+    // moves ~1.4x more elements per ms than the step computes), the final part
+    // <= 1/128 of the owned elements. OSH_TAPER=0 keeps the last wave whole.
+    if (taper) {
+      const auto numel = [&](int ti) { return static_cast<double>(tensors[ti].rows) * tensors[ti].cols; };
+      double total = 0.0;
+      for (const MuonTensorDesc& t : tensors) total += numel(static_cast<int>(&t - tensors.data()));
+      std::vector<int> src = wave_members.back();
+      wave_members.pop_back();
+      std::vector<std::vector<int>> parts;  // built from the back: smallest first
+      double target = total / 128.0;
+      while (!src.empty()) {
+        std::vector<int> part;
+        double acc = 0.0;
+        while (!src.empty() && (part.empty() || acc + numel(src.back()) <= target)) {
+          acc += numel(src.back());
+          part.insert(part.begin(), src.back());
+          src.pop_back();
+        }
+        parts.push_back(part);
+        target /= 0.7;
+      }
+      for (auto it = parts.rbegin(); it != parts.rend(); ++it) wave_members.push_back(*it);
+    }
   }
 
   // fused FINAL targets: (tensor, m, n, partial offset) per fused matrix slot
