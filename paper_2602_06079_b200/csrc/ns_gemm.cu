@@ -40,14 +40,19 @@ struct Cfg {
 #endif
   // FINAL also stages W boxes (48 KiB); 5 stages still fit (209 KiB) and
   // measured 5 % faster than 4 (OSH_FINAL_STAGE_DROP=1: one stage fewer)
-  static constexpr int kStages =
-      (CG == 1 ? 4 : OSH_CG2_STAGES) - (MODE == kEpiFinal ? OSH_FINAL_STAGE_DROP : 0);
+  // (1-CTA tiles stage 48 KiB per slot: FINAL keeps 3 of them there)
+  static constexpr int kStages = CG == 1 ? (MODE == kEpiFinal ? 3 : 4)
+                                         : OSH_CG2_STAGES - (MODE == kEpiFinal ? OSH_FINAL_STAGE_DROP : 0);
 };
 constexpr uint32_t kTmemCols = 512;
 // kEpiFinal staging per epilogue warp: kFinBufs 32x32 fp32 W boxes in flight
 constexpr int kFinBufs = 3;
 constexpr uint32_t kFinWBox = 32 * 32 * 4;
 constexpr uint32_t kFinBytes = 4 * kFinBufs * kFinWBox;
+template <int MODE, int CG>
+constexpr uint32_t smem_bytes();
+static_assert(1024 + 5 * (16384 + 16384) + 4 * 3 * 4096 + 256 <= 232448, "FINAL (2-CTA) exceeds smem");
+static_assert(1024 + 3 * (16384 + 32768) + 4 * 3 * 4096 + 256 <= 232448, "FINAL (1-CTA) exceeds smem");
 template <int MODE, int CG>
 constexpr uint32_t smem_bytes() {
   // [1 KiB align][stage ring][FINAL staging][barriers 256 B]
