@@ -286,7 +286,14 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
     if (nccl_uid == nullptr) return osh::fail(OSH_ERR_ARG, "nccl_uid required for dp_size > 1");
     ncclUniqueId id;
     std::memcpy(&id, nccl_uid, sizeof(id));
-    OSH_NCCL_TRY(ncclCommInitRank(&ctx->comm, dp_size, id, dp_rank));
+    // OSH_NCCL_MAX_CTAS caps the SMs NCCL's kernels may take from the
+    // persistent GEMMs they overlap (NCCL collective path / TP path)
+    ncclConfig_t config = NCCL_CONFIG_INITIALIZER;
+    if (const char* mc = std::getenv("OSH_NCCL_MAX_CTAS"); mc != nullptr && std::atoi(mc) > 0)
+      config.maxCTAs = std::atoi(mc);
+    if (const char* cp = std::getenv("OSH_NCCL_CTA_POLICY"); cp != nullptr)
+      config.CTAPolicy = std::atoi(cp);  // NCCL_CTA_POLICY_{DEFAULT,EFFICIENCY,ZERO}
+    OSH_NCCL_TRY(ncclCommInitRankConfig(&ctx->comm, dp_size, id, dp_rank, &config));
   }
   ctx->tp_rank = tp_rank;
   ctx->tp_size = tp_size;
@@ -294,7 +301,12 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
     if (tp_uid == nullptr) return osh::fail(OSH_ERR_ARG, "tp_uid required for tp_size > 1");
     ncclUniqueId id;
     std::memcpy(&id, tp_uid, sizeof(id));
-    OSH_NCCL_TRY(ncclCommInitRank(&ctx->tp_comm, tp_size, id, tp_rank));
+    ncclConfig_t config = NCCL_CONFIG_INITIALIZER;
+    if (const char* mc = std::getenv("OSH_NCCL_MAX_CTAS"); mc != nullptr && std::atoi(mc) > 0)
+      config.maxCTAs = std::atoi(mc);
+    if (const char* cp = std::getenv("OSH_NCCL_CTA_POLICY"); cp != nullptr)
+      config.CTAPolicy = std::atoi(cp);
+    OSH_NCCL_TRY(ncclCommInitRankConfig(&ctx->tp_comm, tp_size, id, tp_rank, &config));
     OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->tp_stream, cudaStreamNonBlocking));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_start_ev, cudaEventDisableTiming));
     OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->tp_done_ev, cudaEventDisableTiming));
