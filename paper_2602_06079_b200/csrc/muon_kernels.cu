@@ -13,8 +13,36 @@ using namespace ew;
 // One 64x64 tile of one matrix per CTA; 256 threads = 8 rows x 32 columns
 // per pass, so every global access is a coalesced 128-byte (fp32) or
 // 64-byte (bf16) warp transaction.
+#ifndef OSH_MOM_MINB
+#define OSH_MOM_MINB 4
+#endif
+#ifndef OSH_MOM_STREAM
+#define OSH_MOM_STREAM 1
+#endif
+// streaming (read-once / write-once) accesses of the momentum pass
+__device__ __forceinline__ void load_f8_stream(const float* p, float (&v)[8]) {
+#if OSH_MOM_STREAM
+  // one 256-bit load (sm_100) per 8 values, evicted first from L2
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+                 "=f"(v[7])
+               : "l"(p));
+#else
+  load_f8(p, v);
+#endif
+}
+__device__ __forceinline__ void store_f8_stream(float* p, const float (&v)[8]) {
+#if OSH_MOM_STREAM
+  asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+#else
+  store_f8(p, v);
+#endif
+}
+
 template <typename G>
-__global__ void __launch_bounds__(256, 4) momentum_matrix_kernel(const MomentumMatrixTask* tasks,
+__global__ void __launch_bounds__(256, OSH_MOM_MINB) momentum_matrix_kernel(const MomentumMatrixTask* tasks,
                                                               int n_tasks, float beta) {
   __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
   __shared__ double red[8];
@@ -51,7 +79,7 @@ __global__ void __launch_bounds__(256, 4) momentum_matrix_kernel(const MomentumM
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h)
-      if (ok[h]) load_f8(T.m + static_cast<size_t>(r0 + rr + 32 * h) * T.cols + c0 + c8, mv[h]);
+      if (ok[h]) load_f8_stream(T.m + static_cast<size_t>(r0 + rr + 32 * h) * T.cols + c0 + c8, mv[h]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int lr = rr + 32 * h;
@@ -65,7 +93,7 @@ __global__ void __launch_bounds__(256, 4) momentum_matrix_kernel(const MomentumM
           sq += mv[h][q] * mv[h][q];
           xv[q] = mv[h][q];
         }
-        store_f8(T.m + idx, mv[h]);
+        store_f8_stream(T.m + idx, mv[h]);
         if (!T.transposed)
           *reinterpret_cast<uint4*>(T.x0 + static_cast<size_t>(row) * T.ldx + col) = pack_bf16x8(xv);
       } else {
