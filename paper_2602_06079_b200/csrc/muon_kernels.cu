@@ -305,6 +305,36 @@ __global__ void __launch_bounds__(256) mc_copy_kernel(const McCopyTask* tasks, i
   __threadfence_system();  // the multicast stores land before the step's end barrier
 }
 
+template <typename G>
+__global__ void __launch_bounds__(256) mc_reduce_kernel(const McReduceTask* tasks, int n_tasks,
+                                                        long long total_vecs) {
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < total_vecs; v += 256ll * gridDim.x) {
+    int lo = 0, hi = n_tasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tasks[mid].vec_start <= v) lo = mid;
+      else hi = mid - 1;
+    }
+    const McReduceTask& T = tasks[lo];
+    const size_t i = 8 * static_cast<size_t>(v - T.vec_start);
+    float x[8];
+    mc_load_grad8<G>(T.mc, i, x);
+    G* d = static_cast<G*>(T.dst) + i;
+    if constexpr (sizeof(G) == 2) {
+      // (the switch returned bf16 already: the conversion back is exact)
+      uint4 u;
+      u.x = (__float_as_uint(x[0]) >> 16) | (__float_as_uint(x[1]) & 0xFFFF0000u);
+      u.y = (__float_as_uint(x[2]) >> 16) | (__float_as_uint(x[3]) & 0xFFFF0000u);
+      u.z = (__float_as_uint(x[4]) >> 16) | (__float_as_uint(x[5]) & 0xFFFF0000u);
+      u.w = (__float_as_uint(x[6]) >> 16) | (__float_as_uint(x[7]) & 0xFFFF0000u);
+      *reinterpret_cast<uint4*>(d) = u;
+    } else {
+      reinterpret_cast<float4*>(d)[0] = make_float4(x[0], x[1], x[2], x[3]);
+      reinterpret_cast<float4*>(d)[1] = make_float4(x[4], x[5], x[6], x[7]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) partial_sums_kernel(const double* partial,
                                                            const long long* begin,
                                                            const int* count, const int* target,
@@ -432,6 +462,21 @@ cudaError_t launch_mc_copy(const McCopyTask* d_tasks, int n_tasks, long long tot
   if (n_tasks == 0 || total_vecs == 0) return cudaSuccess;
   const long long blocks = std::min<long long>((total_vecs + 255) / 256, 148ll * 8);
   mc_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_tasks, n_tasks, total_vecs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mc_reduce(const McReduceTask* d_tasks, int n_tasks, long long total_vecs,
+                             int grad_bf16, cudaStream_t s) {
+  if (n_tasks == 0 || total_vecs == 0) return cudaSuccess;
+  // 2 CTAs per SM keep enough multicast loads in flight for the NVLink rate
+  // while leaving the SMs to the DP waves' kernels running beside it
+  const long long blocks = std::min<long long>((total_vecs + 255) / 256, 148ll * 2);
+  if (grad_bf16)
+    mc_reduce_kernel<__nv_bfloat16><<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_tasks, n_tasks,
+                                                                                  total_vecs);
+  else
+    mc_reduce_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_tasks, n_tasks,
+                                                                          total_vecs);
   return cudaGetLastError();
 }
 

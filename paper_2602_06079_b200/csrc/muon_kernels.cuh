@@ -90,6 +90,21 @@ struct McCopyTask {
 cudaError_t launch_mc_copy(const McCopyTask* d_tasks, int n_tasks, long long total_vecs,
                            cudaStream_t s);
 
+// NVLS + TP: the DP owner's reduced gradient shard of a TP-plane tensor is
+// read through the multicast address (the switch sums the DP group's
+// gradients) and written over the owner's own local copy, which the TP
+// gather then sends to the tensor's host. Only the owner reads its slice, so
+// overwriting it in place is race-free; the step's end barrier keeps the
+// peers' copies alive until then.
+struct McReduceTask {
+  const void* mc;            // multicast address of the slice
+  void* dst;                 // the same slice in the local gradient buffer
+  long long n;               // elements (multiple of 8)
+  long long vec_start;       // first 8-element vector of this task (prefix sum)
+};
+cudaError_t launch_mc_reduce(const McReduceTask* d_tasks, int n_tasks, long long total_vecs,
+                             int grad_bf16, cudaStream_t s);
+
 struct CopyTask {
   const uint16_t* src;
   uint16_t* dst;

@@ -282,6 +282,8 @@ osh_status osh_ctx_create_tp(int32_t device, int32_t dp_rank, int32_t dp_size, i
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
   OSH_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
   for (cudaEvent_t& e : ctx->ev) OSH_CUDA_TRY(cudaEventCreate(&e));
+  for (cudaEvent_t& e : ctx->seq_pre_ev) OSH_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  OSH_CUDA_TRY(cudaEventCreateWithFlags(&ctx->seq_ns_ev, cudaEventDisableTiming));
   if (comm_mode == OSH_COMM_NCCL && dp_size > 1) {
     if (nccl_uid == nullptr) return osh::fail(OSH_ERR_ARG, "nccl_uid required for dp_size > 1");
     ncclUniqueId id;
@@ -407,6 +409,8 @@ osh_status osh_ctx_destroy(osh_ctx* ctx) {
     cudaEventDestroy(ctx->tp_end_ev);
   }
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->seq_pre_ev) cudaEventDestroy(e);
+  if (ctx->seq_ns_ev != nullptr) cudaEventDestroy(ctx->seq_ns_ev);
   cudaStreamDestroy(ctx->compute);
   cudaStreamDestroy(ctx->comm_stream);
   cudaStreamDestroy(ctx->gemm_stream);
@@ -556,7 +560,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   const size_t es = grad_esize(grad_dtype);
   // NVLS needs every tensor on the 16-byte vector layout (decided from the
   // model alone, so every rank takes the same branch of the collective setup)
-  bool nvls_layout = distributed(ctx) && ctx->tp_size == 1 && ctx->strategy == OSH_STRAT_SHARDED;
+  bool nvls_layout = distributed(ctx) && ctx->strategy == OSH_STRAT_SHARDED;
   for (size_t p = 0; p < ctx->params.size() && nvls_layout; ++p) {
     const ParamSpec& ps = ctx->params[p];
     const int64_t inner = ps.is_matrix() ? ps.shape[1] : ps.numel;
@@ -564,7 +568,7 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   }
   if (ctx->coll_mode == OSH_COLL_NVLS && !nvls_layout)
     return osh::fail(OSH_ERR_UNSUPPORTED,
-                     "NVLS collectives need dp_size > 1, tp_size == 1 and 8-element aligned tensors");
+                     "NVLS collectives need dp_size > 1 and 8-element aligned tensors");
   if (nvls_layout && ctx->coll_mode != OSH_COLL_NCCL) {
     constexpr size_t kGran = 2u << 20;
     const size_t gb = (es * static_cast<size_t>(ctx->total_numel) + kGran - 1) / kGran * kGran;
@@ -650,7 +654,19 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   else
     ctx->engine = std::make_unique<osh::MuonEngine>();
   const char* ov = std::getenv("OSH_OVERLAP");
-  ctx->overlap = ctx->tp_size == 1 && !reduce_out && !(ov != nullptr && std::strcmp(ov, "0") == 0);
+  const bool overlap_on = !(ov != nullptr && std::strcmp(ov, "0") == 0);
+  // run_waves_local's schedule (one rank, NVLS, SC / NV-layerwise), or the
+  // stage sequence of the NCCL RS-v / AG-v and TP paths (Muon: split phases)
+  const bool seq_path = (distributed(ctx) && ctx->strategy == OSH_STRAT_SHARDED && !ctx->nvls) ||
+                        ctx->tp_size > 1;
+  ctx->overlap = ctx->tp_size == 1 && !reduce_out && overlap_on;
+  // (opt-in, OSH_SEQ_OVERLAP=1: measured neutral to slightly slower on these
+  // paths — their momentum reads local HBM at full rate and, under the power
+  // cap, slows the GEMMs beside it by as much as it hides; profiles/
+  // r02_seq_overlap_ab.json)
+  const char* so = std::getenv("OSH_SEQ_OVERLAP");
+  ctx->seq_overlap = seq_path && overlap_on && ctx->optimizer == OSH_OPT_MUON &&
+                     so != nullptr && std::strcmp(so, "1") == 0;
   int min_waves = ctx->min_waves > 0 ? ctx->min_waves
                   : ctx->overlap ? 8 : (reduce_out && ctx->tp_size == 1) ? 4 : 1;
   if (const char* mw = std::getenv("OSH_MIN_WAVES"); mw != nullptr && std::atoi(mw) > 0)
@@ -662,7 +678,8 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   const bool reorder = ctx->tp_size == 1 && ctx->strategy == OSH_STRAT_SHARDED &&
                        (!distributed(ctx) || ctx->nvls) && !(ro != nullptr && std::strcmp(ro, "0") == 0);
   ctx->engine->set_wave_reorder(reorder);
-  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves, ctx->overlap);
+  if (osh_status st = ctx->engine->build(tensors, grad_dtype, budget, min_waves,
+                                         ctx->overlap || ctx->seq_overlap);
       st != OSH_OK)
     return st;
   {
@@ -1039,6 +1056,64 @@ osh_status run_waves_local(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t c
 
 }  // namespace
 
+extern "C++" {  // (a template inside the C-ABI block)
+namespace {
+
+// One stage of the NCCL / TP step: wave `w` of engine `eng` (the DP engine,
+// group -1, or micro group `group`'s engine).
+struct Stage {
+  osh::OptimizerEngine* eng;
+  int w, group;
+};
+
+// Runs `stages` on cs in order, `before(i)` ahead of stage i's momentum and
+// `after(i)` behind its weight update. Overlapped (ctx->seq_overlap): the
+// momentum of stage i+1 runs on cs beside the Newton-Schulz GEMMs of stage i
+// on the high-priority gemm stream, as run_waves_local does — across engines
+// always, within one engine only when it double-buffers its workspace.
+template <typename Before, typename After>
+osh_status run_stages(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs,
+                      const std::vector<Stage>& stages, Before&& before, After&& after) {
+  const int n = static_cast<int>(stages.size());
+  if (!ctx->seq_overlap) {
+    for (int i = 0; i < n; ++i) {
+      if (osh_status st = before(i); st != OSH_OK) return st;
+      if (osh_status st = stages[i].eng->run_wave(stages[i].w, cfg, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaGetLastError());
+      if (osh_status st = after(i); st != OSH_OK) return st;
+    }
+    return OSH_OK;
+  }
+  cudaStream_t gs = ctx->gemm_stream;
+  auto pre = [&](int i) -> osh_status {
+    if (osh_status st = before(i); st != OSH_OK) return st;
+    if (osh_status st = stages[i].eng->run_pre(stages[i].w, cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->seq_pre_ev[i & 1], cs));
+    return OSH_OK;
+  };
+  if (n > 0)
+    if (osh_status st = pre(0); st != OSH_OK) return st;
+  for (int i = 0; i < n; ++i) {
+    const Stage& s = stages[static_cast<size_t>(i)];
+    const bool early = i + 1 < n && (stages[i + 1].eng != s.eng || s.eng->double_buffered());
+    if (early)
+      if (osh_status st = pre(i + 1); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaStreamWaitEvent(gs, ctx->seq_pre_ev[i & 1], 0));
+    if (osh_status st = s.eng->run_ns(s.w, cfg, gs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->seq_ns_ev, gs));
+    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->seq_ns_ev, 0));
+    if (osh_status st = s.eng->run_post(s.w, cfg, cs); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaGetLastError());
+    if (osh_status st = after(i); st != OSH_OK) return st;
+    if (i + 1 < n && !early)
+      if (osh_status st = pre(i + 1); st != OSH_OK) return st;
+  }
+  return OSH_OK;
+}
+
+}  // namespace
+}  // extern "C++"
+
 osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grads,
                     void* host_replica_out) {
   if (osh_status st = check_ctx(ctx, true); st != OSH_OK) return st;
@@ -1109,6 +1184,82 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   osh::OptimizerEngine& eng = *ctx->engine;
   const int nw = eng.num_waves();
   if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
+  auto all_gather = [&](int b) -> osh_status {
+    // AG-v of bucket b: every owner broadcasts its updated bf16 slice.
+    const auto [o0, o1] = ctx->sched_ag[static_cast<size_t>(b)];
+    if (osh_status st = osh::issue_ops(ctx, o0, o1, ns); st != OSH_OK) return st;
+    OSH_CUDA_TRY(cudaEventRecord(ctx->ag_ev[b], ns));
+    return d2h_buckets(ctx, io, b, ctx->ag_ev[b]);
+  };
+  int ag_next = 0;
+  ctx->last_seq = false;
+  // The stage sequence (NCCL RS-v / AG-v path and TP): this rank's DP waves
+  // (bucket order), then the micro groups' waves. Hooks around each stage
+  // wait for its inputs and release its outputs: a DP wave waits for the RS-v
+  // of its buckets and releases the AG-v of the buckets it completes; a micro
+  // group waits for its gather and, after its last wave, packs and scatters.
+  // (NVLS + TP: no RS-v / AG-v legs, the step barriers bracket the sequence.)
+  auto run_seq = [&]() -> osh_status {
+    std::vector<Stage> stages;
+    for (int w = 0; w < nw; ++w) stages.push_back(Stage{&eng, w, -1});
+    for (int g = 0; g < ctx->tp_groups; ++g)
+      for (int w = 0; w < ctx->tp_engines[g]->num_waves(); ++w)
+        stages.push_back(Stage{ctx->tp_engines[g].get(), w, g});
+    if (ctx->tp_size > 1 && nw == 0) OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));
+    auto before = [&](int i) -> osh_status {
+      const Stage& s = stages[static_cast<size_t>(i)];
+      if (s.group < 0) {
+        for (int b = eng.wave_first_bucket(s.w); b <= eng.wave_last_bucket(s.w); ++b) {
+          if (dist && !ctx->nvls) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
+          else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
+        }
+        OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[s.w], cs));
+      } else if (s.w == 0) {
+        if (s.group == 0) OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
+        if (osh_status st = osh::tp_group_begin(ctx, s.group, cs); st != OSH_OK) return st;
+      }
+      if (i == 0) OSH_CUDA_TRY(cudaEventRecord(ctx->ev[7], cs));
+      return OSH_OK;
+    };
+    auto after = [&](int i) -> osh_status {
+      const Stage& s = stages[static_cast<size_t>(i)];
+      if (s.group < 0) {
+        OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[s.w], cs));
+        if (dist && !ctx->nvls && ctx->tp_size == 1) {
+          // buckets no later wave of this rank touches are final on this rank
+          const int done = s.w + 1 < nw ? eng.wave_first_bucket(s.w + 1) - 1 : nb - 1;
+          if (done >= ag_next) {
+            OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[s.w], 0));
+            for (; ag_next <= done; ++ag_next)
+              if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+          }
+        }
+        if (ctx->tp_size > 1 && s.w + 1 == nw)  // every DP (non-TP-plane) wave is done
+          OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));
+      } else if (s.w + 1 == s.eng->num_waves()) {
+        if (osh_status st = osh::tp_group_end(ctx, s.group, cs); st != OSH_OK) return st;
+      }
+      return OSH_OK;
+    };
+    if (osh_status st = run_stages(ctx, *cfg, cs, stages, before, after); st != OSH_OK) return st;
+    ctx->last_seq = true;
+    if (ctx->tp_size > 1) {
+      if (osh_status st = osh::tp_finish(ctx, cs); st != OSH_OK) return st;
+      OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
+      if (dist && !ctx->nvls) {
+        // AG-v per bucket, in bucket order on every rank, as soon as the DP
+        // waves and the last micro group with a TP item in the bucket have
+        // scattered — overlapping the remaining groups' Newton-Schulz
+        OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[1], 0));
+        for (; ag_next < nb; ++ag_next) {
+          const int g = ctx->tp_bucket_group[static_cast<size_t>(ag_next)];
+          if (g >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->tp_scatter_ev[g], 0));
+          if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
+        }
+      }
+    }
+    return OSH_OK;
+  };
   if (ctx->nvls) {
     // barrier -> waves (reduce / broadcast inside the kernels) -> barrier.
     // With host buffers the barriers go per bucket on the comm stream: bucket b
@@ -1119,7 +1270,8 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       return OSH_OK;
     };
     HostIo nvls_io;
-    const bool pipe_in = host_grads != nullptr && !marked;
+    const bool tp = ctx->tp_size > 1;  // (TP: whole-buffer host copies)
+    const bool pipe_in = host_grads != nullptr && !marked && !tp;
     if (pipe_in) {
       OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev[5], 0));
       OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[5], 0));
@@ -1144,19 +1296,32 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       if (osh_status st = barrier(cs); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaEventRecord(ctx->rs_ev.back(), cs));
     }
-    if (host_replica_out != nullptr) {
+    if (host_replica_out != nullptr && !tp) {
       nvls_io.replica_out = host_replica_out;
       nvls_io.nvls_out = true;
       OSH_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev[5], 0));
     }
-    if (osh_status st = run_waves_local(ctx, *cfg, cs, nvls_io); st != OSH_OK) return st;
+    if (tp) {
+      // TP-plane shards: reduced through the multicast address into the
+      // owner's local copy, then gathered to the hosts (TP stream), while the
+      // DP waves run; each group's scattered shards are re-stored through the
+      // replica's multicast address (AG-v) on the TP stream
+      if (osh_status st = osh::tp_gather(ctx, {ctx->rs_ev.back()}); st != OSH_OK) return st;
+      if (osh_status st = run_seq(); st != OSH_OK) return st;
+    } else if (osh_status st = run_waves_local(ctx, *cfg, cs, nvls_io); st != OSH_OK) {
+      return st;
+    }
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
     // end barrier on the comm stream (after any per-bucket barriers there)
     OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[2], 0));
     if (osh_status st = barrier(ns); st != OSH_OK) return st;
     OSH_CUDA_TRY(cudaEventRecord(ctx->ev[3], ns));
     OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[3], 0));
-    if (host_replica_out != nullptr) {
+    if (host_replica_out != nullptr && tp) {
+      OSH_CUDA_TRY(cudaMemcpyAsync(host_replica_out, ctx->replica,
+                                   2 * static_cast<size_t>(ctx->total_numel),
+                                   cudaMemcpyDeviceToHost, cs));
+    } else if (host_replica_out != nullptr) {
       if (osh_status st = d2h_buckets(ctx, nvls_io, nb - 1, ctx->ev[3]); st != OSH_OK) return st;
       OSH_CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->d2h_stream));
       OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[6], 0));
@@ -1167,6 +1332,11 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
     ctx->last_timing.gemm_launches = s.launches_gemm;
     ctx->last_timing.elementwise_launches = s.launches_elementwise;
     ctx->last_timing.gemm_flops = s.gemm_flops;
+    for (const auto& e : ctx->tp_engines) {
+      ctx->last_timing.gemm_launches += e->stats().launches_gemm;
+      ctx->last_timing.elementwise_launches += e->stats().launches_elementwise;
+      ctx->last_timing.gemm_flops += e->stats().gemm_flops;
+    }
     if (host_replica_out != nullptr) return osh::wait_stream(ctx, cs);
     return OSH_OK;
   }
@@ -1226,14 +1396,6 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
       if (osh_status st = osh::issue_rs(ctx, b); st != OSH_OK) return st;
     }
   }
-  auto all_gather = [&](int b) -> osh_status {
-    // AG-v of bucket b: every owner broadcasts its updated bf16 slice.
-    const auto [o0, o1] = ctx->sched_ag[static_cast<size_t>(b)];
-    if (osh_status st = osh::issue_ops(ctx, o0, o1, ns); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaEventRecord(ctx->ag_ev[b], ns));
-    return d2h_buckets(ctx, io, b, ctx->ag_ev[b]);
-  };
-  int ag_next = 0;
   if (ctx->tp_size > 1) {
     // micro-group gathers need every reduced shard of the TP plane: they go
     // out on the TP stream once the whole reduce-scatter (or H2D) landed,
@@ -1247,42 +1409,7 @@ osh_status osh_step(osh_ctx* ctx, const osh_muon_cfg* cfg, const void* host_grad
   if (!dist && ctx->tp_size == 1) {
     if (osh_status st = run_waves_local(ctx, *cfg, cs, io); st != OSH_OK) return st;
   } else {
-    for (int w = 0; w < nw; ++w) {
-      for (int b = eng.wave_first_bucket(w); b <= eng.wave_last_bucket(w); ++b) {
-        if (dist) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->rs_ev[b], 0));
-        else if (io.h2d) OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->h2d_ev[b], 0));
-      }
-      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_begin[w], cs));
-      if (osh_status st = eng.run_wave(w, *cfg, cs); st != OSH_OK) return st;
-      OSH_CUDA_TRY(cudaGetLastError());
-      OSH_CUDA_TRY(cudaEventRecord(ctx->wave_end[w], cs));
-      if (dist && ctx->tp_size == 1) {
-        // buckets no later wave of this rank touches are final on this rank
-        const int done = w + 1 < nw ? eng.wave_first_bucket(w + 1) - 1 : nb - 1;
-        if (done >= ag_next) {
-          OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->wave_end[w], 0));
-          for (; ag_next <= done; ++ag_next)
-            if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
-        }
-      }
-    }
-  }
-  if (ctx->tp_size > 1) {
-    OSH_CUDA_TRY(cudaEventRecord(ctx->ev[1], cs));  // every DP (non-TP-plane) wave is done
-    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_begin_ev, cs));
-    if (osh_status st = osh::tp_compute(ctx, *cfg, cs); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_end_ev, cs));
-    if (dist) {
-      // AG-v per bucket, in bucket order on every rank, as soon as the DP
-      // waves and the last micro group with a TP item in the bucket have
-      // scattered — overlapping the remaining groups' Newton-Schulz
-      OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->ev[1], 0));
-      for (; ag_next < nb; ++ag_next) {
-        const int g = ctx->tp_bucket_group[static_cast<size_t>(ag_next)];
-        if (g >= 0) OSH_CUDA_TRY(cudaStreamWaitEvent(ns, ctx->tp_scatter_ev[g], 0));
-        if (osh_status st = all_gather(ag_next); st != OSH_OK) return st;
-      }
-    }
+    if (osh_status st = run_seq(); st != OSH_OK) return st;
   }
   OSH_CUDA_TRY(cudaEventRecord(ctx->ev[2], cs));
   if (dist) {
@@ -1439,13 +1566,19 @@ osh_status osh_last_timing(osh_ctx* ctx, osh_step_timing* out) {
   const bool dist = distributed(ctx);
   t.rs_ms = dist && !ctx->rs_ev.empty() ? span(ctx->ev[0], ctx->rs_ev.back()) : 0.f;
   t.compute_ms = 0.f;  // busy time of the waves (excludes waiting for the RS)
-  if (ctx->overlap && !ctx->wave_begin.empty())
-    t.compute_ms = span(ctx->wave_begin.front(), ctx->wave_end.back());
-  else
-    for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
-      t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
-  if (ctx->tp_size > 1 && ctx->tp_begin_ev != nullptr)  // + the micro groups (gathers overlap the waves)
-    t.compute_ms += span(ctx->tp_begin_ev, ctx->tp_end_ev);
+  if (ctx->last_seq && ctx->seq_overlap) {  // first stage start -> last stage end
+    cudaEvent_t end = ctx->tp_size > 1 ? ctx->tp_end_ev
+                      : !ctx->wave_end.empty() ? ctx->wave_end.back() : ctx->ev[7];
+    t.compute_ms = span(ctx->ev[7], end);
+  } else {
+    if (ctx->overlap && !ctx->last_seq && !ctx->wave_begin.empty())
+      t.compute_ms = span(ctx->wave_begin.front(), ctx->wave_end.back());
+    else
+      for (size_t w = 0; w < ctx->wave_begin.size(); ++w)
+        t.compute_ms += span(ctx->wave_begin[w], ctx->wave_end[w]);
+    if (ctx->tp_size > 1 && ctx->tp_begin_ev != nullptr)  // + the micro groups (gathers overlap the waves)
+      t.compute_ms += span(ctx->tp_begin_ev, ctx->tp_end_ev);
+  }
   t.ag_ms = ms(2, 3);  // all-gather tail exposed after the last wave
   t.d2h_ms = ms(3, 4);
   t.total_ms = ms(5, 4);

@@ -79,6 +79,13 @@ struct osh_ctx {
   // high-priority gemm_stream (double-buffered NS workspace)
   bool overlap = false;
   std::vector<cudaEvent_t> pre_ev, ns_ev;  // per wave
+  // the same overlap for the NCCL RS-v / AG-v path and the TP path, over the
+  // stage sequence DP waves -> micro-group waves (osh_step run_stages):
+  // momentum of stage i+1 beside the GEMMs of stage i; ev[7] marks the first
+  // stage's start (compute_ms = ev[7] -> tp_end_ev / last wave_end)
+  bool seq_overlap = false;
+  bool last_seq = false;                 // the last step ran the stage sequence
+  cudaEvent_t seq_pre_ev[2] = {}, seq_ns_ev = nullptr;
   // waves may run out of bucket order (single rank / NVLS, MuonEngine
   // set_wave_reorder): per wave, the last bucket index B such that every
   // bucket <= B is final once the wave is done; and the order in which a
@@ -150,6 +157,13 @@ struct osh_ctx {
   std::vector<std::vector<osh::CopyTask>> tp_unpack, tp_pack;  // per group (host side)
   std::vector<osh::CopyTask*> d_tp_unpack, d_tp_pack;
   std::vector<long long> tp_unpack_tiles, tp_pack_tiles;
+  // NVLS + TP, per group: my shards of its items, reduced through the
+  // multicast gradient before the gather / re-stored through the multicast
+  // replica after the scatter (same regions, same vector counts)
+  std::vector<osh::McReduceTask*> d_tp_mc_reduce;
+  std::vector<osh::McCopyTask*> d_tp_mc_copy;
+  std::vector<int> tp_mc_tasks;
+  std::vector<long long> tp_mc_vecs;
 };
 
 namespace osh {
@@ -159,7 +173,13 @@ osh_status tp_setup(osh_ctx* ctx, int64_t workspace_budget);
 // before the DP waves so the gathers overlap them; tp_compute (on cs) runs
 // each group's full-matrix Muon after its gather, then packs and scatters.
 osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready);
-osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs);
+// Per micro group g on cs: tp_group_begin (wait for gather g, unpack the
+// full gradients, engine begin_step) before its first wave's momentum;
+// tp_group_end (pack the result shards, scatter them on the TP stream) after
+// its last wave; tp_finish joins the TP stream back into cs.
+osh_status tp_group_begin(osh_ctx* ctx, int g, cudaStream_t cs);
+osh_status tp_group_end(osh_ctx* ctx, int g, cudaStream_t cs);
+osh_status tp_finish(osh_ctx* ctx, cudaStream_t cs);
 osh_status tp_refresh_replica(osh_ctx* ctx, cudaStream_t cs);  // checkpoint resume
 void tp_free(osh_ctx* ctx);
 void* grad_ptr(osh_ctx* ctx, int pid);

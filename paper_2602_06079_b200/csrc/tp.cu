@@ -4,14 +4,16 @@
 // chosen by build_micro_groups (tp_schedule.hpp:90-131) over the items my DP
 // rank owns; the host keeps that tensor's full fp32 master + momentum. Per
 // micro group, in plan order:
-//   gather : every TP rank sends its reduced-gradient shard to the host
+//   gather : every TP rank sends its reduced-gradient shard to the host (NVLS:
+//            first reduced in place through the DP multicast gradient)
 //            (row splits land in place; column splits via a staging block)
 //   compute: the host runs the full-matrix Muon update (MuonEngine: momentum,
 //            5 Newton-Schulz iterations on tcgen05, weight update)
 //   scatter: the host sends each TP rank its updated bf16 shard, which lands
 //            in that rank's replica slot (the DP all-gather then spreads it)
-// All TP traffic is NCCL send/recv on the TP communicator, issued on the
-// compute stream so it is ordered with the kernels that produce/consume it.
+//            (NVLS: re-stored through the DP multicast replica)
+// All TP traffic is NCCL send/recv on the TP communicator, issued on the TP
+// stream and ordered by events with the kernels that produce / consume it.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -134,6 +136,12 @@ void tp_free(osh_ctx* ctx) {
   ctx->tp_pack_ev.clear();
   ctx->tp_scatter_ev.clear();
   ctx->tp_bucket_group.clear();
+  for (McReduceTask* p : ctx->d_tp_mc_reduce) cudaFree(p);
+  for (McCopyTask* p : ctx->d_tp_mc_copy) cudaFree(p);
+  ctx->d_tp_mc_reduce.clear();
+  ctx->d_tp_mc_copy.clear();
+  ctx->tp_mc_tasks.clear();
+  ctx->tp_mc_vecs.clear();
   for (CopyTask* p : ctx->d_tp_unpack) cudaFree(p);
   for (CopyTask* p : ctx->d_tp_pack) cudaFree(p);
   ctx->d_tp_unpack.clear();
@@ -257,7 +265,8 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
     finalize_tiles(ctx->tp_unpack[g], &ctx->tp_unpack_tiles[g]);
     finalize_tiles(ctx->tp_pack[g], &ctx->tp_pack_tiles[g]);
     auto eng = std::make_unique<MuonEngine>();
-    if (osh_status st = eng->build(tensors, ctx->grad_dtype, static_cast<size_t>(budget), 1, false);
+    if (osh_status st = eng->build(tensors, ctx->grad_dtype, static_cast<size_t>(budget), 1,
+                                   ctx->seq_overlap);
         st != OSH_OK)
       return st;
     ctx->tp_engines.push_back(std::move(eng));
@@ -284,6 +293,31 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
     ctx->d_tp_unpack.push_back(u);
     ctx->d_tp_pack.push_back(p);
   }
+  if (ctx->nvls) {
+    // every TP rank of the owning DP rank holds one shard of each item, at
+    // the item's flat offset (8-element aligned: the NVLS layout check)
+    for (int g = 0; g < ctx->tp_groups; ++g) {
+      std::vector<McReduceTask> red;
+      std::vector<McCopyTask> cp;
+      long long vecs = 0;
+      for (const osh_ctx::TpItem& it : ctx->tp_items) {
+        if (it.group != g) continue;
+        const int64_t off = ctx->flat_off[it.pid], n = ctx->params[it.pid].numel;
+        red.push_back(McReduceTask{static_cast<const uint8_t*>(ctx->mc_grad) + es * static_cast<size_t>(off),
+                                   static_cast<uint8_t*>(ctx->grad) + es * static_cast<size_t>(off), n, vecs});
+        cp.push_back(McCopyTask{ctx->replica + off, ctx->mc_replica + off, n, vecs});
+        vecs += n / 8;
+      }
+      McReduceTask* dr = nullptr;
+      McCopyTask* dc = nullptr;
+      OSH_CUDA_TRY(upload_vec(&dr, red));
+      OSH_CUDA_TRY(upload_vec(&dc, cp));
+      ctx->d_tp_mc_reduce.push_back(dr);
+      ctx->d_tp_mc_copy.push_back(dc);
+      ctx->tp_mc_tasks.push_back(static_cast<int>(red.size()));
+      ctx->tp_mc_vecs.push_back(vecs);
+    }
+  }
   return OSH_OK;
 }
 
@@ -299,6 +333,9 @@ osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready) {
   cudaStream_t ts = ctx->tp_stream;
   for (cudaEvent_t e : ready) OSH_CUDA_TRY(cudaStreamWaitEvent(ts, e, 0));
   for (int g = 0; g < ctx->tp_groups; ++g) {
+    if (ctx->nvls)  // NVLS: my shards' DP sums first (in place, see McReduceTask)
+      OSH_CUDA_TRY(launch_mc_reduce(ctx->d_tp_mc_reduce[g], ctx->tp_mc_tasks[g], ctx->tp_mc_vecs[g],
+                                    ctx->grad_dtype == OSH_GRAD_BF16, ts));
     // ---- gather reduced-gradient shards to the hosts
     TP_NCCL(ncclGroupStart());
     for (osh_ctx::TpItem& it : ctx->tp_items) {
@@ -321,26 +358,29 @@ osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready) {
   return OSH_OK;
 }
 
-osh_status tp_compute(osh_ctx* ctx, const osh_muon_cfg& cfg, cudaStream_t cs) {
+osh_status tp_group_begin(osh_ctx* ctx, int g, cudaStream_t cs) {
+  OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
+  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
+                                  ctx->tp_unpack_tiles[g], cs));
+  return ctx->tp_engines[g]->begin_step(cs);  // the host's full-matrix Muon follows
+}
+
+osh_status tp_group_end(osh_ctx* ctx, int g, cudaStream_t cs) {
   cudaStream_t ts = ctx->tp_stream;
-  for (int g = 0; g < ctx->tp_groups; ++g) {
-    OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
-    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
-                                    ctx->tp_unpack_tiles[g], cs));
-    // ---- full-matrix Muon on the host
-    MuonEngine& eng = *ctx->tp_engines[g];
-    if (osh_status st = eng.begin_step(cs); st != OSH_OK) return st;
-    for (int w = 0; w < eng.num_waves(); ++w)
-      if (osh_status st = eng.run_wave(w, cfg, cs); st != OSH_OK) return st;
-    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
-                                    ctx->tp_pack_tiles[g], cs));
-    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
-    OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
-    // ---- scatter updated bf16 shards into every rank's replica slot
-    if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
-    OSH_CUDA_TRY(cudaEventRecord(ctx->tp_scatter_ev[g], ts));
-  }
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ts));
+  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
+                                  ctx->tp_pack_tiles[g], cs));
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
+  OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
+  // ---- scatter updated bf16 shards into every rank's replica slot
+  if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
+  if (ctx->nvls)  // AG-v of the group's shards: every DP peer's replica slot
+    OSH_CUDA_TRY(launch_mc_copy(ctx->d_tp_mc_copy[g], ctx->tp_mc_tasks[g], ctx->tp_mc_vecs[g], ts));
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_scatter_ev[g], ts));
+  return OSH_OK;
+}
+
+osh_status tp_finish(osh_ctx* ctx, cudaStream_t cs) {
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_done_ev, ctx->tp_stream));
   OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_done_ev, 0));
   return OSH_OK;
 }

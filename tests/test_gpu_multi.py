@@ -56,8 +56,15 @@ def test_tp2_micro_groups_match_oracle():
     _run(2, "multi_gpu_check_tp.py", 1, 2, 3)
 
 
-def test_dp2_tp2_micro_groups_match_oracle():
-    _run(4, "multi_gpu_check_tp.py", 2, 2, 3)
+@pytest.mark.parametrize("coll,gdt", [("auto", "f32"), ("nccl", "f32"), ("auto", "bf16")])
+def test_dp2_tp2_micro_groups_match_oracle(coll, gdt):
+    # auto = NVLS on NVSwitch boxes: TP-plane shards reduced through the
+    # multicast gradient before the gathers, scattered shards re-stored
+    # through the multicast replica; nccl = NCCL reduce / broadcast legs
+    res = _run(4, "multi_gpu_check_tp.py", 2, 2, 3, "-", coll, gdt)
+    if coll == "nccl":
+        assert res["collectives"] == "nccl"
+    assert res["grad_dtype"] == gdt
 
 
 def test_dp2_nccl_bucket_ready_matches_oracle():
@@ -128,8 +135,9 @@ def test_tp2_checkpoint_restores_replica():
     assert res["checkpoint_replica_ok"] is True
 
 
-def test_dp2_tp2_checkpoint_restores_replica():
-    res = _run(4, "multi_gpu_check_tp.py", 2, 2, 2, "ckpt")
+@pytest.mark.parametrize("coll", ["auto", "nccl"])
+def test_dp2_tp2_checkpoint_restores_replica(coll):
+    res = _run(4, "multi_gpu_check_tp.py", 2, 2, 2, "ckpt", coll)
     assert res["checkpoint_replica_ok"] is True
 
 
