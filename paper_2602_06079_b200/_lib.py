@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libosh.so")
+LIB_PATH = os.environ.get("OSH_LIB") or os.path.join(_HERE, "libosh.so")  # (OSH_LIB: A/B builds)
 
 
 class OshLibraryMissing(RuntimeError):

@@ -583,6 +583,24 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const int row = row_base + row_in_tile;
       const bool row_ok = row < pr.M;
       const float s = pr.scale != nullptr ? __ldg(pr.scale + c.b) : 1.f;
+      // POLY: the aux row segment (b·A) of the next chunk is loaded one chunk
+      // ahead — the first while waiting for the accumulator — so its L2/DRAM
+      // latency hides behind the TMEM loads and stores of the current chunk
+      uint4 ax_nxt[4];
+      bool ax_nxt_ok = false;
+      const __nv_bfloat16* ax_row =
+          MODE == kEpiPoly && pr.aux != nullptr ? pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld : nullptr;
+      auto ax_prefetch = [&](int chunk) {
+        const int col = c.tn * kNsBN + chunk * 32;
+        ax_nxt_ok = MODE == kEpiPoly && P.alpha != 0.f && row_ok && col + 32 <= pr.N &&
+                    ((reinterpret_cast<uintptr_t>(ax_row + col) & 15) == 0);
+        if (ax_nxt_ok) {
+          const uint4* s4 = reinterpret_cast<const uint4*>(ax_row + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ax_nxt[q] = __ldg(s4 + q);
+        }
+      };
+      if constexpr (MODE == kEpiPoly) ax_prefetch(0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kNsBN;
@@ -590,6 +608,14 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const int slot = (MODE == kEpiGram && sched && P.seg_slot != nullptr) ? __ldg(P.seg_slot + it) : -1;
 #pragma unroll 1
       for (int chunk = 0; chunk < kNsBN / 32; ++chunk) {
+        uint4 ax_cur[4];
+        bool ax_cur_ok = false;
+        if constexpr (MODE == kEpiPoly) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ax_cur[q] = ax_nxt[q];
+          ax_cur_ok = ax_nxt_ok;
+          if (chunk + 1 < kNsBN / 32) ax_prefetch(chunk + 1);
+        }
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + chunk * 32, r);
         tmem_ld_wait();
@@ -615,7 +641,19 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           else
             store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiPoly) {
-          if (P.alpha != 0.f)
+          if (ax_cur_ok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              v[q * 8 + 0] = bf16_lo(ax_cur[q].x);
+              v[q * 8 + 1] = bf16_hi(ax_cur[q].x);
+              v[q * 8 + 2] = bf16_lo(ax_cur[q].y);
+              v[q * 8 + 3] = bf16_hi(ax_cur[q].y);
+              v[q * 8 + 4] = bf16_lo(ax_cur[q].z);
+              v[q * 8 + 5] = bf16_hi(ax_cur[q].z);
+              v[q * 8 + 6] = bf16_lo(ax_cur[q].w);
+              v[q * 8 + 7] = bf16_hi(ax_cur[q].w);
+            }
+          } else if (P.alpha != 0.f)
             load_row32(pr.aux + c.b * pr.aux_bstride + row * pr.aux_ld + col0, col0, pr.N, v);
           else
 #pragma unroll
