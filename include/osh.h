@@ -179,7 +179,8 @@ typedef struct osh_gemm_problem {
   osh_matrix_ref aux; /* M x N bf16 */
   const float* scale; /* per batch, nullable */
   const osh_final_target* final_targets;
-  int32_t symmetric;  /* GRAM / POLY / STAT / SPLIT with M == N: upper-triangle tiles, mirror */
+  int32_t symmetric;  /* GRAM / POLY / STAT / SPLIT with M == N: upper-triangle tiles, mirror;
+                         2 (STAT only): upper triangle written, lower left untouched */
   int32_t out_seg;    /* OSH_EPI_SPLIT: segment width in elements (>= N) */
 } osh_gemm_problem;
 

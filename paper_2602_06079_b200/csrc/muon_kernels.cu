@@ -335,6 +335,35 @@ __global__ void __launch_bounds__(256) mc_reduce_kernel(const McReduceTask* task
   }
 }
 
+__global__ void __launch_bounds__(256) sym_fill_lower_kernel(const SymFillTask* tasks, int n_tasks) {
+  __shared__ float t[32][33];
+  const long long b = blockIdx.x;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const SymFillTask T = tasks[lo];
+  // lower-triangle tile (I, J), I >= J, from its index u = I (I + 1) / 2 + J
+  const int u = static_cast<int>(b - T.tile_start);
+  int I = static_cast<int>((sqrtf(8.f * u + 1.f) - 1.f) * 0.5f);
+  while (I * (I + 1) / 2 > u) --I;
+  while ((I + 1) * (I + 2) / 2 <= u) ++I;
+  const int J = u - I * (I + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // read the mirror tile (J, I) of the upper triangle, coalesced along its rows
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = J * 32 + r, gc = I * 32 + tx;
+    t[r][tx] = (gr < T.n && gc < T.n) ? T.s[static_cast<long long>(gr) * T.ld + gc] : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = I * 32 + r, gc = J * 32 + tx;
+    if (gr < T.n && gc < T.n && gr > gc) T.s[static_cast<long long>(gr) * T.ld + gc] = t[tx][r];
+  }
+}
+
 __global__ void __launch_bounds__(256) partial_sums_kernel(const double* partial,
                                                            const long long* begin,
                                                            const int* count, const int* target,
@@ -477,6 +506,14 @@ cudaError_t launch_mc_reduce(const McReduceTask* d_tasks, int n_tasks, long long
   else
     mc_reduce_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_tasks, n_tasks,
                                                                           total_vecs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sym_fill_lower(const SymFillTask* d_tasks, int n_tasks, long long total_tiles,
+                                  cudaStream_t s) {
+  if (n_tasks == 0 || total_tiles == 0) return cudaSuccess;
+  if (total_tiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  sym_fill_lower_kernel<<<static_cast<unsigned>(total_tiles), 256, 0, s>>>(d_tasks, n_tasks);
   return cudaGetLastError();
 }
 

@@ -105,6 +105,19 @@ struct McReduceTask {
 cudaError_t launch_mc_reduce(const McReduceTask* d_tasks, int n_tasks, long long total_vecs,
                              int grad_bf16, cudaStream_t s);
 
+// Completes symmetric fp32 matrices whose upper triangle alone is current
+// (STAT GEMMs with symmetric = 2): S[i][j] = S[j][i] for i > j, 32 x 32 tiles
+// of the lower triangle (diagonal tiles included), one CTA each.
+struct SymFillTask {
+  float* s;
+  long long ld;
+  int n;
+  int tiles;                 // T (T + 1) / 2, T = ceil(n / 32)
+  long long tile_start;      // prefix sum over the tasks
+};
+cudaError_t launch_sym_fill_lower(const SymFillTask* d_tasks, int n_tasks, long long total_tiles,
+                                  cudaStream_t s);
+
 struct CopyTask {
   const uint16_t* src;
   uint16_t* dst;

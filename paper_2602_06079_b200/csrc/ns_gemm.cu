@@ -601,6 +601,25 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         }
       };
       if constexpr (MODE == kEpiPoly) ax_prefetch(0);
+      // STAT read-modify-write (alpha != 0) of a plain or upper-only output:
+      // the old fp32 values of the next chunk are loaded one chunk ahead
+      float4 so_nxt[8];
+      bool so_nxt_ok = false;
+      float* so_row = MODE == kEpiStat && pr.out32 != nullptr
+                          ? pr.out32 + c.b * pr.out_bstride + row * pr.out_ld
+                          : nullptr;
+      auto so_prefetch = [&](int chunk) {
+        const int col = c.tn * kNsBN + chunk * 32;
+        so_nxt_ok = MODE == kEpiStat && P.alpha != 0.f && pr.symmetric != 1 && row_ok &&
+                    col + 32 <= pr.N && (pr.symmetric == 0 || col >= row) &&
+                    ((reinterpret_cast<uintptr_t>(so_row + col) & 15) == 0);
+        if (so_nxt_ok) {
+          const float4* s4 = reinterpret_cast<const float4*>(so_row + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) so_nxt[q] = s4[q];
+        }
+      };
+      if constexpr (MODE == kEpiStat) so_prefetch(0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kNsBN;
@@ -615,6 +634,14 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           for (int q = 0; q < 4; ++q) ax_cur[q] = ax_nxt[q];
           ax_cur_ok = ax_nxt_ok;
           if (chunk + 1 < kNsBN / 32) ax_prefetch(chunk + 1);
+        }
+        float4 so_cur[8];
+        bool so_cur_ok = false;
+        if constexpr (MODE == kEpiStat) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) so_cur[q] = so_nxt[q];
+          so_cur_ok = so_nxt_ok;
+          if (chunk + 1 < kNsBN / 32) so_prefetch(chunk + 1);
         }
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + chunk * 32, r);
@@ -683,10 +710,30 @@ __global__ void __launch_bounds__(kNsThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = s * __uint_as_float(r[j]);
           float* o = pr.out32 + c.b * pr.out_bstride;
-          if (pr.symmetric)
+          if (so_cur_ok) {  // whole chunk on or above the diagonal, old values in registers
+            float4* d4 = reinterpret_cast<float4*>(o + row * pr.out_ld + col0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              d4[q] = make_float4(P.alpha * so_cur[q].x + v[q * 4 + 0], P.alpha * so_cur[q].y + v[q * 4 + 1],
+                                  P.alpha * so_cur[q].z + v[q * 4 + 2], P.alpha * so_cur[q].w + v[q * 4 + 3]);
+          } else if (pr.symmetric == 1) {
             rmw_row32_sym(o, pr.out_ld, row, col0, pr.N, P.alpha, v);
-          else
+          } else if (pr.symmetric == 2) {
+            // upper triangle only (the owner fills the lower one before reading
+            // the whole matrix: launch_sym_fill_lower)
+            if (col0 >= row) {
+              rmw_row32(o + row * pr.out_ld + col0, col0, pr.N, P.alpha, v);
+            } else if (col0 + 31 >= row) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j >= row && col0 + j < pr.N) {
+                  float* p = o + row * pr.out_ld + col0 + j;
+                  *p = P.alpha == 0.f ? v[j] : P.alpha * *p + v[j];
+                }
+            }
+          } else {
             rmw_row32(o + row * pr.out_ld + col0, col0, pr.N, P.alpha, v);
+          }
         } else if constexpr (MODE == kEpiSplit) {
           float lo[32];
 #pragma unroll
@@ -1137,9 +1184,10 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     pr.symmetric = d.symmetric && pr.M == pr.N &&
                            (mode == kEpiGram || mode == kEpiPoly || mode == kEpiStat ||
                             mode == kEpiSplit)
-                       ? 1
+                       ? (d.symmetric == 2 ? 2 : 1)
                        : 0;
     if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
+    if (pr.symmetric == 2 && mode != kEpiStat) return cudaErrorInvalidValue;  // upper-only: STAT
     pr.tiles_per_batch =
         pr.symmetric ? sym_tiles(pr.tiles_m, pr.tiles_n, P.tile_m) : pr.tiles_m * pr.tiles_n;
     pr.tile_start = tiles;

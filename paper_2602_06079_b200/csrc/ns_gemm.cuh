@@ -71,7 +71,8 @@ struct alignas(64) NsGemmProblem {
   int batch, M, N, K;
   int b_mn_major;
   int symmetric;      // output is symmetric (M == N): only tiles touching the
-                      // upper triangle run; the epilogue mirrors them
+                      // upper triangle run; 1: the epilogue mirrors them,
+                      // 2 (STAT): it writes the upper triangle only
   int tiles_m, tiles_n;
   int tiles_per_batch;
   int tile_start;
@@ -119,7 +120,9 @@ struct NsProblemDesc {
   NsMatrixRef aux;      // M x N (bf16) or nullptr
   const float* scale;   // device, per batch
   const NsFinalTarget* final_targets;  // device, per batch
-  int symmetric = 0;    // GRAM / POLY / STAT / SPLIT: out = out^T, upper-triangle tiles only
+  int symmetric = 0;    // GRAM / POLY / STAT / SPLIT: out = out^T, upper-triangle tiles only;
+                        // 1: the epilogue mirrors them, 2 (STAT): upper triangle written
+                        // only — launch_sym_fill_lower completes the matrix before a reader
   long long out_seg = 0;  // kEpiSplit segment width (elements)
 };
 

@@ -74,6 +74,7 @@ void ShampooEngine::release() {
                   static_cast<void*>(d_root_), static_cast<void*>(d_newton_),
                   static_cast<void*>(d_extract_), static_cast<void*>(d_apply_),
                   static_cast<void*>(d_sgd_), static_cast<void*>(d_blockrefs_),
+                  static_cast<void*>(d_symf_),
                   static_cast<void*>(d_slot_begin_), static_cast<void*>(d_slot_count_),
                   static_cast<void*>(d_slot_target_)})
     cudaFree(p);
@@ -88,6 +89,7 @@ void ShampooEngine::release() {
   d_apply_ = nullptr;
   d_sgd_ = nullptr;
   d_blockrefs_ = nullptr;
+  d_symf_ = nullptr;
   d_slot_begin_ = nullptr;
   d_slot_count_ = d_slot_target_ = nullptr;
   waves_.clear();
@@ -149,6 +151,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
   std::vector<ShPrepTask> prep;
   std::vector<ShMatTask<__nv_bfloat16>> usq;
   std::vector<ShMatTask<float>> ssq;
+  std::vector<SymFillTask> symf;
   std::vector<ShRootTask> root;
   std::vector<ShNewtonTask> newton0, newton1, extract;
   std::vector<ShApplyTask> apply;
@@ -197,6 +200,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
     w.prep.first = static_cast<int>(prep.size());
     w.usq.first = static_cast<int>(usq.size());
     w.ssq.first = static_cast<int>(ssq.size());
+    w.symf.first = static_cast<int>(symf.size());
     w.root_init[0].first = static_cast<int>(root.size());
     w.newton[0].first = static_cast<int>(newton0.size());
     w.newton[1].first = static_cast<int>(newton1.size());
@@ -326,6 +330,17 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
           slot_target.push_back(stat);
           st += tiles_of(n, n);
           ssq.push_back(mt);
+          {
+            SymFillTask sf{};
+            sf.s = static_cast<float*>(off_ptr(S));
+            sf.ld = ldn;
+            sf.n = n;
+            const int T = (n + 31) / 32;
+            sf.tiles = T * (T + 1) / 2;
+            sf.tile_start = w.symf.tiles;
+            w.symf.tiles += sf.tiles;
+            symf.push_back(sf);
+          }
           ShRootTask r{};
           r.s = static_cast<const float*>(off_ptr(S));
           r.lds = ldn;
@@ -372,6 +387,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
       }
     }
     w.ssq.count = static_cast<int>(ssq.size()) - w.ssq.first;
+    w.symf.count = static_cast<int>(symf.size()) - w.symf.first;
     w.ssq.tiles = st;
     w.slot_s.count = static_cast<int>(slot_begin.size()) - w.slot_s.first;
     partial_off += static_cast<size_t>(st);
@@ -508,6 +524,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
     t.src = reinterpret_cast<const float*>(stp(t.src));
     t.partial = part(t.partial);
   }
+  for (auto& t : symf) t.s = reinterpret_cast<float*>(stp(t.s));
   for (auto& t : root) {
     t.s = reinterpret_cast<const float*>(stp(t.s));
     t.a5 = reinterpret_cast<__nv_bfloat16*>(ws(t.a5));
@@ -539,6 +556,7 @@ osh_status ShampooEngine::build(const std::vector<MuonTensorDesc>& tensors, int 
   OSH_CUDA_TRY(upload(&d_prep_, prep));
   OSH_CUDA_TRY(upload(&d_usq_tasks_, usq));
   OSH_CUDA_TRY(upload(&d_ssq_tasks_, ssq));
+  OSH_CUDA_TRY(upload(&d_symf_, symf));
   OSH_CUDA_TRY(upload(&d_root_, root));
   OSH_CUDA_TRY(upload(&d_newton_, newton));
   OSH_CUDA_TRY(upload(&d_extract_, extract));
@@ -602,17 +620,20 @@ osh_status ShampooEngine::run_wave(int wi, const osh_muon_cfg& mcfg, cudaStream_
       pd[0].a = mref(at(k.gb), k.nb, k.p, k.q, k.ldq, gq);
       pd[0].b = pd[0].a;
       pd[0].out = mref(st(k.L), k.nb, k.p, k.p, k.ldp, Lb);
-      pd[0].symmetric = 1;
+      pd[0].symmetric = 2;  // upper triangle; filled below before the refresh reads
       pd[1].a = mref(at(k.gbt), k.nb, k.q, k.p, k.ldp, gtp);
       pd[1].b = pd[1].a;
       pd[1].out = mref(st(k.R), k.nb, k.q, k.q, k.ldq, Rb);
-      pd[1].symmetric = 1;
+      pd[1].symmetric = 2;
       if (osh_status e = gemm(kEpiStat, pd, 2, static_cast<float>(cfg_.beta2), 0.f); e != OSH_OK)
         return e;
     }
     if (refresh) {
       const int s0 = w.cls.front().stat0;
       if (osh_status e = ew(1, 0.0, [&] {
+            const cudaError_t r =
+                launch_sym_fill_lower(d_symf_ + w.symf.first, w.symf.count, w.symf.tiles, s);
+            if (r != cudaSuccess) return r;
             return launch_sh_sumsq_f32(d_ssq_tasks_ + w.ssq.first, w.ssq.count, w.ssq.tiles, s);
           }); e != OSH_OK)
         return e;

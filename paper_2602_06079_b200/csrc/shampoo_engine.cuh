@@ -70,6 +70,7 @@ class ShampooEngine : public OptimizerEngine {
     int first_bucket = 0, last_bucket = 0;
     std::vector<Cls> cls;
     Range prep, usq, ssq, apply, sgd;     // task ranges (tiles = sum over the range)
+    Range symf;                           // L / R lower-triangle fills (refresh steps)
     Range root_init[1], newton[2], extract[1];
     Range slot_g, slot_u, slot_s, slot_t; // partial-sum slot ranges
     int n_blocks = 0, n_stats = 0;
@@ -101,6 +102,7 @@ class ShampooEngine : public OptimizerEngine {
   ShApplyTask* d_apply_ = nullptr;
   ShSgdTask* d_sgd_ = nullptr;
   ShBlockRef* d_blockrefs_ = nullptr;
+  SymFillTask* d_symf_ = nullptr;
   long long* d_slot_begin_ = nullptr;
   int* d_slot_count_ = nullptr;
   int* d_slot_target_ = nullptr;

@@ -76,6 +76,7 @@ void SoapEngine::release() {
                   static_cast<void*>(d_apply_), static_cast<void*>(d_blockrefs_),
                   static_cast<void*>(d_adam_), static_cast<void*>(d_basis_),
                   static_cast<void*>(d_vperm_), static_cast<void*>(d_qcast_),
+                  static_cast<void*>(d_symf_),
                   static_cast<void*>(d_slot_begin_), static_cast<void*>(d_slot_count_),
                   static_cast<void*>(d_slot_target_)})
     cudaFree(p);
@@ -94,6 +95,7 @@ void SoapEngine::release() {
   d_basis_ = nullptr;
   d_vperm_ = nullptr;
   d_qcast_ = nullptr;
+  d_symf_ = nullptr;
   d_slot_begin_ = nullptr;
   d_slot_count_ = d_slot_target_ = nullptr;
   waves_.clear();
@@ -579,6 +581,32 @@ osh_status SoapEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   OSH_CUDA_TRY(upload(&d_basis_, basis));
   OSH_CUDA_TRY(upload(&d_vperm_, vperm));
   OSH_CUDA_TRY(upload(&d_qcast_, qcast));
+  {  // the statistics are accumulated upper-triangle only (STAT symmetric = 2)
+    std::vector<SymFillTask> symf;
+    for (Wave& w : waves_) {
+      w.symf = Range{};
+      w.symf.first = static_cast<int>(symf.size());
+      for (const Cls& k : w.cls)
+        for (int side = 0; side < 2; ++side) {
+          const int n = side == 0 ? k.p : k.q, ld = side == 0 ? k.ldp : k.ldq;
+          const Side& sd = side == 0 ? k.l : k.r;
+          if (sd.frozen) continue;  // never read
+          for (int i = 0; i < k.nb; ++i) {
+            SymFillTask sf{};
+            sf.s = reinterpret_cast<float*>(d_state_ + sd.S) + static_cast<size_t>(i) * n * ld;
+            sf.ld = ld;
+            sf.n = n;
+            const int T = (n + 31) / 32;
+            sf.tiles = T * (T + 1) / 2;
+            sf.tile_start = w.symf.tiles;
+            w.symf.tiles += sf.tiles;
+            symf.push_back(sf);
+          }
+        }
+      w.symf.count = static_cast<int>(symf.size()) - w.symf.first;
+    }
+    OSH_CUDA_TRY(upload(&d_symf_, symf));
+  }
   OSH_CUDA_TRY(upload(&d_split_, split));
   OSH_CUDA_TRY(upload(&d_chol_, chol));
   OSH_CUDA_TRY(upload(&d_slot_begin_, slot_begin));
@@ -664,6 +692,9 @@ osh_status SoapEngine::refresh_side(const Side& sd, int iters, cudaStream_t s) {
 }
 
 osh_status SoapEngine::refresh(const Wave& w, int iters, bool permute_v, cudaStream_t s) {
+  OSH_CUDA_TRY(timed_elementwise(kModeElementwise + 7, 0.0, 0.0, s, [&] {
+    return launch_sym_fill_lower(d_symf_ + w.symf.first, w.symf.count, w.symf.tiles, s);
+  }));
   for (const Cls& k : w.cls)
     for (const Side* sd : {&k.l, &k.r})
       if (!sd->frozen)
@@ -804,14 +835,14 @@ osh_status SoapEngine::run_wave(int wi, const osh_muon_cfg& cfg, cudaStream_t s)
       L.b = mref(d_ws_ + k.Gs + 2ull * b_off * k.ldq, k.nb, k.p, ks * k.ldq, 4ll * k.ldq, cpq);
       L.out = S16(k.l.S, k.nb, k.p, k.p, k.ldp);
       L.scale = d_bscale_;
-      L.symmetric = 1;
+      L.symmetric = 2;  // upper triangle; refresh() fills the lower one first
       NsProblemDesc R{};
       const long long cqp = static_cast<long long>(k.q) * 4 * k.ldp;
       R.a = mref(d_ws_ + k.Gts, k.nb, k.q, ks * k.ldp, 4ll * k.ldp, cqp);
       R.b = mref(d_ws_ + k.Gts + 2ull * b_off * k.ldp, k.nb, k.q, ks * k.ldp, 4ll * k.ldp, cqp);
       R.out = S16(k.r.S, k.nb, k.q, k.q, k.ldq);
       R.scale = d_bscale_;
-      R.symmetric = 1;
+      R.symmetric = 2;
       pd.push_back(L);
       pd.push_back(R);
     }

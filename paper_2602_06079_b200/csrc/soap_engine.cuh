@@ -103,6 +103,7 @@ class SoapEngine : public OptimizerEngine {
     int first_bucket = 0, last_bucket = 0;
     std::vector<Cls> cls;
     Range prep, rot, apply, adam, basis, vperm, qcast, slots;
+    Range symf;  // L / R lower-triangle fills before a refresh reads them
     double elems_pre = 0.0, elems_adam = 0.0;
   };
   const char* elementwise_name(int mode) const override;
@@ -133,6 +134,7 @@ class SoapEngine : public OptimizerEngine {
   SoapBasisTask* d_basis_ = nullptr;
   SoapVpermTask* d_vperm_ = nullptr;
   SoapQcastTask* d_qcast_ = nullptr;
+  SymFillTask* d_symf_ = nullptr;
   long long* d_slot_begin_ = nullptr;
   int* d_slot_count_ = nullptr;
   int* d_slot_target_ = nullptr;

@@ -249,10 +249,14 @@ def mref32(t):
     return m
 
 
-@pytest.mark.parametrize("sym", [1, 0])
+@pytest.mark.parametrize("alpha", [0.95, 0.0])
+@pytest.mark.parametrize("sym", [1, 0, 2])
 @pytest.mark.parametrize("batch,m,n", [(2, 256, 768), (1, 200, 328), (3, 512, 512)])
-def test_stat_fp32_accumulate(batch, m, n, sym):
-    """Shampoo statistics: L = beta2 * L + G G^T in fp32 (read-modify-write)."""
+def test_stat_fp32_accumulate(batch, m, n, sym, alpha):
+    """Shampoo statistics: L = beta2 * L + G G^T in fp32 (read-modify-write).
+    sym = 2 (the engines' per-step statistics): the upper triangle only, the
+    lower one left as it was, and bit-identical to the mirrored (sym = 1)
+    result where written."""
     g = padded(batch, m, n, n + (-n) % 8, scale=0.3)
     l0 = torch.randn(batch, m, m, device="cuda")
     l0 = l0 + l0.transpose(1, 2)  # symmetric like a statistics matrix
@@ -262,11 +266,21 @@ def test_stat_fp32_accumulate(batch, m, n, sym):
     p.b = mref(g, cols=n)
     p.out = mref32(out)
     p.symmetric = sym
-    run(4, [p], alpha=0.95)
+    run(4, [p], alpha=alpha)
     gf = g[:, :, :n].float()
-    ref = 0.95 * l0 + gf @ gf.transpose(1, 2)
-    assert relerr(out, ref) < 1e-5
-    if sym:
+    ref = alpha * l0 + gf @ gf.transpose(1, 2)
+    if sym == 2:
+        up = torch.ones(m, m, device="cuda", dtype=torch.bool).triu()
+        assert relerr(out[:, up], ref[:, up]) < 1e-5
+        assert torch.equal(out[:, ~up], l0[:, ~up])  # lower triangle untouched
+        full = l0.clone()
+        p.out = mref32(full)
+        p.symmetric = 1
+        run(4, [p], alpha=alpha)
+        assert torch.equal(out[:, up], full[:, up])
+    else:
+        assert relerr(out, ref) < 1e-5
+    if sym == 1:
         assert torch.equal(out, out.transpose(1, 2))
 
 
