@@ -49,6 +49,16 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kFinBufs = 3;
 constexpr uint32_t kFinWBox = 32 * 32 * 4;
 constexpr uint32_t kFinBytes = 4 * kFinBufs * kFinWBox;
+// kEpiSplit (symmetric): per epilogue warp, its 32 x 32 chunk as bf16 hi and
+// lo, transposed through shared memory (80 B row pitch: conflict-free 16 B
+// reads) so the mirrored half leaves as 16 B row stores, not 2 B scalars
+constexpr uint32_t kSplitPitch = 40;  // bf16 elements per staged row
+constexpr uint32_t kSplitWarpBytes = 2 * 32 * kSplitPitch * 2;
+constexpr uint32_t kSplitBytes = 4 * kSplitWarpBytes;
+template <int MODE>
+constexpr uint32_t epi_stage_bytes() {
+  return MODE == kEpiFinal ? kFinBytes : MODE == kEpiSplit ? kSplitBytes : 0;
+}
 template <int MODE, int CG>
 constexpr uint32_t smem_bytes();
 static_assert(1024 + 5 * (16384 + 16384) + 4 * 3 * 4096 + 256 <= 232448, "FINAL (2-CTA) exceeds smem");
@@ -57,7 +67,7 @@ template <int MODE, int CG>
 constexpr uint32_t smem_bytes() {
   // [1 KiB align][stage ring][FINAL staging][barriers 256 B]
   return 1024 + Cfg<MODE, CG>::kStages * (Cfg<MODE, CG>::kStageA + Cfg<MODE, CG>::kStageB) +
-         (MODE == kEpiFinal ? kFinBytes : 0) + 256;
+         epi_stage_bytes<MODE>() + 256;
 }
 constexpr int kRasterGroup = 8;
 
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   uint8_t* smem_a = base;
   uint8_t* smem_b = base + kStages * kStageBytesA;
   uint8_t* fin = smem_b + kStages * kStageBytesB;  // 1 KiB aligned (kEpiFinal staging)
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(fin + (MODE == kEpiFinal ? kFinBytes : 0));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(fin + epi_stage_bytes<MODE>());
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -744,7 +754,42 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           }
           __nv_bfloat16* o = pr.out + c.b * pr.out_bstride;
           const long long sg = pr.out_seg;
-          if (pr.symmetric) {
+          const int rblk = row_base + quarter * 32;  // this warp's 32 rows (32-aligned)
+          if (pr.symmetric && col0 >= rblk + 32 && rblk + 32 <= pr.M && col0 + 32 <= pr.N &&
+              (pr.out_ld & 7) == 0 && (sg & 7) == 0 &&
+              (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+            // whole chunk above this warp's diagonal: rows leave as 16 B
+            // stores; the mirrored block goes through shared memory
+            __nv_bfloat16* d = o + row * pr.out_ld + col0;
+            store_row32(d, col0, pr.N, v);
+            store_row32(d + sg, col0, pr.N, lo);
+            store_row32(d + 2 * sg, col0, pr.N, v);
+            store_row32(d + 3 * sg, col0, pr.N, v);
+            __nv_bfloat16* th = reinterpret_cast<__nv_bfloat16*>(fin + quarter * kSplitWarpBytes);
+            __nv_bfloat16* tl = th + 32 * kSplitPitch;
+            __syncwarp();  // the previous chunk's reads of the staging are done
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {  // staged[j][lane] = value (row, col0 + j)
+              th[j * kSplitPitch + lane] = __float2bfloat16_rn(v[j]);
+              tl[j * kSplitPitch + lane] = __float2bfloat16_rn(lo[j]);
+            }
+            __syncwarp();
+            // lane L: output row col0 + L, columns rblk .. rblk + 31
+            const uint4* sh = reinterpret_cast<const uint4*>(th + lane * kSplitPitch);
+            const uint4* sl = reinterpret_cast<const uint4*>(tl + lane * kSplitPitch);
+            uint4* m = reinterpret_cast<uint4*>(o + static_cast<long long>(col0 + lane) * pr.out_ld + rblk);
+            uint4* m1 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(m) + sg);
+            uint4* m2 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(m) + 2 * sg);
+            uint4* m3 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(m) + 3 * sg);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 hv = sh[q], lv = sl[q];
+              m[q] = hv;
+              m1[q] = lv;
+              m2[q] = hv;
+              m3[q] = hv;
+            }
+          } else if (pr.symmetric) {
             store_row32_sym(o, pr.out_ld, row, col0, pr.N, v);
             store_row32_sym(o + sg, pr.out_ld, row, col0, pr.N, lo);
             store_row32_sym(o + 2 * sg, pr.out_ld, row, col0, pr.N, v);
