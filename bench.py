@@ -114,7 +114,8 @@ class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+         "power.limit")
 
     def __init__(self):
         self.proc, self.lines = None, []
@@ -143,7 +144,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, lim, reasons = [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -154,14 +155,26 @@ class ClockSampler:
                 mx.append(float(f[2]))
             except ValueError:
                 continue
+            try:  # (power: the energy budget the step runs against under sw_power_cap)
+                pw.append((float(f[1]), float(f[3])))
+                if len(f) > 9:
+                    lim.append(float(f[9]))
+            except ValueError:
+                pass
             for name, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(name)
         if not sm:
             return None
         load = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "samples": len(sm),
-                "reasons": sorted(reasons)}
+        out = {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "samples": len(sm),
+               "reasons": sorted(reasons)}
+        busy = [p for s, p in pw if s > 0.5 * max(sm)]
+        if busy:
+            out["power_w"] = round(statistics.median(busy), 1)
+        if lim:
+            out["power_limit_w"] = max(lim)
+        return out
 
 
 def measured_peaks():

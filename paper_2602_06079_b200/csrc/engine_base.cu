@@ -91,7 +91,7 @@ void OptimizerEngine::read_profile(int* launches, double* flops, double* exec_fl
 
 const char* OptimizerEngine::elementwise_name(int) const { return "elementwise"; }
 
-std::string OptimizerEngine::profile_text() const {
+std::string OptimizerEngine::profile_text(cudaEvent_t ref) const {
   static const char* kGemm[] = {"gram", "poly", "update", "final", "stat", "split", "?", "?"};
   std::string out;
   char line[512];
@@ -100,9 +100,15 @@ std::string OptimizerEngine::profile_text() const {
     cudaEventSynchronize(t.b);
     if (cudaEventElapsedTime(&dt, t.a, t.b) != cudaSuccess) continue;
     const char* name = t.mode < kModeElementwise ? kGemm[t.mode] : elementwise_name(t.mode);
-    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s\n", name, dt, t.flops, t.exec_flops,
+    std::snprintf(line, sizeof(line), "%s %.4f %.6e %.6e %s", name, dt, t.flops, t.exec_flops,
                   t.what.c_str());
     out += line;
+    float t0 = 0.f;
+    if (ref != nullptr && cudaEventElapsedTime(&t0, ref, t.a) == cudaSuccess) {
+      std::snprintf(line, sizeof(line), " @%.4f", t0);
+      out += line;
+    }
+    out += "\n";
   }
   return out;
 }

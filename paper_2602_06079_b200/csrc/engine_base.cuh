@@ -86,8 +86,10 @@ class OptimizerEngine {
   // read_profile totals cover the GEMMs only, profile_text lists all launches.
   void set_profile(bool on) { profile_ = on; }
   void read_profile(int* launches, double* flops, double* exec_flops, double* ms, bool reset);
-  // One line per recorded launch: "mode ms flops exec_flops shapes".
-  std::string profile_text() const;
+  // One line per recorded launch: "mode ms flops exec_flops shapes", plus
+  // " @start" (ms after `ref`, a timing event recorded before the launches)
+  // when ref is given.
+  std::string profile_text(cudaEvent_t ref = nullptr) const;
 
  protected:
   struct Timed {

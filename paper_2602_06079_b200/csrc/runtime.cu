@@ -1537,8 +1537,10 @@ osh_status osh_gemm_profile_read(osh_ctx* ctx, osh_gemm_profile* out, int32_t re
 osh_status osh_gemm_profile_dump(osh_ctx* ctx, char* buf, size_t cap, size_t* len) {
   if (osh_status st = osh_ctx_sync(ctx); st != OSH_OK) return st;
   if (!ctx->layout_ready) return osh::fail(OSH_ERR_PLAN, "no layout");
-  std::string s = ctx->engine->profile_text();
-  for (auto& e : ctx->tp_engines) s += e->profile_text();
+  // start offsets relative to the last step's start (ev[5]): a timeline
+  // when a single step was profiled
+  std::string s = ctx->engine->profile_text(ctx->ev[5]);
+  for (auto& e : ctx->tp_engines) s += e->profile_text(ctx->ev[5]);
   if (len != nullptr) *len = s.size();
   if (buf != nullptr && cap > 0) {
     const size_t n = std::min(s.size(), cap - 1);

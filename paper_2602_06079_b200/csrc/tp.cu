@@ -174,9 +174,21 @@ osh_status tp_setup(osh_ctx* ctx, int64_t budget) {
   }
   ctx->tp_item_of.assign(ctx->params.size(), -1);
   ctx->tp_groups = static_cast<int>(plan.groups.size());
+  // Execution order of the groups (free: they are independent; the same on
+  // every TP rank, since all compute the same plan): largest first, so the
+  // last group's pack / scatter / AG-v — the step's unhidden TP tail — is the
+  // smallest. Group ids below are execution positions.
+  std::vector<size_t> order(plan.groups.size());
+  std::vector<int64_t> gsize(plan.groups.size(), 0);
+  for (size_t g = 0; g < plan.groups.size(); ++g) {
+    order[g] = g;
+    for (int r = 0; r < T; ++r)
+      for (const int pid : plan.groups[g].rank_params[r]) gsize[g] += ctx->params_full[pid].numel;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return gsize[a] > gsize[b]; });
   for (size_t g = 0; g < plan.groups.size(); ++g)
     for (int r = 0; r < T; ++r)
-      for (const int pid : plan.groups[g].rank_params[r]) {
+      for (const int pid : plan.groups[order[g]].rank_params[r]) {
         osh_ctx::TpItem it;
         it.pid = pid;
         it.group = static_cast<int>(g);
@@ -353,24 +365,27 @@ osh_status tp_gather(osh_ctx* ctx, const std::vector<cudaEvent_t>& ready) {
       }
     }
     TP_NCCL(ncclGroupEnd());
+    // the hosted full gradients are assembled here too, off the compute stream
+    OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
+                                    ctx->tp_unpack_tiles[g], ts));
     OSH_CUDA_TRY(cudaEventRecord(ctx->tp_gather_ev[g], ts));
   }
   return OSH_OK;
 }
 
 osh_status tp_group_begin(osh_ctx* ctx, int g, cudaStream_t cs) {
-  OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));
-  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_unpack[g], static_cast<int>(ctx->tp_unpack[g].size()),
-                                  ctx->tp_unpack_tiles[g], cs));
+  OSH_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->tp_gather_ev[g], 0));  // gathered + unpacked
   return ctx->tp_engines[g]->begin_step(cs);  // the host's full-matrix Muon follows
 }
 
 osh_status tp_group_end(osh_ctx* ctx, int g, cudaStream_t cs) {
+  // pack, scatter and AG-v of the group on the TP stream: the compute stream
+  // goes straight on to the next group
   cudaStream_t ts = ctx->tp_stream;
-  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
-                                  ctx->tp_pack_tiles[g], cs));
-  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));
+  OSH_CUDA_TRY(cudaEventRecord(ctx->tp_pack_ev[g], cs));  // the group's update is done
   OSH_CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tp_pack_ev[g], 0));
+  OSH_CUDA_TRY(launch_copy_blocks(ctx->d_tp_pack[g], static_cast<int>(ctx->tp_pack[g].size()),
+                                  ctx->tp_pack_tiles[g], ts));
   // ---- scatter updated bf16 shards into every rank's replica slot
   if (osh_status st = issue_tp_scatter(ctx, g, ts); st != OSH_OK) return st;
   if (ctx->nvls)  // AG-v of the group's shards: every DP peer's replica slot

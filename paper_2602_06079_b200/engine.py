@@ -257,9 +257,24 @@ class DistributedMuon:
         _lib.check(L.osh_gemm_profile_dump(self._ctx, buf, n.value + 1, ctypes.byref(n)))
         out = []
         for line in buf.value.decode().splitlines():
-            mode, ms, fl, ex, what = line.split()
+            mode, ms, fl, ex, what = line.split()[:5]
             out.append((mode, float(ms), float(fl), float(ex), what))
         return out
+
+    def gemm_profile_timeline(self) -> list:
+        """Per-launch [(mode, start_ms, ms, shapes)], start relative to the last
+        step's start: a timeline when exactly one step was profiled."""
+        n = ctypes.c_size_t(0)
+        L = _lib.lib()
+        _lib.check(L.osh_gemm_profile_dump(self._ctx, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _lib.check(L.osh_gemm_profile_dump(self._ctx, buf, n.value + 1, ctypes.byref(n)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            f = line.split()
+            if len(f) >= 6 and f[5].startswith("@"):
+                out.append((f[0], float(f[5][1:]), float(f[1]), f[4]))
+        return sorted(out, key=lambda r: r[1])
 
     def gemm_profile(self, reset: bool = True) -> dict:
         p = _lib.GemmProfile()
