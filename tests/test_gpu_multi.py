@@ -67,6 +67,14 @@ def test_dp2_tp2_micro_groups_match_oracle(coll, gdt):
     assert res["grad_dtype"] == gdt
 
 
+def test_stage_overlap_opt_in_matches_oracle(monkeypatch):
+    # OSH_SEQ_OVERLAP=1: momentum of stage i+1 beside the GEMMs of stage i on
+    # the NCCL RS-v / AG-v path and across TP micro groups (opt-in schedule)
+    monkeypatch.setenv("OSH_SEQ_OVERLAP", "1")
+    assert _run(2, "multi_gpu_check.py", 3, "nccl")["collectives"] == "nccl"
+    _run(2, "multi_gpu_check_tp.py", 1, 2, 3)
+
+
 def test_dp2_nccl_bucket_ready_matches_oracle():
     # gradients announced bucket by bucket in reverse order: the RS-v of each
     # bucket starts before the next one is written (backward overlap)
