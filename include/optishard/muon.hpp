@@ -14,12 +14,17 @@
 //   FaultSpec / run_partitioned(params, cfg, steps, seed,
 //       shard_layout, dp_plan, tp_plan*, fault)             verify.hpp:212-322
 // `Matrix` stands in for Eigen::MatrixXd (Eigen is not a dependency of this
-// build): dense doubles, row-major storage — element (i, j) has the same
-// value as the reference's, only the memory order differs. Each function
-// takes an optional trailing `device` (default 0). The Newton-Schulz
-// orthogonalisation runs on the GPU (bf16 operands, fp32 accumulation:
-// within the tolerance of tests/test_gpu_parity.py of the fp64 reference, not
-// bit for bit); the momentum / axpy are the reference's fp64 expressions.
+// build) with the same interface subset and the same COLUMN-MAJOR storage:
+// rows(), cols(), size(), operator()(i, j), data(), Zero, transpose(),
+// norm(), squaredNorm(), setZero(). newton_schulz_orthogonalize and
+// muon_apply are templates over the matrix type, so a caller holding real
+// Eigen::MatrixXd values (column-major, contiguous) passes them unchanged;
+// tests/cpp/muon_dropin.cpp checks that against an Eigen stand-in. Each
+// function takes an optional trailing `device` (default 0). The
+// Newton-Schulz orthogonalisation runs on the GPU (bf16 operands, fp32
+// accumulation: within the tolerance of tests/test_gpu_parity.py of the fp64
+// reference, not bit for bit); the momentum / axpy are the reference's fp64
+// expressions.
 //
 // The production distributed step (run_partitioned executed for real across
 // GPUs: RS-v -> owner Muon -> AG-v over NCCL) is the RAII class
@@ -51,28 +56,38 @@ struct OptimizerConfig {
   int ns_steps = 5;
 };
 
-// Dense matrix of doubles (vectors: cols == 1), row-major storage.
-struct Matrix {
-  std::int64_t rows = 0, cols = 0;
-  std::vector<double> v;
+// Dense matrix of doubles (vectors: cols == 1), column-major like
+// Eigen::MatrixXd: element (i, j) at data()[j * rows() + i].
+class Matrix {
+ public:
+  using Index = std::int64_t;
   Matrix() = default;
-  Matrix(std::int64_t r, std::int64_t c) : rows(r), cols(c), v(static_cast<std::size_t>(r * c)) {}
-  static Matrix Zero(std::int64_t r, std::int64_t c) { return Matrix(r, c); }
-  double& operator()(std::int64_t i, std::int64_t j) { return v[static_cast<std::size_t>(i * cols + j)]; }
-  double operator()(std::int64_t i, std::int64_t j) const {
-    return v[static_cast<std::size_t>(i * cols + j)];
-  }
+  Matrix(Index r, Index c) : rows_(r), cols_(c), v_(static_cast<std::size_t>(r * c), 0.0) {}
+  static Matrix Zero(Index r, Index c) { return Matrix(r, c); }
+  Index rows() const { return rows_; }
+  Index cols() const { return cols_; }
+  Index size() const { return rows_ * cols_; }
+  double& operator()(Index i, Index j) { return v_[static_cast<std::size_t>(j * rows_ + i)]; }
+  double operator()(Index i, Index j) const { return v_[static_cast<std::size_t>(j * rows_ + i)]; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+  void setZero() { std::fill(v_.begin(), v_.end(), 0.0); }
   Matrix transpose() const {
-    Matrix t(cols, rows);
-    for (std::int64_t i = 0; i < rows; ++i)
-      for (std::int64_t j = 0; j < cols; ++j) t(j, i) = (*this)(i, j);
+    Matrix t(cols_, rows_);
+    for (Index j = 0; j < cols_; ++j)
+      for (Index i = 0; i < rows_; ++i) t(j, i) = (*this)(i, j);
     return t;
   }
-  double norm() const {  // Frobenius
+  double squaredNorm() const {  // storage (column-major) order, as Eigen's
     double s = 0.0;
-    for (const double x : v) s += x * x;
-    return std::sqrt(s);
+    for (const double x : v_) s += x * x;
+    return s;
   }
+  double norm() const { return std::sqrt(squaredNorm()); }  // Frobenius
+
+ private:
+  Index rows_ = 0, cols_ = 0;
+  std::vector<double> v_;
 };
 
 namespace detail {
@@ -158,7 +173,8 @@ inline std::uint64_t stream_seed(std::uint64_t seed, int kind, int step, int par
 inline Matrix filled_normal(const ParamSpec& p, std::uint64_t seed, double scale) {
   Matrix m(p.shape.at(0), p.is_matrix() ? p.shape[1] : 1);
   NormalStream s(seed);
-  for (double& x : m.v) x = s.next() * scale;  // row-major fill order (i, j)
+  for (Matrix::Index i = 0; i < m.rows(); ++i)  // the reference's fill order: (i, j) row by row
+    for (Matrix::Index j = 0; j < m.cols(); ++j) m(i, j) = s.next() * scale;
   return m;
 }
 
@@ -176,23 +192,34 @@ inline Matrix init_weight(const ParamSpec& p, std::uint64_t seed) {
 }
 
 // Quintic Newton-Schulz on the GPU: unit Frobenius scaling, transposed
-// iteration when taller than wide, zero input returned unchanged.
-inline Matrix newton_schulz_orthogonalize(Matrix x, int steps, int device = 0) {
-  detail::osh_check(osh_newton_schulz_host(device, x.v.data(), x.rows, x.cols, steps));
+// iteration when taller than wide, zero input returned unchanged. `Mat`:
+// Matrix or any column-major contiguous matrix with rows() / cols() /
+// data() (Eigen::MatrixXd). The C ABI takes row-major arrays; column-major
+// rows x cols storage is the row-major cols x rows transpose, and
+// NS(X^T) = NS(X)^T, so the storage goes through as that transpose.
+template <class Mat>
+Mat newton_schulz_orthogonalize(Mat x, int steps, int device = 0) {
+  detail::osh_check(osh_newton_schulz_host(device, x.data(), static_cast<std::int64_t>(x.cols()),
+                                           static_cast<std::int64_t>(x.rows()), steps));
   return x;
 }
 
 // momentum = beta*momentum + grad; matrix: weight -= lr*NS(momentum);
-// vector: weight -= lr*momentum.
-inline void muon_apply(const ParamSpec& p, const OptimizerConfig& cfg, Matrix& weight,
-                       Matrix& momentum, const Matrix& grad, int device = 0) {
-  if (weight.v.size() != static_cast<std::size_t>(p.numel) || momentum.v.size() != weight.v.size() ||
-      grad.v.size() != weight.v.size())
+// vector: weight -= lr*momentum. (`Mat` as above: the elementwise terms are
+// layout-free, the NS term runs on the column-major storage's transpose.)
+template <class Mat>
+void muon_apply(const ParamSpec& p, const OptimizerConfig& cfg, Mat& weight, Mat& momentum,
+                const Mat& grad, int device = 0) {
+  const auto n = [](const Mat& m) { return static_cast<std::int64_t>(m.rows()) * m.cols(); };
+  if (n(weight) != p.numel || n(momentum) != p.numel || n(grad) != p.numel ||
+      (p.is_matrix() && (weight.rows() != p.shape[0] || momentum.rows() != p.shape[0] ||
+                         grad.rows() != p.shape[0])))
     throw ShardError("muon_apply: weight / momentum / grad do not match the parameter shape");
-  const osh_param_desc d = detail::to_desc(p);
+  osh_param_desc d = detail::to_desc(p);
+  if (p.is_matrix()) std::swap(d.shape[0], d.shape[1]);  // column-major storage
   const osh_muon_cfg c = detail::to_cfg(cfg);
-  detail::osh_check(osh_muon_apply_host(device, &d, &c, weight.v.data(), momentum.v.data(),
-                                        grad.v.data(), nullptr));
+  detail::osh_check(osh_muon_apply_host(device, &d, &c, weight.data(), momentum.data(),
+                                        grad.data(), nullptr));
 }
 
 struct VerifyTrace {
@@ -214,9 +241,11 @@ inline double max_abs_diff(const VerifyTrace& a, const VerifyTrace& b) {
     }
   for (const auto& [id, w] : a.final_weights) {
     const auto it = b.final_weights.find(id);
-    if (it == b.final_weights.end() || it->second.v.size() != w.v.size())
+    if (it == b.final_weights.end() || it->second.rows() != w.rows() || it->second.cols() != w.cols())
       throw UnsupportedError("traces cover different parameters");
-    for (std::size_t i = 0; i < w.v.size(); ++i) mx = std::max(mx, std::abs(w.v[i] - it->second.v[i]));
+    const double* x = w.data();
+    const double* y = it->second.data();
+    for (Matrix::Index i = 0; i < w.size(); ++i) mx = std::max(mx, std::abs(x[i] - y[i]));
   }
   return mx;
 }
@@ -226,7 +255,7 @@ inline Matrix reduced_gradient(const ParamSpec& p, std::uint64_t seed, int step,
   Matrix g = synth_gradient(p, seed, step, 0);
   for (int r = 1; r < contributors; ++r) {
     const Matrix x = synth_gradient(p, seed, step, r);
-    for (std::size_t i = 0; i < g.v.size(); ++i) g.v[i] += x.v[i];
+    for (Matrix::Index i = 0; i < g.size(); ++i) g.data()[i] += x.data()[i];
   }
   return g;
 }
@@ -238,8 +267,11 @@ inline double traced_apply(const ParamSpec& p, const OptimizerConfig& cfg, Matri
                            const Matrix& g, int device) {
   const Matrix before = w;
   muon_apply(p, cfg, w, m, g, device);
-  double s = 0.0;
-  for (std::size_t i = 0; i < w.v.size(); ++i) s += (w.v[i] - before.v[i]) * (w.v[i] - before.v[i]);
+  double s = 0.0;  // ||W_new - W_old||_F over the column-major storage, as Eigen's norm()
+  for (Matrix::Index i = 0; i < w.size(); ++i) {
+    const double d = w.data()[i] - before.data()[i];
+    s += d * d;
+  }
   return std::sqrt(s);
 }
 
@@ -252,7 +284,7 @@ inline VerifyTrace run_replicated(const std::vector<ParamSpec>& params, const Op
   std::map<int, Matrix> weights, momenta;
   for (const ParamSpec& p : params) {
     weights[p.id] = init_weight(p, seed);
-    momenta[p.id] = Matrix::Zero(weights[p.id].rows, weights[p.id].cols);
+    momenta[p.id] = Matrix::Zero(weights[p.id].rows(), weights[p.id].cols());
     trace.state_hosts[p.id].insert("replicated");
   }
   for (int step = 0; step < steps; ++step) {
@@ -320,7 +352,7 @@ inline VerifyTrace run_partitioned(const std::vector<ParamSpec>& params, const O
   for (const ParamSpec& p : params) {
     weights[p.id] = init_weight(p, seed);
     const std::string k = key_of(host[p.id]);
-    stores[k][p.id] = Matrix::Zero(weights[p.id].rows, weights[p.id].cols);
+    stores[k][p.id] = Matrix::Zero(weights[p.id].rows(), weights[p.id].cols());
     trace.state_hosts[p.id].insert(k);
   }
   for (int step = 0; step < steps; ++step) {
@@ -338,7 +370,7 @@ inline VerifyTrace run_partitioned(const std::vector<ParamSpec>& params, const O
       auto& store = stores[k];
       auto it = store.find(p.id);
       if (it == store.end())  // a rerouted parameter meets a cold momentum buffer
-        it = store.emplace(p.id, Matrix::Zero(weights[p.id].rows, weights[p.id].cols)).first;
+        it = store.emplace(p.id, Matrix::Zero(weights[p.id].rows(), weights[p.id].cols())).first;
       trace.update_norms.back()[p.id] =
           detail::traced_apply(p, cfg, weights[p.id], it->second,
                                reduced_gradient(p, seed, step, dp_plan.ranks), device);

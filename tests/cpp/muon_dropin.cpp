@@ -2,7 +2,10 @@
 // re-expressed against THIS build's C++ drop-in (include/optishard/muon.hpp +
 // libosh.so): the same calls, the same assertions, the GPU underneath.
 // Built and run by tests/test_gpu_dropin.py (needs a B200):
-//   g++ -std=c++20 -O2 -Iinclude tests/cpp/muon_dropin.cpp -Lpaper_2602_06079_b200 -losh
+//   g++ -std=c++20 -O2 -Iinclude -Ioracle/eigen_shim tests/cpp/muon_dropin.cpp
+//       -Lpaper_2602_06079_b200 -losh
+// (oracle/eigen_shim: a column-major Eigen::MatrixXd stand-in, so the
+// entry points are also exercised with the reference's own matrix type)
 //   ./muon_dropin <trace-out.bin>
 // Prints one "PASS <case>" / "FAIL <case>: <why>" line per case and exits
 // non-zero if any case fails. The replicated toy trace (update norms and
@@ -15,6 +18,8 @@
 #include <random>
 #include <string>
 #include <vector>
+
+#include <Eigen/Dense>
 
 #include "optishard/muon.hpp"
 
@@ -69,11 +74,18 @@ ModelConfig toy_config() {  // test_verify.cpp toy_config()
 }
 
 Matrix matmul(const Matrix& a, const Matrix& b) {
-  Matrix c(a.rows, b.cols);
-  for (std::int64_t i = 0; i < a.rows; ++i)
-    for (std::int64_t k = 0; k < a.cols; ++k)
-      for (std::int64_t j = 0; j < b.cols; ++j) c(i, j) += a(i, k) * b(k, j);
+  Matrix c(a.rows(), b.cols());
+  for (std::int64_t i = 0; i < a.rows(); ++i)
+    for (std::int64_t k = 0; k < a.cols(); ++k)
+      for (std::int64_t j = 0; j < b.cols(); ++j) c(i, j) += a(i, k) * b(k, j);
   return c;
+}
+
+// fills x(i, j) row by row from a generator
+template <class Mat, class F>
+void fill(Mat& x, F&& next) {
+  for (std::int64_t i = 0; i < x.rows(); ++i)
+    for (std::int64_t j = 0; j < x.cols(); ++j) x(i, j) = next();
 }
 
 // One-sided Jacobi SVD (small matrices): A = U diag(s) V^T, thin.
@@ -83,9 +95,9 @@ struct Svd {
 };
 
 Svd svd(const Matrix& a_in) {
-  const bool tall = a_in.rows >= a_in.cols;
+  const bool tall = a_in.rows() >= a_in.cols();
   Matrix a = tall ? a_in : a_in.transpose();  // work on m >= n
-  const std::int64_t m = a.rows, n = a.cols;
+  const std::int64_t m = a.rows(), n = a.cols();
   Matrix v(n, n);
   for (std::int64_t i = 0; i < n; ++i) v(i, i) = 1.0;
   for (int sweep = 0; sweep < 60; ++sweep) {
@@ -137,9 +149,11 @@ std::string in_band(const std::vector<double>& svs, double lo, double hi) {
   return "";
 }
 
-double max_abs(const Matrix& a, const Matrix& b) {
+template <class A, class B>
+double max_abs(const A& a, const B& b) {
   double m = 0;
-  for (std::size_t i = 0; i < a.v.size(); ++i) m = std::max(m, std::abs(a.v[i] - b.v[i]));
+  for (std::int64_t i = 0; i < a.rows(); ++i)
+    for (std::int64_t j = 0; j < a.cols(); ++j) m = std::max(m, std::abs(a(i, j) - b(i, j)));
   return m;
 }
 
@@ -168,7 +182,7 @@ int main(int argc, char** argv) {
   run_case("orthogonalization commutes with transposition", [] {
     detail::NormalStream stream(99);
     Matrix x(3, 7);
-    for (double& e : x.v) e = stream.next();
+    fill(x, [&] { return stream.next(); });
     const Matrix a = newton_schulz_orthogonalize(x, 5);
     const Matrix b = newton_schulz_orthogonalize(x.transpose(), 5);
     const double d = max_abs(a.transpose(), b);
@@ -177,9 +191,7 @@ int main(int argc, char** argv) {
   // :95-98
   run_case("zero input passes through", [] {
     const Matrix y = newton_schulz_orthogonalize(Matrix(3, 5), 5);
-    for (const double e : y.v)
-      if (e != 0.0) return std::string("non-zero output");
-    return std::string();
+    return max_abs(y, Matrix(3, 5)) == 0.0 ? std::string() : std::string("non-zero output");
   });
   // :100-123
   run_case("well-conditioned inputs land in the band", [] {
@@ -188,11 +200,11 @@ int main(int argc, char** argv) {
     for (int trial = 0; trial < 40; ++trial) {
       const int rows = 2 + static_cast<int>(rng() % 5), cols = 2 + static_cast<int>(rng() % 5);
       Matrix x(rows, cols);
-      for (double& e : x.v) e = normal(rng);
+      fill(x, [&] { return normal(rng); });
       Svd d = svd(x);  // clamp the spectrum into [0.5, 2]
       const std::int64_t k = static_cast<std::int64_t>(d.s.size());
-      Matrix us(d.u.rows, k);
-      for (std::int64_t i = 0; i < d.u.rows; ++i)
+      Matrix us(d.u.rows(), k);
+      for (std::int64_t i = 0; i < d.u.rows(); ++i)
         for (std::int64_t j = 0; j < k; ++j) us(i, j) = d.u(i, j) * std::clamp(d.s[j], 0.5, 2.0);
       x = matmul(us, d.v.transpose());
       const std::string why = in_band(svd(newton_schulz_orthogonalize(x, 5)).s, 0.55, 1.45);
@@ -208,7 +220,8 @@ int main(int argc, char** argv) {
     const Matrix before = w;
     muon_apply(p, cfg, w, m, synth_gradient(p, 3, 0, 0));
     Matrix d = w;
-    for (std::size_t i = 0; i < d.v.size(); ++i) d.v[i] -= before.v[i];
+    for (std::int64_t i = 0; i < d.rows(); ++i)
+      for (std::int64_t j = 0; j < d.cols(); ++j) d(i, j) -= before(i, j);
     const double ideal = cfg.lr * std::sqrt(8.0), n = d.norm();
     return (n > 0.6 * ideal && n < 1.4 * ideal) ? std::string() : "norm " + std::to_string(n);
   });
@@ -220,7 +233,7 @@ int main(int argc, char** argv) {
     const Matrix g = synth_gradient(p, 3, 0, 0), before = w;
     muon_apply(p, cfg, w, m, g);
     Matrix expected = before;
-    for (std::size_t i = 0; i < expected.v.size(); ++i) expected.v[i] = before.v[i] - cfg.lr * g.v[i];
+    for (std::int64_t i = 0; i < expected.rows(); ++i) expected(i, 0) = before(i, 0) - cfg.lr * g(i, 0);
     return max_abs(w, expected) == 0.0 ? std::string() : std::string("differs");
   });
   // :152-160
@@ -290,6 +303,34 @@ int main(int argc, char** argv) {
       if (hosts.size() == 2) return std::string();
     return std::string("no two-host trail");
   });
+  // the reference's own matrix type (column-major Eigen::MatrixXd) through
+  // the same entry points: identical storage, so bit-identical results
+  run_case("Eigen::MatrixXd callers get the same results", [] {
+    detail::NormalStream stream(5);
+    Matrix x(6, 10);
+    Eigen::MatrixXd ex(6, 10);
+    fill(x, [&] { return stream.next(); });
+    for (std::int64_t i = 0; i < 6; ++i)
+      for (std::int64_t j = 0; j < 10; ++j) ex(i, j) = x(i, j);
+    if (max_abs(newton_schulz_orthogonalize(x, 5), newton_schulz_orthogonalize(ex, 5)) != 0.0)
+      return std::string("newton_schulz_orthogonalize differs");
+    const ParamSpec p = matrix_param(0, 6, 10);
+    OptimizerConfig cfg;
+    Matrix w = init_weight(p, 9), m = Matrix::Zero(6, 10);
+    const Matrix g = synth_gradient(p, 9, 0, 0);
+    Eigen::MatrixXd ew(6, 10), em = Eigen::MatrixXd::Zero(6, 10), eg(6, 10);
+    for (std::int64_t i = 0; i < 6; ++i)
+      for (std::int64_t j = 0; j < 10; ++j) {
+        ew(i, j) = w(i, j);
+        eg(i, j) = g(i, j);
+      }
+    for (int step = 0; step < 3; ++step) {
+      muon_apply(p, cfg, w, m, g);
+      muon_apply(p, cfg, ew, em, eg);
+    }
+    if (max_abs(w, ew) != 0.0 || max_abs(m, em) != 0.0) return std::string("muon_apply differs");
+    return std::string();
+  });
   // errors cross the ABI as the reference's exception classes
   run_case("shape mismatch raises ShardError", [] {
     const ParamSpec p = matrix_param(0, 4, 4);
@@ -324,10 +365,14 @@ int main(int argc, char** argv) {
         const double rec[2] = {static_cast<double>(id), n};
         std::fwrite(rec, 8, 2, f);
       }
-    for (const auto& [id, w] : replicated_toy.final_weights) {
-      const double hdr[2] = {static_cast<double>(id), static_cast<double>(w.v.size())};
+    for (const auto& [id, w] : replicated_toy.final_weights) {  // values row by row
+      const double hdr[2] = {static_cast<double>(id), static_cast<double>(w.size())};
       std::fwrite(hdr, 8, 2, f);
-      std::fwrite(w.v.data(), 8, w.v.size(), f);
+      for (std::int64_t i = 0; i < w.rows(); ++i)
+        for (std::int64_t j = 0; j < w.cols(); ++j) {
+          const double x = w(i, j);
+          std::fwrite(&x, 8, 1, f);
+        }
     }
     if (std::fclose(f) != 0) return 2;
   }

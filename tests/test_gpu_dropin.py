@@ -25,7 +25,7 @@ SRC = os.path.join(ROOT, "tests", "cpp", "muon_dropin.cpp")
 def _build(tmp_path):
     exe = str(tmp_path / "muon_dropin")
     subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror",
-                    "-I", os.path.join(ROOT, "include"), SRC, "-o", exe, "-L", LIBDIR, "-l:libosh.so",
+                    "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "oracle", "eigen_shim"), SRC, "-o", exe, "-L", LIBDIR, "-l:libosh.so",
                     f"-Wl,-rpath,{LIBDIR}"], check=True, capture_output=True, text=True)
     return exe
 
