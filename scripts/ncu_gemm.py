@@ -30,9 +30,11 @@ ox = torch.empty_like(x)
 g = _lib.GemmProblem(); g.a = mref(x); g.b = mref(x); g.out = mref(oa); g.symmetric = int('--sym' in sys.argv)
 pl = _lib.GemmProblem(); pl.a = mref(a); pl.b = mref(a); pl.out = mref(oa); pl.aux = mref(a); pl.symmetric = int('--sym' in sys.argv)
 u = _lib.GemmProblem(); u.a = mref(a); u.b = mref(x); u.b_mn_major = 1; u.out = mref(ox); u.aux = mref(x)
+# --noaux: the step's UPDATE form (the 'a X' term folded into B by POLY: no aux read)
+ua = 0.0 if '--noaux' in sys.argv else 3.4445
 for _ in range(2):  # warm-up
-    run(0, g); run(1, pl, -4.775, 2.0315); run(2, u, 3.4445)
+    run(0, g); run(1, pl, -4.775, 2.0315); run(2, u, ua)
 torch.cuda.synchronize()
-run(0, g); run(1, pl, -4.775, 2.0315); run(2, u, 3.4445)
+run(0, g); run(1, pl, -4.775, 2.0315); run(2, u, ua)
 torch.cuda.synchronize()
 print("ok")
