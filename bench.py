@@ -188,6 +188,21 @@ def measured_peaks():
             "fallback (B200_PROFILING.md)"
 
 
+def gpu_local_cpus(torch, dev):
+    """Binds the calling thread to the CPUs NVML names as close to GPU `dev`,
+    so pinned host buffers allocated next land on that GPU's NUMA node (the
+    caller restores its affinity after allocating). True when bound."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+        return True
+    except Exception:
+        return False
+
+
 def ncu_traffic():
     """Per-launch DRAM bytes of the dominant GEMM from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ns_gemm_ncu.json")
@@ -385,6 +400,10 @@ def run_ours(a, dist: Dist):
         gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
         # every rank pins a full gradient and replica (N x 29 GB at 8B bf16):
         # all ranks take the e2e leg together or none does
+        numa = os.environ.get("OSH_BENCH_NUMA", "1") != "0"
+        saved_cpus = os.sched_getaffinity(0)
+        if numa:
+            numa = gpu_local_cpus(torch, dist.local)
         try:
             hg = torch.empty(total, dtype=gdt, pin_memory=True)
             hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
@@ -392,6 +411,8 @@ def run_ours(a, dist: Dist):
         except RuntimeError as exc:  # pinned host memory exhausted
             hg = hr = None
             pinned = str(exc).splitlines()[0][:200]
+        finally:  # (the pages stay where they were allocated)
+            os.sched_setaffinity(0, saved_cpus)
         flags = dist.gather(pinned)
         if any(f is not True for f in flags):
             e2e_skip = next(f for f in flags if f is not True)
@@ -423,7 +444,8 @@ def run_ours(a, dist: Dist):
         e2e_ms = f0.elapsed_time(f1) / a.e2e_steps
         e2e = {"e2e_ms": e2e_ms, "h2d": total * hg.element_size(),
                "d2h": (info["owned_numel"] if owned_out else total) * 2,
-               "d2h_what": "own updated slices" if owned_out else "full bf16 replica"}
+               "d2h_what": "own updated slices" if owned_out else "full bf16 replica",
+               "numa_local": bool(numa)}
         del hg, hr
 
     rec = {"ms": ms, "prof": prof, "prof_steps": prof_steps, "by_mode": by_mode, "last": last, "info": info, "e2e": e2e,
@@ -525,7 +547,9 @@ def run_ours(a, dist: Dist):
                       "h2d_bytes_per_step": allrec[0]["e2e"]["h2d"],
                       "d2h_bytes_per_step": allrec[0]["e2e"]["d2h"],
                       "note": "per rank: H2D its full local bf16 gradient (pinned), D2H "
-                              + allrec[0]["e2e"]["d2h_what"] + "; bytes are rank 0's"}
+                              + allrec[0]["e2e"]["d2h_what"] + "; bytes are rank 0's"
+                              + ("; pinned buffers on each GPU's NUMA node" if allrec[0]["e2e"]["numa_local"]
+                                 else "")}
     if a.optimizer == "soap":
         rms = max(r["refresh_ms"] for r in allrec)
         out["soap"] = {"block": a.shampoo_block, "precond_every": a.precond_every,
