@@ -188,6 +188,18 @@ def measured_peaks():
             "fallback (B200_PROFILING.md)"
 
 
+def host_mem_available():
+    """MemAvailable of this host in bytes (None if unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return None
+
+
 def gpu_local_cpus(torch, dev):
     """Binds the calling thread to the CPUs NVML names as close to GPU `dev`,
     so pinned host buffers allocated next land on that GPU's NUMA node (the
@@ -402,17 +414,26 @@ def run_ours(a, dist: Dist):
         # all ranks take the e2e leg together or none does
         numa = os.environ.get("OSH_BENCH_NUMA", "1") != "0"
         saved_cpus = os.sched_getaffinity(0)
-        if numa:
-            numa = gpu_local_cpus(torch, dist.local)
-        try:
-            hg = torch.empty(total, dtype=gdt, pin_memory=True)
-            hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
-            pinned = True
-        except RuntimeError as exc:  # pinned host memory exhausted
-            hg = hr = None
-            pinned = str(exc).splitlines()[0][:200]
-        finally:  # (the pages stay where they were allocated)
-            os.sched_setaffinity(0, saved_cpus)
+        # every local rank pins its buffers at once: skip the leg (all ranks
+        # agree below) rather than let pinned pages exhaust the host's memory
+        need = dist.world * total * (torch.tensor([], dtype=gdt).element_size() + 2)
+        avail = host_mem_available()
+        hg = hr = None
+        if avail is not None and need > 0.8 * avail:
+            pinned = (f"host memory: {dist.world} ranks x {need / dist.world / 1e9:.1f} GB pinned "
+                      f"> 80 % of MemAvailable {avail / 1e9:.1f} GB")
+        else:
+            if numa:
+                numa = gpu_local_cpus(torch, dist.local)
+            try:
+                hg = torch.empty(total, dtype=gdt, pin_memory=True)
+                hr = torch.empty(total, dtype=torch.bfloat16, pin_memory=True)
+                pinned = True
+            except RuntimeError as exc:  # pinned host memory exhausted
+                hg = hr = None
+                pinned = str(exc).splitlines()[0][:200]
+            finally:  # (the pages stay where they were allocated)
+                os.sched_setaffinity(0, saved_cpus)
         flags = dist.gather(pinned)
         if any(f is not True for f in flags):
             e2e_skip = next(f for f in flags if f is not True)
