@@ -70,6 +70,13 @@ constexpr uint32_t smem_bytes() {
          epi_stage_bytes<MODE>() + 256;
 }
 constexpr int kRasterGroup = 8;
+// Tile rows per raster group: UPDATE sweeps 16 (a 4096-row iterate's X column
+// panels are then read once, not twice: -0.9 % on the N=1 step, profiles/
+// r02_update_raster16_ab.json); the other modes keep 8.
+#ifndef OSH_UPDATE_RASTER
+#define OSH_UPDATE_RASTER 16
+#endif
+inline int raster_group(int mode) { return mode == kEpiUpdate ? OSH_UPDATE_RASTER : kRasterGroup; }
 
 struct TileCoord {
   int p, b, tm, tn;
@@ -98,11 +105,12 @@ __device__ __forceinline__ TileCoord decode_tile(const NsGemmParams& P, int t) {
     c.tn = tn;
     return c;
   }
-  // grouped rasterisation: kRasterGroup tile-rows sweep one column panel
-  const int span = kRasterGroup * pr.tiles_n;
+  // grouped rasterisation: P.raster tile-rows sweep one column panel
+  const int rg = P.raster;
+  const int span = rg * pr.tiles_n;
   const int group = rem / span;
-  const int first_m = group * kRasterGroup;
-  const int gsz = min(pr.tiles_m - first_m, kRasterGroup);
+  const int first_m = group * rg;
+  const int gsz = min(pr.tiles_m - first_m, rg);
   const int r2 = rem - group * span;
   c.tm = first_m + r2 % gsz;
   c.tn = r2 / gsz;
@@ -1067,8 +1075,9 @@ int ns_gemm_stream_k_schedule(const NsProblemDesc* probs, int num_problems,
             ts.push_back({i, b, tm, tn, nkb});
       } else {  // grouped rasterisation (decode_tile)
         for (int rem = 0; rem < tmn * tnn; ++rem) {
-          const int span = kRasterGroup * tnn, group = rem / span, first_m = group * kRasterGroup;
-          const int gsz = std::min(tmn - first_m, kRasterGroup), r2 = rem - group * span;
+          const int rg = kRasterGroup;  // (stream-K: GRAM only)
+          const int span = rg * tnn, group = rem / span, first_m = group * rg;
+          const int gsz = std::min(tmn - first_m, rg), r2 = rem - group * span;
           ts.push_back({i, b, first_m + r2 % gsz, r2 / gsz, nkb});
         }
       }
@@ -1261,6 +1270,7 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     if (mode == kEpiSplit && d.out_seg < pr.N) return cudaErrorInvalidValue;
   }
   P.total_tiles = tiles;
+  P.raster = raster_group(mode);
   bool stream_k = false;
   if (sched != nullptr && sched->tiles != nullptr && sched->total_tiles == tiles &&
       sched->units == std::min(tiles, cg == 2 ? sm_count() / 2 : sm_count())) {

@@ -93,6 +93,7 @@ struct NsGemmParams {
   const int* sched;      // optional: tiles of unit u are sched[sched_off[u] .. sched_off[u+1])
   const int* sched_off;
   int sched_units;       // units (clusters / CTAs) the schedule was built for
+  int raster;            // tile rows per raster group (non-symmetric problems)
   // stream-K (kEpiGram only, with a schedule): entry i covers k-blocks
   // [seg_kb[i].x, seg_kb[i].y) of its tile; seg_slot[i] >= 0 means a PART of
   // the tile, whose raw fp32 accumulator goes to seg_ws slot seg_slot[i]
