@@ -76,7 +76,12 @@ constexpr int kRasterGroup = 8;
 #ifndef OSH_UPDATE_RASTER
 #define OSH_UPDATE_RASTER 16
 #endif
-inline int raster_group(int mode) { return mode == kEpiUpdate ? OSH_UPDATE_RASTER : kRasterGroup; }
+#ifndef OSH_FINAL_RASTER
+#define OSH_FINAL_RASTER 8
+#endif
+inline int raster_group(int mode) {
+  return mode == kEpiUpdate ? OSH_UPDATE_RASTER : mode == kEpiFinal ? OSH_FINAL_RASTER : kRasterGroup;
+}
 
 struct TileCoord {
   int p, b, tm, tn;
