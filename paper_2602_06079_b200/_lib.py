@@ -91,7 +91,7 @@ class GemmProblem(ctypes.Structure):
     _fields_ = [("a", MatrixRef), ("b", MatrixRef), ("b_mn_major", c_int32),
                 ("reserved_", c_int32), ("out", MatrixRef), ("aux", MatrixRef),
                 ("scale", c_void_p), ("final_targets", c_void_p), ("symmetric", c_int32),
-                ("out_seg", c_int32)]
+                ("out_seg", c_int32), ("a_upper", c_int32), ("b_upper", c_int32)]
 
 
 class CollOp(ctypes.Structure):

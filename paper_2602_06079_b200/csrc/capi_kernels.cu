@@ -96,6 +96,8 @@ extern "C" osh_status osh_ns_gemm(int32_t epilogue, const osh_gemm_problem* prob
     d[i].final_targets = d_ft != nullptr ? d_ft + first[static_cast<size_t>(i)] : nullptr;
     d[i].symmetric = p.symmetric;
     d[i].out_seg = p.out_seg;
+    d[i].a_upper = p.a_upper;
+    d[i].b_upper = p.b_upper;
   }
   cudaError_t e = osh::ns_gemm_launch(epilogue, d, n_problems, alpha, beta, lr, st);
   for (int i = 0; i < n_problems && e == cudaSuccess && epilogue == OSH_EPI_FINAL; ++i) {

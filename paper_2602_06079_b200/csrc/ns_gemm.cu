@@ -526,14 +526,25 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // the leader's full barrier counts the bytes of both CTAs of the pair
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
-          load(smem_a + stage * kStageBytesA, &pr.tmA, kb * kNsBK, a_row, c.b);
-          uint8_t* sb = smem_b + stage * kStageBytesB;
-          if (!pr.b_mn_major) {
-            load(sb, &pr.tmB, kb * kNsBK, b_row, c.b);
+          // upper-tile operands: k-blocks left of the diagonal tile come from
+          // the mirrored tile through the MN-major view
+          const int kt = kb * kNsBK / kNsBN;
+          uint8_t* sa = smem_a + stage * kStageBytesA;
+          if (pr.a_upper && kt < c.tm) {
+#pragma unroll
+            for (int q = 0; q < static_cast<int>(C::kRowsA) / 64; ++q)
+              load(sa + q * 8192, &pr.tmA2, a_row + q * 64, kb * kNsBK, c.b);
           } else {
+            load(sa, &pr.tmA, kb * kNsBK, a_row, c.b);
+          }
+          uint8_t* sb = smem_b + stage * kStageBytesB;
+          if (pr.b_mn_major || (pr.b_upper && kt < c.tn)) {
+            const CUtensorMap* mb = pr.b_mn_major ? &pr.tmB : &pr.tmB2;
 #pragma unroll
             for (int q = 0; q < static_cast<int>(C::kRowsB) / 64; ++q)
-              load(sb + q * 8192, &pr.tmB, b_row + q * 64, kb * kNsBK, c.b);
+              load(sb + q * 8192, mb, b_row + q * 64, kb * kNsBK, c.b);
+          } else {
+            load(sb, &pr.tmB, kb * kNsBK, b_row, c.b);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -547,6 +558,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     if (lane == 0 && rank == 0) {
       const uint32_t idesc_k = idesc_bf16_f32(C::kTileM, kNsBN, false, false);
       const uint32_t idesc_mn = idesc_bf16_f32(C::kTileM, kNsBN, false, true);
+      const uint32_t idesc_ak = idesc_bf16_f32(C::kTileM, kNsBN, true, false);
+      const uint32_t idesc_amn = idesc_bf16_f32(C::kTileM, kNsBN, true, true);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       for (int it = it_begin; it < it_end; it += it_step) {
         const int t = sched ? __ldg(P.sched + it) : it;
@@ -567,15 +580,20 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
           const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
+          const int kt = kb * kNsBK / kNsBN;
+          const bool amn = pr.a_upper && kt < c.tm;               // (as the producer)
+          const bool bmn = mn || (pr.b_upper && kt < c.tn);
+          const uint32_t idesc = amn ? (bmn ? idesc_amn : idesc_ak) : (bmn ? idesc_mn : idesc_k);
 #pragma unroll
           for (int k = 0; k < kNsBK / 16; ++k) {
-            const uint64_t adesc = smem_desc_sw128(a0 + k * 32, 16, 1024);
-            const uint64_t bdesc = mn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
-                                      : smem_desc_sw128(b0 + k * 32, 16, 1024);
+            const uint64_t adesc = amn ? smem_desc_sw128(a0 + k * 2048, 8192, 1024)
+                                       : smem_desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bdesc = bmn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
+                                       : smem_desc_sw128(b0 + k * 32, 16, 1024);
             if constexpr (CG == 2)
-              umma_bf16_cg2(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
+              umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
             else
-              umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
+              umma_bf16(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
           }
           if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
           else umma_commit(&empty_bar[stage]);
@@ -686,9 +704,9 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         if constexpr (MODE == kEpiGram) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = s * __uint_as_float(r[j]);
-          if (pr.symmetric)
+          if (pr.symmetric && !(pr.symmetric == 3 && c.tn != c.tm))
             store_row32_sym(pr.out + c.b * pr.out_bstride, pr.out_ld, row, col0, pr.N, v);
-          else
+          else  // (upper-tile form: an off-diagonal tile is stored as computed)
             store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
         } else if constexpr (MODE == kEpiPoly) {
           if (ax_cur_ok) {
@@ -716,7 +734,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             for (int j = 0; j < 32; ++j)
               if (col0 + j == row) v[j] += P.lr;
           }
-          if (pr.symmetric)
+          if (pr.symmetric && !(pr.symmetric == 3 && c.tn != c.tm))
             store_row32_sym(pr.out + c.b * pr.out_bstride, pr.out_ld, row, col0, pr.N, v);
           else
             store_row32(pr.out + c.b * pr.out_bstride + row * pr.out_ld + col0, col0, pr.N, v);
@@ -867,7 +885,8 @@ __global__ void __launch_bounds__(256) stream_k_fixup_kernel(const __grid_consta
       out[row * pr.out_ld + col] = v;
     } else {
       if (col >= row) out[row * pr.out_ld + col] = v;
-      if (col > row) out[static_cast<long long>(col) * pr.out_ld + row] = v;
+      if (col > row && (pr.symmetric != 3 || tm == tn))  // (upper-tile form: diagonal tiles only)
+        out[static_cast<long long>(col) * pr.out_ld + row] = v;
     }
   }
 }
@@ -1238,13 +1257,22 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     } else {
       if (!make_map(&pr.tmB, d.b, 64, kNsBK)) return cudaErrorInvalidValue;
     }
+    // upper-tile form: 2-CTA (256 x 256) tiles only; 1-CTA launches read and
+    // write full matrices instead (same values)
+    pr.a_upper = cg == 2 && d.a_upper ? 1 : 0;
+    pr.b_upper = cg == 2 && d.b_upper ? 1 : 0;
+    if ((pr.a_upper && pr.M != pr.K) || (pr.b_upper && (d.b_mn_major || pr.N != pr.K)))
+      return cudaErrorInvalidValue;
+    if (pr.a_upper && !make_map(&pr.tmA2, d.a, 64, kNsBK)) return cudaErrorInvalidValue;
+    if (pr.b_upper && !make_map(&pr.tmB2, d.b, 64, kNsBK)) return cudaErrorInvalidValue;
     pr.tiles_m = (pr.M + P.tile_m - 1) / P.tile_m;
     pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
     pr.symmetric = d.symmetric && pr.M == pr.N &&
                            (mode == kEpiGram || mode == kEpiPoly || mode == kEpiStat ||
                             mode == kEpiSplit)
-                       ? (d.symmetric == 2 ? 2 : 1)
+                       ? (d.symmetric == 2 ? 2 : (d.symmetric == 3 && cg == 2 ? 3 : 1))
                        : 0;
+    if (pr.symmetric == 3 && mode != kEpiGram && mode != kEpiPoly) return cudaErrorInvalidValue;
     if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
     if (pr.symmetric == 2 && mode != kEpiStat) return cudaErrorInvalidValue;  // upper-only: STAT
     pr.tiles_per_batch =

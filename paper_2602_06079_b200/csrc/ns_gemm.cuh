@@ -68,8 +68,11 @@ int final_partials(int M, int N);  // tiles * CTAs per tile * 4 epilogue warps
 struct alignas(64) NsGemmProblem {
   CUtensorMap tmA;  // [batch][M][K], K-major, box {64, 128, 1}
   CUtensorMap tmB;  // K-major: [batch][N][K] box {64, 256, 1}; MN-major: [batch][K][N] box {64, 64, 1}
+  CUtensorMap tmA2;  // a_upper: the same square matrix as MN-major [batch][K][M] boxes {64, 64, 1}
+  CUtensorMap tmB2;  // b_upper: likewise for B
   int batch, M, N, K;
   int b_mn_major;
+  int a_upper, b_upper;  // operands in the upper-tile form (NsProblemDesc)
   int symmetric;      // output is symmetric (M == N): only tiles touching the
                       // upper triangle run; 1: the epilogue mirrors them,
                       // 2 (STAT): it writes the upper triangle only
@@ -125,6 +128,14 @@ struct NsProblemDesc {
                         // 1: the epilogue mirrors them, 2 (STAT): upper triangle written
                         // only — launch_sym_fill_lower completes the matrix before a reader
   long long out_seg = 0;  // kEpiSplit segment width (elements)
+  // Upper-tile form (2-CTA tiles only; 1-CTA launches fall back to the full
+  // mirror): symmetric = 3 (GRAM / POLY) writes the 256 x 256 tiles on and
+  // above the diagonal — diagonal tiles whole — and skips the mirror of the
+  // others; an operand flagged a_upper / b_upper is such a matrix, its
+  // k-blocks left of the diagonal are loaded from the mirrored upper tile
+  // through an MN-major view (same values, no lower half needed).
+  int a_upper = 0;
+  int b_upper = 0;
 };
 
 // A cost-balanced static tile schedule for one grouped launch (device arrays).

@@ -348,3 +348,54 @@ def test_poly_diagonal_add():
         af = a.float()
         ref = B * af + C * af @ af + A * torch.eye(256, device="cuda")
         assert relerr(out, ref) < 1e-2
+
+
+@pytest.mark.parametrize("batch,m,n", [(2, 512, 768), (1, 1024, 3072), (3, 300, 328)])
+def test_upper_tile_form_chain(batch, m, n, cta_group):
+    """GRAM and POLY in the upper-tile form (symmetric = 3: no mirror of the
+    off-diagonal tiles) feeding POLY / UPDATE that read the left-of-diagonal
+    k-blocks from the mirrored tiles (a_upper / b_upper): the chain equals the
+    fully mirrored chain bit for bit, and the torch fp32 reference within
+    the bf16 tolerance. (1-CTA launches fall back to full matrices.)"""
+    x = padded(batch, m, n, n + (-n) % 8, scale=0.02)
+
+    ldm = m + (-m) % 8  # 16-byte row pitch (TMA)
+
+    def chain(upper):
+        a = torch.zeros(batch, m, ldm, device="cuda", dtype=torch.bfloat16)
+        b = torch.zeros_like(a)
+        xo = torch.zeros_like(x)
+        g = _lib.GemmProblem()
+        g.a = mref(x, cols=n)
+        g.b = mref(x, cols=n)
+        g.out = mref(a, cols=m)
+        g.symmetric = 3 if upper else 1
+        run(0, [g])
+        p = _lib.GemmProblem()
+        p.a = mref(a, cols=m)
+        p.b = mref(a, cols=m)
+        p.out = mref(b, cols=m)
+        p.aux = mref(a, cols=m)
+        p.symmetric = 3 if upper else 1
+        p.a_upper = p.b_upper = int(upper)
+        run(1, [p], alpha=B, beta=C, lr=A)
+        u = _lib.GemmProblem()
+        u.a = mref(b, cols=m)
+        u.b = mref(x, cols=n)
+        u.b_mn_major = 1
+        u.out = mref(xo, cols=n)
+        u.a_upper = int(upper)
+        run(2, [u], alpha=0.0)
+        return a, b, xo
+
+    a1, b1, x1 = chain(False)
+    a3, b3, x3 = chain(True)
+    a1, b1, a3, b3 = (t[:, :, :m] for t in (a1, b1, a3, b3))
+    up = torch.ones(m, m, device="cuda", dtype=torch.bool).triu()
+    assert torch.equal(a3[:, up], a1[:, up]) and torch.equal(b3[:, up], b1[:, up])
+    assert torch.equal(x3[:, :, :n], x1[:, :, :n])
+    xf = x[:, :, :n].float()
+    af = xf @ xf.transpose(1, 2)
+    bf = A * torch.eye(m, device="cuda") + B * af + C * (af @ af)
+    ref = bf @ xf
+    assert relerr(x3[:, :, :n], ref) < 2e-2
