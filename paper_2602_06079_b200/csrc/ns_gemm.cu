@@ -528,23 +528,29 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
           // upper-tile operands: k-blocks left of the diagonal tile come from
           // the mirrored tile through the MN-major view
-          const int kt = kb * kNsBK / kNsBN;
+          const int kv = kb * kNsBK, sgi = kv / pr.k_seg, cc = kv - sgi * pr.k_seg;
+          const int kt = cc / kNsBN;  // the k-block's tile column inside its segment
           uint8_t* sa = smem_a + stage * kStageBytesA;
           if (pr.a_upper && kt < c.tm) {
+            const int col = (sgi + pr.a_seg0) * pr.k_seg + a_row;
 #pragma unroll
             for (int q = 0; q < static_cast<int>(C::kRowsA) / 64; ++q)
-              load(sa + q * 8192, &pr.tmA2, a_row + q * 64, kb * kNsBK, c.b);
+              load(sa + q * 8192, &pr.tmA2, col + q * 64, cc, c.b);
           } else {
-            load(sa, &pr.tmA, kb * kNsBK, a_row, c.b);
+            load(sa, &pr.tmA, kv, a_row, c.b);
           }
           uint8_t* sb = smem_b + stage * kStageBytesB;
-          if (pr.b_mn_major || (pr.b_upper && kt < c.tn)) {
-            const CUtensorMap* mb = pr.b_mn_major ? &pr.tmB : &pr.tmB2;
+          if (pr.b_mn_major) {
 #pragma unroll
             for (int q = 0; q < static_cast<int>(C::kRowsB) / 64; ++q)
-              load(sb + q * 8192, mb, b_row + q * 64, kb * kNsBK, c.b);
+              load(sb + q * 8192, &pr.tmB, b_row + q * 64, kv, c.b);
+          } else if (pr.b_upper && kt < c.tn) {
+            const int col = (sgi + pr.b_seg0) * pr.k_seg + b_row;
+#pragma unroll
+            for (int q = 0; q < static_cast<int>(C::kRowsB) / 64; ++q)
+              load(sb + q * 8192, &pr.tmB2, col + q * 64, cc, c.b);
           } else {
-            load(sb, &pr.tmB, kb * kNsBK, b_row, c.b);
+            load(sb, &pr.tmB, kv, b_row, c.b);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -580,7 +586,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
           const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
-          const int kt = kb * kNsBK / kNsBN;
+          const int kv = kb * kNsBK;
+          const int kt = (kv - (kv / pr.k_seg) * pr.k_seg) / kNsBN;
           const bool amn = pr.a_upper && kt < c.tm;               // (as the producer)
           const bool bmn = mn || (pr.b_upper && kt < c.tn);
           const uint32_t idesc = amn ? (bmn ? idesc_amn : idesc_ak) : (bmn ? idesc_mn : idesc_k);
@@ -786,7 +793,8 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           __nv_bfloat16* o = pr.out + c.b * pr.out_bstride;
           const long long sg = pr.out_seg;
           const int rblk = row_base + quarter * 32;  // this warp's 32 rows (32-aligned)
-          if (pr.symmetric && col0 >= rblk + 32 && rblk + 32 <= pr.M && col0 + 32 <= pr.N &&
+          const bool mirror = pr.symmetric == 1 || (pr.symmetric == 3 && c.tn == c.tm);
+          if (mirror && col0 >= rblk + 32 && rblk + 32 <= pr.M && col0 + 32 <= pr.N &&
               (pr.out_ld & 7) == 0 && (sg & 7) == 0 &&
               (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
             // whole chunk above this warp's diagonal: rows leave as 16 B
@@ -820,7 +828,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
               m2[q] = hv;
               m3[q] = hv;
             }
-          } else if (pr.symmetric) {
+          } else if (mirror) {
             store_row32_sym(o, pr.out_ld, row, col0, pr.N, v);
             store_row32_sym(o + sg, pr.out_ld, row, col0, pr.N, lo);
             store_row32_sym(o + 2 * sg, pr.out_ld, row, col0, pr.N, v);
@@ -1261,10 +1269,24 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
     // write full matrices instead (same values)
     pr.a_upper = cg == 2 && d.a_upper ? 1 : 0;
     pr.b_upper = cg == 2 && d.b_upper ? 1 : 0;
-    if ((pr.a_upper && pr.M != pr.K) || (pr.b_upper && (d.b_mn_major || pr.N != pr.K)))
-      return cudaErrorInvalidValue;
-    if (pr.a_upper && !make_map(&pr.tmA2, d.a, 64, kNsBK)) return cudaErrorInvalidValue;
-    if (pr.b_upper && !make_map(&pr.tmB2, d.b, 64, kNsBK)) return cudaErrorInvalidValue;
+    pr.k_seg = d.k_seg > 0 ? d.k_seg : pr.K;
+    pr.a_seg0 = d.k_seg > 0 ? d.a_seg0 : 0;
+    pr.b_seg0 = d.k_seg > 0 ? d.b_seg0 : 0;
+    if ((pr.a_upper || pr.b_upper) && (pr.k_seg % kNsBK != 0 && pr.k_seg != pr.K))
+      return cudaErrorInvalidValue;  // a k-block never straddles two segments
+    if ((pr.a_upper && pr.M > pr.k_seg) || (pr.b_upper && (d.b_mn_major || pr.N > pr.k_seg)))
+      return cudaErrorInvalidValue;  // each segment holds a square (padded) matrix
+    // the MN-major mirror views span the whole segmented buffer of the operand
+    const auto whole = [&](const NsMatrixRef& v, int seg0) {
+      NsMatrixRef w = v;
+      if (d.k_seg > 0) {
+        w.ptr = static_cast<const __nv_bfloat16*>(v.ptr) - static_cast<long long>(seg0) * d.k_seg;
+        w.cols = static_cast<int>(v.ld);
+      }
+      return w;
+    };
+    if (pr.a_upper && !make_map(&pr.tmA2, whole(d.a, pr.a_seg0), 64, kNsBK)) return cudaErrorInvalidValue;
+    if (pr.b_upper && !make_map(&pr.tmB2, whole(d.b, pr.b_seg0), 64, kNsBK)) return cudaErrorInvalidValue;
     pr.tiles_m = (pr.M + P.tile_m - 1) / P.tile_m;
     pr.tiles_n = (pr.N + kNsBN - 1) / kNsBN;
     pr.symmetric = d.symmetric && pr.M == pr.N &&
@@ -1272,7 +1294,8 @@ cudaError_t ns_gemm_launch(int mode, const NsProblemDesc* probs, int num_problem
                             mode == kEpiSplit)
                        ? (d.symmetric == 2 ? 2 : (d.symmetric == 3 && cg == 2 ? 3 : 1))
                        : 0;
-    if (pr.symmetric == 3 && mode != kEpiGram && mode != kEpiPoly) return cudaErrorInvalidValue;
+    if (pr.symmetric == 3 && mode != kEpiGram && mode != kEpiPoly && mode != kEpiSplit)
+      return cudaErrorInvalidValue;
     if (d.symmetric && !pr.symmetric) return cudaErrorInvalidValue;
     if (pr.symmetric == 2 && mode != kEpiStat) return cudaErrorInvalidValue;  // upper-only: STAT
     pr.tiles_per_batch =

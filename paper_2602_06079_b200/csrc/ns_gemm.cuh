@@ -73,6 +73,7 @@ struct alignas(64) NsGemmProblem {
   int batch, M, N, K;
   int b_mn_major;
   int a_upper, b_upper;  // operands in the upper-tile form (NsProblemDesc)
+  int k_seg, a_seg0, b_seg0;  // K segments of the upper-form views (k_seg = K: one)
   int symmetric;      // output is symmetric (M == N): only tiles touching the
                       // upper triangle run; 1: the epilogue mirrors them,
                       // 2 (STAT): it writes the upper triangle only
@@ -136,6 +137,12 @@ struct NsProblemDesc {
   // through an MN-major view (same values, no lower half needed).
   int a_upper = 0;
   int b_upper = 0;
+  // K in segments (kEpiSplit views): the operand rows hold consecutive
+  // segments of k_seg columns, each segment one symmetric matrix; the A / B
+  // view starts at stored segment a_seg0 / b_seg0 of that buffer. k_seg 0:
+  // one segment (K).
+  int k_seg = 0;
+  int a_seg0 = 0, b_seg0 = 0;
 };
 
 // A cost-balanced static tile schedule for one grouped launch (device arrays).

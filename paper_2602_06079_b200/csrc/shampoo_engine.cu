@@ -670,7 +670,17 @@ osh_status ShampooEngine::run_wave(int wi, const osh_muon_cfg& mcfg, cudaStream_
             d.b = split_ref(b, n, true);
             d.out = out_ref(o, n);
             d.out_seg = seg_of(n);
-            d.symmetric = 1;
+            // upper-tile form (ns_gemm.cuh): no mirror stores off the diagonal;
+            // the k-blocks left of it come from the mirrored tile of the same
+            // segment (A view = stored segments 0..2, B view = 1..3). Needs
+            // 64-wide segments (k-blocks inside one segment); ragged blocks
+            // keep the mirrored form (same values either way)
+            const bool upper = seg_of(n) % 64 == 0;
+            d.symmetric = upper ? 3 : 1;
+            d.a_upper = d.b_upper = upper ? 1 : 0;
+            d.k_seg = upper ? seg_of(n) : 0;
+            d.a_seg0 = 0;
+            d.b_seg0 = upper ? 1 : 0;
             return d;
           };
           // X' = X T and T2 = T T (both sides), then T4 = T2 T2, then M' = T4 M

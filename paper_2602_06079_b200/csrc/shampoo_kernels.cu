@@ -206,7 +206,11 @@ __global__ void __launch_bounds__(256) sh_extract_kernel(const ShNewtonTask* tas
     if (r >= T.n) continue;
     for (int j = 0; j < kTile / 32; ++j) {
       const int c = c0 + tx + 32 * j;
-      if (c < T.n) T.dst[static_cast<size_t>(r) * T.ldd + c] = T.src5[static_cast<size_t>(r) * T.ld5 + c];
+      // the Newton products are in the upper-tile form: (r, c) from the
+      // upper triangle, so P is exactly symmetric
+      if (c < T.n)
+        T.dst[static_cast<size_t>(r) * T.ldd + c] =
+            T.src5[static_cast<size_t>(min(r, c)) * T.ld5 + max(r, c)];
     }
   }
 }
