@@ -128,7 +128,7 @@ osh_status MuonEngine::build(const std::vector<MuonTensorDesc>& tensors, int gra
   const char* ff = std::getenv("OSH_FUSE_FINAL");
   fuse_final_ = !(ff != nullptr && std::strcmp(ff, "0") == 0);
   const char* uf = std::getenv("OSH_UPPER_FORM");
-  upper_form_ = !(uf != nullptr && std::strcmp(uf, "0") == 0);
+  upper_form_ = uf != nullptr && std::strcmp(uf, "1") == 0;  // opt-in (see problems())
   std::vector<char> fused_t(tensors.size(), 0);
   for (size_t i = 0; i < tensors.size(); ++i) {
     const MuonTensorDesc& t = tensors[i];
@@ -602,15 +602,19 @@ void MuonEngine::problems(const Wave& w, int it, NsProblemDesc* gram, NsProblemD
     const NsMatrixRef Xo = ref(xout, c.batch, c.m, c.n, c.ldn, xbs);
     const NsMatrixRef Am = ref(d_ws_ + c.a, c.batch, c.m, c.m, c.ldm, abs);
     const NsMatrixRef Bm = ref(d_ws_ + c.b, c.batch, c.m, c.m, c.ldm, abs);
-    // symmetric A = X X^T and B = b A + c A^2 in the upper-tile form (no
-    // lower-half stores; POLY and UPDATE read the left-of-diagonal k-blocks
-    // from the mirrored tiles), OSH_UPPER_FORM=0: full mirrored matrices
-    const int sym = symmetric_ ? (upper_form_ ? 3 : 1) : 0;
+    // OSH_UPPER_FORM=1 (opt-in): B = b A + c A^2 in the upper-tile form (no
+    // lower-half stores; UPDATE / FINAL read the left-of-diagonal k-blocks of
+    // B from the mirrored tiles). Measured against the mirrored step it is
+    // slower inside the step (UPDATE / FINAL with MN-major A k-blocks beside
+    // the momentum pass) though not in isolation, and POLY reading A through
+    // the mirror is 13 % slower in isolation (profiles/r02_upper_form_ab.json),
+    // so the Muon step keeps mirrored matrices by default; the Shampoo Newton
+    // products use the form (shampoo_engine.cu).
+    const int sym = symmetric_ ? 1 : 0;
     const int up = symmetric_ && upper_form_ ? 1 : 0;
     gram[q] = NsProblemDesc{X, X, 0, Am, NsMatrixRef{},
                             first ? d_scale_gram_ + c.slot0 : nullptr, nullptr, sym};
-    poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, sym};
-    poly[q].a_upper = poly[q].b_upper = up;
+    poly[q] = NsProblemDesc{Am, Am, 0, Bm, Am, nullptr, nullptr, up ? 3 : sym};
     upd[q] = NsProblemDesc{Bm, X, 1, Xo, X, first ? d_scale_update_ + c.slot0 : nullptr,
                            nullptr, 0};
     upd[q].a_upper = up;

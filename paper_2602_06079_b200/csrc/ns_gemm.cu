@@ -522,13 +522,38 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         }
         const int a_row = c.tm * C::kTileM + rank * C::kRowsA;
         const int b_row = c.tn * kNsBN + rank * C::kRowsB;
+        // operands in the upper-tile form need the per-k-block mirror choice;
+        // every other tile runs the plain loop (the choice costs issue slots)
+        const bool up = (pr.a_upper && c.tm > 0) || (pr.b_upper && c.tn > 0);
+        if (!up) {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            // the leader's full barrier counts the bytes of both CTAs of the pair
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
+            load(smem_a + stage * kStageBytesA, &pr.tmA, kb * kNsBK, a_row, c.b);
+            uint8_t* sb = smem_b + stage * kStageBytesB;
+            if (!pr.b_mn_major) {
+              load(sb, &pr.tmB, kb * kNsBK, b_row, c.b);
+            } else {
+#pragma unroll
+              for (int q = 0; q < static_cast<int>(C::kRowsB) / 64; ++q)
+                load(sb + q * 8192, &pr.tmB, b_row + q * 64, kb * kNsBK, c.b);
+            }
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          continue;
+        }
+        // upper-tile operands: k-blocks left of the diagonal tile come from
+        // the mirrored tile of the same K segment through the MN-major view
+        int sgi = kb0 * kNsBK / pr.k_seg;                // segment, and column inside it
+        int cc = kb0 * kNsBK - sgi * pr.k_seg;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          // the leader's full barrier counts the bytes of both CTAs of the pair
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * (kStageBytesA + kStageBytesB));
-          // upper-tile operands: k-blocks left of the diagonal tile come from
-          // the mirrored tile through the MN-major view
-          const int kv = kb * kNsBK, sgi = kv / pr.k_seg, cc = kv - sgi * pr.k_seg;
+          const int kv = kb * kNsBK;
           const int kt = cc / kNsBN;  // the k-block's tile column inside its segment
           uint8_t* sa = smem_a + stage * kStageBytesA;
           if (pr.a_upper && kt < c.tm) {
@@ -551,6 +576,10 @@ __global__ void __launch_bounds__(kNsThreads, 1)
               load(sb + q * 8192, &pr.tmB2, col + q * 64, cc, c.b);
           } else {
             load(sb, &pr.tmB, kv, b_row, c.b);
+          }
+          if ((cc += kNsBK) == pr.k_seg) {
+            cc = 0;
+            ++sgi;
           }
           if (++stage == kStages) {
             stage = 0;
@@ -581,32 +610,59 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kNsBN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
-          const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
-          const int kv = kb * kNsBK;
-          const int kt = (kv - (kv / pr.k_seg) * pr.k_seg) / kNsBN;
-          const bool amn = pr.a_upper && kt < c.tm;               // (as the producer)
-          const bool bmn = mn || (pr.b_upper && kt < c.tn);
-          const uint32_t idesc = amn ? (bmn ? idesc_amn : idesc_ak) : (bmn ? idesc_mn : idesc_k);
+        const bool up = (pr.a_upper && c.tm > 0) || (pr.b_upper && c.tn > 0);
+        if (!up) {  // (as the producer: the plain loop)
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
+            const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
 #pragma unroll
-          for (int k = 0; k < kNsBK / 16; ++k) {
-            const uint64_t adesc = amn ? smem_desc_sw128(a0 + k * 2048, 8192, 1024)
-                                       : smem_desc_sw128(a0 + k * 32, 16, 1024);
-            const uint64_t bdesc = bmn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
-                                       : smem_desc_sw128(b0 + k * 32, 16, 1024);
-            if constexpr (CG == 2)
-              umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
-            else
-              umma_bf16(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
+            for (int k = 0; k < kNsBK / 16; ++k) {
+              const uint64_t adesc = smem_desc_sw128(a0 + k * 32, 16, 1024);
+              const uint64_t bdesc = mn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
+                                        : smem_desc_sw128(b0 + k * 32, 16, 1024);
+              if constexpr (CG == 2)
+                umma_bf16_cg2(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
+              else
+                umma_bf16(d_tmem, adesc, bdesc, mn ? idesc_mn : idesc_k, (kb != kb0) || k != 0);
+            }
+            if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
+            else umma_commit(&empty_bar[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
-          else umma_commit(&empty_bar[stage]);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+        } else {
+          int cc = kb0 * kNsBK - (kb0 * kNsBK / pr.k_seg) * pr.k_seg;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem_a + stage * kStageBytesA);
+            const uint32_t b0 = smem_u32(smem_b + stage * kStageBytesB);
+            const int kt = cc / kNsBN;
+            const bool amn = pr.a_upper && kt < c.tm;               // (as the producer)
+            const bool bmn = mn || (pr.b_upper && kt < c.tn);
+            const uint32_t idesc = amn ? (bmn ? idesc_amn : idesc_ak) : (bmn ? idesc_mn : idesc_k);
+#pragma unroll
+            for (int k = 0; k < kNsBK / 16; ++k) {
+              const uint64_t adesc = amn ? smem_desc_sw128(a0 + k * 2048, 8192, 1024)
+                                         : smem_desc_sw128(a0 + k * 32, 16, 1024);
+              const uint64_t bdesc = bmn ? smem_desc_sw128(b0 + k * 2048, 8192, 1024)
+                                         : smem_desc_sw128(b0 + k * 32, 16, 1024);
+              if constexpr (CG == 2)
+                umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
+              else
+                umma_bf16(d_tmem, adesc, bdesc, idesc, (kb != kb0) || k != 0);
+            }
+            if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage], 0x3);
+            else umma_commit(&empty_bar[stage]);
+            if ((cc += kNsBK) == pr.k_seg) cc = 0;
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
         if constexpr (CG == 2) umma_commit_cg2_mc(&tfull_bar[acc], 0x3);

@@ -3,7 +3,7 @@
 #   OSH_LIB=ab/libosh_base.so vs the in-tree libosh.so, interleaved.
 mkdir -p gpurun_out/precond_ab
 for rep in 1 2; do
-  for opt in shampoo; do
+  for opt in shampoo soap; do
     for lib in base new; do
       if [ $lib = base ]; then export OSH_LIB=ab/libosh_base.so; else unset OSH_LIB; fi
       timeout 600 python bench.py --config configs/qwen3-1p7b-like.cfg --optimizer $opt --steps 6 --warmup 3 \
