@@ -181,7 +181,7 @@ typedef struct osh_gemm_problem {
   const osh_final_target* final_targets;
   int32_t symmetric;  /* GRAM / POLY / STAT / SPLIT with M == N: upper-triangle tiles, mirror;
                          2 (STAT only): upper triangle written, lower left untouched;
-                         3 (GRAM / POLY): upper-tile form — the 256 x 256 tiles on and above
+                         3 (GRAM / POLY / SPLIT): upper-tile form — the 256 x 256 tiles on and above
                          the diagonal (diagonal tiles whole), no mirror of the others */
   int32_t out_seg;    /* OSH_EPI_SPLIT: segment width in elements (>= N) */
   int32_t a_upper;    /* A (square) is in the upper-tile form: left-of-diagonal k-blocks are

@@ -130,7 +130,7 @@ class MuonEngine : public OptimizerEngine {
   bool stream_k_ = false;         // OSH_STREAM_K=1: tail-split GRAM for few long-K tiles
   float* d_sk_ws_ = nullptr;      // stream-K partial tiles (fp32, 256 x 256 per slot)
   bool symmetric_ = true;
-  bool upper_form_ = true;   // symmetric GEMM outputs in the upper-tile form (ns_gemm.cuh)
+  bool upper_form_ = false;  // POLY output in the upper-tile form (ns_gemm.cuh; OSH_UPPER_FORM=1)
   bool double_buffer_ = false;
   bool reorder_ = false;          // small waves first and last (set_wave_reorder)
   bool lpt_ = true;               // cost-balanced tile schedules (OSH_GEMM_LPT=0: striding)
