@@ -46,7 +46,10 @@ struct Cfg {
 };
 constexpr uint32_t kTmemCols = 512;
 // kEpiFinal staging per epilogue warp: kFinBufs 32x32 fp32 W boxes in flight
-constexpr int kFinBufs = 3;
+#ifndef OSH_FIN_BUFS
+#define OSH_FIN_BUFS 3
+#endif
+constexpr int kFinBufs = OSH_FIN_BUFS;
 constexpr uint32_t kFinWBox = 32 * 32 * 4;
 constexpr uint32_t kFinBytes = 4 * kFinBufs * kFinWBox;
 // kEpiSplit (symmetric): per epilogue warp, its 32 x 32 chunk as bf16 hi and
@@ -61,8 +64,8 @@ constexpr uint32_t epi_stage_bytes() {
 }
 template <int MODE, int CG>
 constexpr uint32_t smem_bytes();
-static_assert(1024 + 5 * (16384 + 16384) + 4 * 3 * 4096 + 256 <= 232448, "FINAL (2-CTA) exceeds smem");
-static_assert(1024 + 3 * (16384 + 32768) + 4 * 3 * 4096 + 256 <= 232448, "FINAL (1-CTA) exceeds smem");
+static_assert(1024 + 5 * (16384 + 16384) + 4 * kFinBufs * 4096 + 256 <= 232448, "FINAL (2-CTA) exceeds smem");
+static_assert(1024 + 3 * (16384 + 32768) + 4 * kFinBufs * 4096 + 256 <= 232448, "FINAL (1-CTA) exceeds smem");
 template <int MODE, int CG>
 constexpr uint32_t smem_bytes() {
   // [1 KiB align][stage ring][FINAL staging][barriers 256 B]
