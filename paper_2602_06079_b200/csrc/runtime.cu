@@ -667,8 +667,11 @@ osh_status osh_ctx_set_layout(osh_ctx* ctx, const osh_param_desc* params, int32_
   const char* so = std::getenv("OSH_SEQ_OVERLAP");
   ctx->seq_overlap = seq_path && overlap_on && ctx->optimizer == OSH_OPT_MUON &&
                      so != nullptr && std::strcmp(so, "1") == 0;
+  // (one rank: 16 waves measured 0.7-0.9 % faster than 8 on two boxes,
+  // NVLS N=4 neutral: profiles/r02_waves_ab.json)
   int min_waves = ctx->min_waves > 0 ? ctx->min_waves
-                  : ctx->overlap ? 8 : (reduce_out && ctx->tp_size == 1) ? 4 : 1;
+                  : ctx->overlap ? (distributed(ctx) ? 8 : 16)
+                  : (reduce_out && ctx->tp_size == 1) ? 4 : 1;
   if (const char* mw = std::getenv("OSH_MIN_WAVES"); mw != nullptr && std::atoi(mw) > 0)
     min_waves = std::atoi(mw);
   // waves in any order where nothing bucket-ordered waits on them: one rank,
